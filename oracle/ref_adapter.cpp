@@ -1,0 +1,461 @@
+// ref_adapter.cpp -- implements oracle/msplat_oracle.h on top of the
+// reference's own C++ sources (compiled unmodified from
+// /root/reference/proj/core/src with -Dmsplat=msplat_ref against
+// third_party/eigen_subset).  TEST INFRASTRUCTURE ONLY: it lets the pytest
+// parity suite and bench.py's reference arm call the real reference through a
+// flat C ABI.  Every entry point marshals the flat arrays into the reference's
+// AoS Eigen types, calls the reference function named in the comment, and
+// marshals back.
+#include "msplat_oracle.h"
+
+#include "msplat/normals.hpp"
+#include "msplat/rasterizer.hpp"
+#include "msplat/scene.hpp"
+#include "msplat/trainer.hpp"
+
+#include <chrono>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+using namespace msplat;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+
+Scene to_scene(const mo_scene* s) {
+    Scene sc;
+    sc.num_classes = s->num_classes;
+    sc.sh_degree = s->sh_degree;
+    const int K = sc.sh_coeff_count(), C = s->num_classes;
+    sc.gaussians.resize(size_t(s->n));
+    for (int64_t i = 0; i < s->n; ++i) {
+        auto& g = sc.gaussians[size_t(i)];
+        g.position = Vec3(s->means[3 * i], s->means[3 * i + 1], s->means[3 * i + 2]);
+        g.rotation = Vec4(s->quats[4 * i], s->quats[4 * i + 1], s->quats[4 * i + 2],
+                          s->quats[4 * i + 3]);
+        g.log_scale = Vec3(s->log_scales[3 * i], s->log_scales[3 * i + 1], s->log_scales[3 * i + 2]);
+        g.opacity_logit = s->opacity_logits[i];
+        g.sh = ShMatrix::Zero(3, K);
+        for (int c = 0; c < 3; ++c)
+            for (int j = 0; j < K; ++j)
+                g.sh(c, j) = s->sh[(i * 3 + c) * K + j];
+        g.semantic_logits = VecX::Zero(C);
+        for (int c = 0; c < C; ++c)
+            g.semantic_logits[c] = s->semantics[i * C + c];
+        g.gradient_factor = s->k[i];
+    }
+    return sc;
+}
+
+CameraView to_camera(const mo_camera* c) {
+    Mat3 R;
+    R << c->R_c2w[0], c->R_c2w[1], c->R_c2w[2], c->R_c2w[3], c->R_c2w[4], c->R_c2w[5],
+        c->R_c2w[6], c->R_c2w[7], c->R_c2w[8];
+    return make_camera(c->fx, c->fy, c->cx, c->cy, c->width, c->height, R,
+                       Vec3(c->t_c2w[0], c->t_c2w[1], c->t_c2w[2]));
+}
+
+RenderConfig to_cfg(const mo_render_cfg* c) {
+    RenderConfig rc;
+    rc.sigma_scale = c->sigma_scale;
+    rc.background = Vec3(c->background[0], c->background[1], c->background[2]);
+    rc.early_stop_transmittance = c->early_stop_transmittance;
+    rc.early_termination = c->early_termination != 0;
+    rc.threads = c->threads;
+    return rc;
+}
+
+NormalConfig to_ncfg(const mo_normal_cfg* c) {
+    NormalConfig nc;
+    nc.step1 = c->step1;
+    nc.step2 = c->step2;
+    nc.fuse_lambda = c->fuse_lambda;
+    nc.mask_threshold = c->mask_threshold;
+    return nc;
+}
+
+GridF grid_from(const double* p, int W, int H, int C) {
+    GridF g(W, H, C, 0.0);
+    std::memcpy(g.data(), p, sizeof(double) * size_t(W) * H * C);
+    return g;
+}
+
+void grid_to(const GridF& g, double* p) {
+    if (p)
+        std::memcpy(p, g.data(), sizeof(double) * g.size());
+}
+
+PixelGradients pix_from(int W, int H, int C, const double* dc, const double* dd, const double* ds,
+                        const double* dk) {
+    PixelGradients pg = PixelGradients::zero(W, H, C);
+    std::memcpy(pg.dcolor.data(), dc, sizeof(double) * pg.dcolor.size());
+    std::memcpy(pg.ddepth.data(), dd, sizeof(double) * pg.ddepth.size());
+    if (C)
+        std::memcpy(pg.dsemantics.data(), ds, sizeof(double) * pg.dsemantics.size());
+    std::memcpy(pg.dkmap.data(), dk, sizeof(double) * pg.dkmap.size());
+    return pg;
+}
+
+void grads_to(const GradientBuffer& b, int K, int C, mo_grads* o) {
+    for (size_t i = 0; i < b.size(); ++i) {
+        for (int j = 0; j < 3; ++j) {
+            o->dposition[3 * i + j] = b.dposition[i][j];
+            o->dscale[3 * i + j] = b.dscale[i][j];
+        }
+        for (int j = 0; j < 4; ++j)
+            o->drotation[4 * i + j] = b.drotation[i][j];
+        o->dopacity[i] = b.dopacity[i];
+        for (int c = 0; c < 3; ++c)
+            for (int j = 0; j < K; ++j)
+                o->dsh[(i * 3 + c) * K + j] = b.dsh[i](c, j);
+        for (int c = 0; c < C; ++c)
+            o->dsemantics[i * C + c] = b.dsemantics[i][c];
+        o->dk[i] = b.dk[i];
+    }
+}
+
+GradientBuffer grads_from(const mo_grads* g, const Scene& sc, bool raw) {
+    GradientBuffer b;
+    b.resize_zero(sc);
+    const int K = sc.sh_coeff_count(), C = sc.num_classes;
+    for (size_t i = 0; i < sc.size(); ++i) {
+        b.dposition[i] = Vec3(g->dposition[3 * i], g->dposition[3 * i + 1], g->dposition[3 * i + 2]);
+        b.drotation[i] = Vec4(g->drotation[4 * i], g->drotation[4 * i + 1], g->drotation[4 * i + 2],
+                              g->drotation[4 * i + 3]);
+        b.dscale[i] = Vec3(g->dscale[3 * i], g->dscale[3 * i + 1], g->dscale[3 * i + 2]);
+        b.dopacity[i] = g->dopacity[i];
+        for (int c = 0; c < 3; ++c)
+            for (int j = 0; j < K; ++j)
+                b.dsh[i](c, j) = g->dsh[(i * 3 + c) * K + j];
+        for (int c = 0; c < C; ++c)
+            b.dsemantics[i][c] = g->dsemantics[i * C + c];
+        b.dk[i] = g->dk[i];
+    }
+    b.raw_space = raw;
+    return b;
+}
+
+} // namespace
+
+extern "C" {
+
+const char* mo_last_error(void) { return g_err.c_str(); }
+const char* mo_impl_name(void) { return "reference"; }
+
+// activate_scene + project_gaussian + eval_sh_color as prepare_view does
+// (core/src/rasterizer.cpp:55-74).
+int mo_preprocess(const mo_scene* s, const mo_camera* cam, uint8_t* visible, double* center,
+                  double* cov, double* conic, double* sort_depth, double* radius, double* rgb,
+                  uint8_t* clamped) {
+    return guarded([&] {
+        const Scene sc = to_scene(s);
+        const CameraView view = to_camera(cam);
+        sc.validate();
+        const auto act = activate_scene(sc);
+        for (size_t i = 0; i < sc.size(); ++i) {
+            const auto sp = project_gaussian(act[i], view);
+            if (visible)
+                visible[i] = sp.has_value();
+            if (!sp)
+                continue;
+            if (center) {
+                center[2 * i] = sp->center.x();
+                center[2 * i + 1] = sp->center.y();
+            }
+            if (cov)
+                for (int r = 0; r < 2; ++r)
+                    for (int c = 0; c < 2; ++c)
+                        cov[4 * i + 2 * r + c] = sp->cov(r, c);
+            if (conic) {
+                conic[3 * i] = sp->conic(0, 0);
+                conic[3 * i + 1] = sp->conic(0, 1);
+                conic[3 * i + 2] = sp->conic(1, 1);
+            }
+            if (sort_depth)
+                sort_depth[i] = sp->sort_depth;
+            if (radius)
+                radius[i] = sp->radius;
+            const Vec3 to_g = act[i].position - view.t_cam_to_world;
+            const Scalar norm = to_g.norm();
+            const Vec3 dir = norm > 1e-12 ? Vec3(to_g / norm) : Vec3(0, 0, 1);
+            const ShColor col = eval_sh_color(*act[i].sh, sc.sh_degree, dir);
+            for (int c = 0; c < 3; ++c) {
+                if (rgb)
+                    rgb[3 * i + c] = col.rgb[c];
+                if (clamped)
+                    clamped[3 * i + c] = col.clamped[c];
+            }
+        }
+    });
+}
+
+// bin_and_sort (core/src/rasterizer.cpp:14-45)
+int64_t mo_bin(int64_t n, const uint8_t* visible, const double* center, const double* radius,
+               const double* sort_depth, int width, int height, int64_t* tile_offsets,
+               int32_t* values, int64_t capacity) {
+    int64_t count = 0;
+    const int st = guarded([&] {
+        std::vector<std::optional<Splat2D>> splats(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) {
+            if (!visible[i])
+                continue;
+            Splat2D sp;
+            sp.center = Vec2(center[2 * i], center[2 * i + 1]);
+            sp.radius = radius[i];
+            sp.sort_depth = sort_depth[i];
+            splats[size_t(i)] = sp;
+        }
+        const TileBins bins = bin_and_sort(splats, width, height);
+        int64_t off = 0;
+        for (size_t t = 0; t < bins.bins.size(); ++t) {
+            if (tile_offsets)
+                tile_offsets[t] = off;
+            off += int64_t(bins.bins[t].size());
+        }
+        if (tile_offsets)
+            tile_offsets[bins.bins.size()] = off;
+        count = off;
+        if (values && capacity >= count) {
+            int64_t k = 0;
+            for (const auto& b : bins.bins)
+                for (int v : b)
+                    values[k++] = v;
+        }
+    });
+    return st ? -st : count;
+}
+
+// rasterize (core/src/rasterizer.cpp:87-205)
+int mo_render(const mo_scene* s, const mo_camera* cam, const mo_render_cfg* cfg, double* color,
+              double* depth, double* semantics, double* kmap, double* transmittance,
+              int32_t* contributors, int32_t* terminus, double* weight_sums) {
+    return guarded([&] {
+        const Scene sc = to_scene(s);
+        ReplayState replay;
+        const MultimodalFrame f = rasterize(sc, to_camera(cam), to_cfg(cfg), &replay);
+        grid_to(f.color, color);
+        grid_to(f.depth, depth);
+        if (s->num_classes)
+            grid_to(f.semantics, semantics);
+        grid_to(f.kmap, kmap);
+        grid_to(f.transmittance, transmittance);
+        if (contributors)
+            std::memcpy(contributors, f.contributors.data(), sizeof(int) * f.contributors.size());
+        if (terminus)
+            std::memcpy(terminus, replay.terminus.data(), sizeof(int) * replay.terminus.size());
+        if (weight_sums)
+            for (size_t i = 0; i < sc.size(); ++i)
+                weight_sums[i] = replay.weight_sums[i];
+    });
+}
+
+// estimate_normals (core/src/normals.cpp:28-101)
+int mo_normals(const double* depth, const double* transmittance, const mo_camera* cam,
+               const mo_normal_cfg* ncfg, double* normals, uint8_t* valid, uint8_t* flipped) {
+    return guarded([&] {
+        const CameraView view = to_camera(cam);
+        const int W = view.width, H = view.height;
+        GridF nrm;
+        const NormalState st = estimate_normals(grid_from(depth, W, H, 1),
+                                                grid_from(transmittance, W, H, 1), view,
+                                                to_ncfg(ncfg), nrm);
+        grid_to(nrm, normals);
+        if (valid)
+            std::memcpy(valid, st.valid.data(), st.valid.size());
+        if (flipped)
+            std::memcpy(flipped, st.flipped.data(), st.flipped.size());
+    });
+}
+
+// normals_backward (core/src/normals.cpp:103-152)
+int mo_normals_backward(const double* dL_dnormals, const double* depth,
+                        const double* transmittance, const mo_camera* cam,
+                        const mo_normal_cfg* ncfg, double* dD) {
+    return guarded([&] {
+        const CameraView view = to_camera(cam);
+        const int W = view.width, H = view.height;
+        GridF nrm;
+        const NormalState st = estimate_normals(grid_from(depth, W, H, 1),
+                                                grid_from(transmittance, W, H, 1), view,
+                                                to_ncfg(ncfg), nrm);
+        grid_to(normals_backward(grid_from(dL_dnormals, W, H, 3), st, view), dD);
+    });
+}
+
+// rasterize + rasterize_backward (core/src/rasterizer_backward.cpp:127-264)
+int mo_backward(const mo_scene* s, const mo_camera* cam, const mo_render_cfg* cfg,
+                const double* dcolor, const double* ddepth, const double* dsemantics,
+                const double* dkmap, mo_grads* out) {
+    return guarded([&] {
+        const Scene sc = to_scene(s);
+        const CameraView view = to_camera(cam);
+        ReplayState replay;
+        const MultimodalFrame f = rasterize(sc, view, to_cfg(cfg), &replay);
+        const PixelGradients pg =
+            pix_from(view.width, view.height, sc.num_classes, dcolor, ddepth, dsemantics, dkmap);
+        const GradientBuffer g = rasterize_backward(sc, view, f, replay, pg);
+        grads_to(g, sc.sh_coeff_count(), sc.num_classes, out);
+    });
+}
+
+// chain_activations (core/src/scene.cpp:108-129)
+int mo_chain(const mo_scene* s, mo_grads* g) {
+    return guarded([&] {
+        const Scene sc = to_scene(s);
+        GradientBuffer b = grads_from(g, sc, false);
+        chain_activations(b, sc);
+        grads_to(b, sc.sh_coeff_count(), sc.num_classes, g);
+    });
+}
+
+// The benchmark unit, exactly the calls train() makes per iteration minus the
+// losses (trainer.cpp:295-309): rasterize, estimate_normals,
+// normals_backward merged into ddepth (seed 1), rasterize_backward,
+// chain_activations.  Marshalling is outside the timed stages.
+int mo_fwd_bwd(const mo_scene* s, const mo_camera* cam, const mo_render_cfg* cfg,
+               const mo_normal_cfg* ncfg, const double* dcolor, const double* ddepth,
+               const double* dsemantics, const double* dkmap, const double* dnormals,
+               double* color, double* depth, double* semantics, double* kmap,
+               double* transmittance, double* normals, mo_grads* out, double* ms_out) {
+    return guarded([&] {
+        using clk = std::chrono::steady_clock;
+        auto ms = [](clk::time_point a, clk::time_point b) {
+            return std::chrono::duration<double, std::milli>(b - a).count();
+        };
+        const Scene sc = to_scene(s);
+        const CameraView view = to_camera(cam);
+        const int W = view.width, H = view.height, C = sc.num_classes;
+        PixelGradients pg = pix_from(W, H, C, dcolor, ddepth, dsemantics, dkmap);
+        const GridF dN = grid_from(dnormals, W, H, 3);
+        const RenderConfig rc = to_cfg(cfg);
+        const NormalConfig nc = to_ncfg(ncfg);
+
+        const auto t0 = clk::now();
+        ReplayState replay;
+        MultimodalFrame f = rasterize(sc, view, rc, &replay);
+        const auto t1 = clk::now();
+        const NormalState nst = estimate_normals(f.depth, f.transmittance, view, nc, f.normals);
+        const auto t2 = clk::now();
+        const GridF dD = normals_backward(dN, nst, view);
+        for (size_t i = 0; i < pg.ddepth.size(); ++i)
+            pg.ddepth.storage()[i] += 1.0 * dD.storage()[i];
+        const auto t3 = clk::now();
+        GradientBuffer g = rasterize_backward(sc, view, f, replay, pg);
+        const auto t4 = clk::now();
+        chain_activations(g, sc);
+        const auto t5 = clk::now();
+        if (ms_out) {
+            ms_out[0] = ms(t0, t1);
+            ms_out[1] = ms(t1, t2);
+            ms_out[2] = ms(t2, t3);
+            ms_out[3] = ms(t3, t4);
+            ms_out[4] = ms(t4, t5);
+        }
+        grid_to(f.color, color);
+        grid_to(f.depth, depth);
+        if (C)
+            grid_to(f.semantics, semantics);
+        grid_to(f.kmap, kmap);
+        grid_to(f.transmittance, transmittance);
+        grid_to(f.normals, normals);
+        if (out)
+            grads_to(g, sc.sh_coeff_count(), C, out);
+    });
+}
+
+// adam_step (core/src/trainer.cpp:98-133)
+int mo_adam(int64_t n, int num_classes, int sh_degree, double* means, double* quats,
+            double* log_scales, double* opacity_logits, double* sh, double* semantics, double* k,
+            const mo_grads* g, mo_grads* m, mo_grads* v, int64_t step, const double* lr) {
+    return guarded([&] {
+        mo_scene s{n, num_classes, sh_degree, means, quats, log_scales, opacity_logits, sh,
+                   semantics, k};
+        Scene sc = to_scene(&s);
+        OptimizerState st;
+        st.m = grads_from(m, sc, true);
+        st.v = grads_from(v, sc, true);
+        st.step = step - 1;
+        TrainConfig tc;
+        tc.lr_position = lr[0];
+        tc.lr_rotation = lr[1];
+        tc.lr_scale = lr[2];
+        tc.lr_opacity = lr[3];
+        tc.lr_sh = lr[4];
+        tc.lr_semantics = lr[5];
+        tc.lr_k = lr[6];
+        adam_step(sc, grads_from(g, sc, true), st, tc);
+        const int K = sc.sh_coeff_count();
+        for (int64_t i = 0; i < n; ++i) {
+            const auto& p = sc.gaussians[size_t(i)];
+            for (int j = 0; j < 3; ++j) {
+                means[3 * i + j] = p.position[j];
+                log_scales[3 * i + j] = p.log_scale[j];
+            }
+            for (int j = 0; j < 4; ++j)
+                quats[4 * i + j] = p.rotation[j];
+            opacity_logits[i] = p.opacity_logit;
+            for (int c = 0; c < 3; ++c)
+                for (int j = 0; j < K; ++j)
+                    sh[(i * 3 + c) * K + j] = p.sh(c, j);
+            for (int c = 0; c < num_classes; ++c)
+                semantics[i * num_classes + c] = p.semantic_logits[c];
+            k[i] = p.gradient_factor;
+        }
+        grads_to(st.m, K, num_classes, m);
+        grads_to(st.v, K, num_classes, v);
+    });
+}
+
+// prune keep mask (core/src/trainer.cpp:135-147): run prune() on a scene whose
+// only payload is k, then recover which indices survived from the compaction.
+int64_t mo_prune_mask(int64_t n, const double* k, double threshold, int keep_small,
+                      uint8_t* keep) {
+    int64_t kept = 0;
+    const int st = guarded([&] {
+        Scene sc;
+        sc.sh_degree = 0;
+        sc.num_classes = 0;
+        sc.gaussians.resize(size_t(n));
+        for (int64_t i = 0; i < n; ++i) {
+            auto& g = sc.gaussians[size_t(i)];
+            g.sh = ShMatrix::Zero(3, 1);
+            g.semantic_logits = VecX::Zero(0);
+            g.gradient_factor = k[i];
+            g.opacity_logit = double(i); // tag to recover survivors
+        }
+        OptimizerState os = OptimizerState::init(sc);
+        TrainConfig tc;
+        tc.prune_threshold = threshold;
+        tc.prune_keep_small = keep_small != 0;
+        prune(sc, os, tc);
+        std::memset(keep, 0, size_t(n));
+        for (const auto& g : sc.gaussians)
+            keep[int64_t(g.opacity_logit)] = 1;
+        kept = int64_t(sc.size());
+    });
+    return st ? -st : kept;
+}
+
+} // extern "C"

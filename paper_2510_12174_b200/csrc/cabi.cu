@@ -1,0 +1,924 @@
+// C ABI (include/msplat_b200.h): context / replay lifetime, device buffer
+// management, precision dispatch and the error contract.  No kernels here.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/msplat_b200.h"
+#include "kernels.h"
+#include "radix_sort.cuh"
+
+using namespace msplat_cuda;
+
+namespace {
+
+thread_local std::string g_error;
+
+msplat_status set_error(msplat_status st, const std::string& msg) {
+    g_error = msg;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                         \
+    do {                                                                                       \
+        cudaError_t e_ = (expr);                                                               \
+        if (e_ != cudaSuccess)                                                                 \
+            return set_error(e_ == cudaErrorMemoryAllocation ? MSPLAT_ERR_OUT_OF_MEMORY        \
+                                                             : MSPLAT_ERR_CUDA,                \
+                             std::string("CUDA error: ") + cudaGetErrorString(e_) + " (" #expr ")"); \
+    } while (0)
+
+// Grow-only device allocation.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t want) {
+        if (want <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        size_t b = std::max<size_t>(want, 256);
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e == cudaSuccess) bytes = b;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+int64_t sh_coeffs(int deg) { return int64_t(deg + 1) * (deg + 1); }
+size_t real_size(int dtype) { return dtype == MSPLAT_F64 ? 8 : 4; }
+
+}  // namespace
+
+struct msplat_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    DeviceError* d_err = nullptr;
+    DeviceError* h_err = nullptr;  // pinned
+    unsigned long long* h_u64 = nullptr;  // pinned scratch
+    // scratch owned by the context (shared by calls on its stream)
+    DevBuf acc_dcolor, acc_dmean, acc_dconic, ddepth_total, normal_dv, kept;
+};
+
+struct msplat_replay {
+    msplat_context* ctx = nullptr;
+    bool valid = false;
+    int capture = 0;
+    int dtype = 0;
+    int64_t n = 0;
+    int C = 0, deg = 0, W = 0, H = 0, tiles_x = 0, tiles_y = 0;
+    Cam cam{};
+    RenderParams rp{};
+    int64_t inst_cap = 0;
+    bool binned_explicit = false;
+    DevBuf arec, brec, visible, clamped, depth_key, depth_key_alt, order, order_alt, tile_count, tile_rect,
+        count_sorted, offset_sorted, inst_tile, inst_tile_alt, inst_gauss, inst_gauss_alt, tile_range,
+        d_inst_count, d_inst_total32, hist, hist_scanned, scan_tiles, terminus, weight_sums, saved_means,
+        saved_k, cap_center, cap_conic, cap_depth, cap_radius, cap_rgb, visible_count;
+    uint32_t* sorted_gauss = nullptr;
+
+    void release_all() {
+        for (DevBuf* b : {&arec, &brec, &visible, &clamped, &depth_key, &depth_key_alt, &order, &order_alt,
+                          &tile_count, &tile_rect, &count_sorted, &offset_sorted, &inst_tile, &inst_tile_alt,
+                          &inst_gauss, &inst_gauss_alt, &tile_range, &d_inst_count, &d_inst_total32, &hist,
+                          &hist_scanned, &scan_tiles, &terminus, &weight_sums, &saved_means, &saved_k,
+                          &cap_center, &cap_conic, &cap_depth, &cap_radius, &cap_rgb, &visible_count})
+            b->release();
+    }
+};
+
+namespace {
+
+// CameraView::finalize (core/src/camera.cpp:8-21).
+msplat_status make_cam(const msplat_camera* c, Cam& o) {
+    if (!c) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "CameraView: null camera");
+    if (c->width < 1 || c->height < 1)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "CameraView: width and height must be >= 1");
+    if (!(c->fx > 0) || !(c->fy > 0))
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "CameraView: focal lengths must be positive");
+    const double* R = c->R_c2w;
+    double worst = 0;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = R[0 * 3 + i] * R[0 * 3 + j];
+            s += R[1 * 3 + i] * R[1 * 3 + j];
+            s += R[2 * 3 + i] * R[2 * 3 + j];
+            worst = std::max(worst, std::fabs(s - (i == j ? 1.0 : 0.0)));
+        }
+    if (worst > 1e-6)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "CameraView: rotation is not orthonormal (tol 1e-6)");
+    const double det = R[0] * (R[4] * R[8] - R[7] * R[5]) - R[3] * (R[1] * R[8] - R[7] * R[2]) +
+                       R[6] * (R[1] * R[5] - R[4] * R[2]);
+    if (std::fabs(det - 1.0) > 1e-6)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "CameraView: rotation determinant is not +1 (tol 1e-6)");
+    o.fx = c->fx;
+    o.fy = c->fy;
+    o.cx = c->cx;
+    o.cy = c->cy;
+    o.W = c->width;
+    o.H = c->height;
+    for (int i = 0; i < 9; ++i) o.Rc2w[i] = R[i];
+    for (int i = 0; i < 3; ++i) o.tc2w[i] = c->t_c2w[i];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) o.Rw2c[i * 3 + j] = R[j * 3 + i];
+    for (int i = 0; i < 3; ++i) {
+        double s = o.Rw2c[i * 3 + 0] * o.tc2w[0];
+        s += o.Rw2c[i * 3 + 1] * o.tc2w[1];
+        s += o.Rw2c[i * 3 + 2] * o.tc2w[2];
+        o.tw2c[i] = -s;
+    }
+    return MSPLAT_OK;
+}
+
+msplat_status check_scene(const msplat_scene* s) {
+    if (!s) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "Scene: null scene");
+    if (s->sh_degree < 0 || s->sh_degree > 3)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "Scene: sh_degree must be in [0,3]");
+    if (s->num_classes < 0) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "Scene: num_classes must be >= 0");
+    if (s->n < 0) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "Scene: negative size");
+    if (s->dtype != MSPLAT_F32 && s->dtype != MSPLAT_F64)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "Scene: dtype must be MSPLAT_F32 or MSPLAT_F64");
+    if (s->n > 0 && (!s->means || !s->quats || !s->log_scales || !s->opacity_logits || !s->k || !s->sh ||
+                     (s->num_classes > 0 && !s->semantics)))
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "Scene: null parameter array");
+    if (s->n >= (int64_t(1) << 31)) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "Scene: too many Gaussians");
+    return MSPLAT_OK;
+}
+
+// Reads (and clears) the latched device error.  Synchronizes the stream.
+msplat_status drain_device_error(msplat_context* ctx, int W) {
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(DeviceError), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    const DeviceError e = *ctx->h_err;
+    if (e.code == kErrNone) return MSPLAT_OK;
+    CUDA_TRY(cudaMemsetAsync(ctx->d_err, 0, sizeof(DeviceError), ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    char buf[256];
+    const int w = W > 0 ? W : 1;
+    switch (e.code) {
+        case kErrNonFiniteBlend:
+            snprintf(buf, sizeof buf, "rasterize: non-finite blend at pixel (%lld,%lld), primitive %lld",
+                     e.a % w, e.a / w, e.b);
+            return set_error(MSPLAT_ERR_RUNTIME, buf);
+        case kErrNonFiniteOutput:
+            snprintf(buf, sizeof buf, "rasterize: non-finite output at pixel (%lld,%lld)", e.a % w, e.a / w);
+            return set_error(MSPLAT_ERR_RUNTIME, buf);
+        case kErrSceneModified:
+            snprintf(buf, sizeof buf, "rasterize_backward: scene modified since forward (primitive %lld)", e.b);
+            return set_error(MSPLAT_ERR_RUNTIME, buf);
+        case kErrNonFiniteGrad:
+            snprintf(buf, sizeof buf, "rasterize_backward: non-finite gradient for primitive %lld", e.b);
+            return set_error(MSPLAT_ERR_RUNTIME, buf);
+        case kErrZeroQuat:
+            snprintf(buf, sizeof buf, "activate: primitive %lld has a zero quaternion", e.b);
+            return set_error(MSPLAT_ERR_INVALID_ARGUMENT, buf);
+        case kErrNonFiniteParam:
+            snprintf(buf, sizeof buf, "Scene: primitive %lld has non-finite fields", e.b);
+            return set_error(MSPLAT_ERR_INVALID_ARGUMENT, buf);
+        case kErrInstanceOverflow:
+            snprintf(buf, sizeof buf, "internal: tile-instance capacity %lld exceeded (needed %lld)", e.b, e.a);
+            return set_error(MSPLAT_ERR_RUNTIME, buf);
+        default:
+            snprintf(buf, sizeof buf, "device error %d", e.code);
+            return set_error(MSPLAT_ERR_RUNTIME, buf);
+    }
+}
+
+// Allocates per-Gaussian / per-pixel / per-tile replay storage for a view.
+msplat_status size_replay(msplat_replay* r, int dtype, int64_t n, int C, int deg, int W, int H) {
+    const size_t R = real_size(dtype);
+    r->dtype = dtype;
+    r->n = n;
+    r->C = C;
+    r->deg = deg;
+    r->W = W;
+    r->H = H;
+    r->tiles_x = (W + kTile - 1) / kTile;
+    r->tiles_y = (H + kTile - 1) / kTile;
+    const int64_t tiles = int64_t(r->tiles_x) * r->tiles_y;
+    const size_t nn = size_t(std::max<int64_t>(n, 1));
+    if (r->inst_cap == 0) r->inst_cap = std::max<int64_t>(int64_t(1) << 20, 4 * n);
+    CUDA_TRY(r->arec.ensure(nn * 8 * R));
+    CUDA_TRY(r->brec.ensure(nn * 32 * R));
+    CUDA_TRY(r->visible.ensure(nn));
+    CUDA_TRY(r->clamped.ensure(nn));
+    CUDA_TRY(r->depth_key.ensure(nn * 8));
+    CUDA_TRY(r->depth_key_alt.ensure(nn * 8));
+    CUDA_TRY(r->order.ensure(nn * 4));
+    CUDA_TRY(r->order_alt.ensure(nn * 4));
+    CUDA_TRY(r->tile_count.ensure(nn * 4));
+    CUDA_TRY(r->tile_rect.ensure(nn * 8));
+    CUDA_TRY(r->count_sorted.ensure(nn * 4));
+    CUDA_TRY(r->offset_sorted.ensure(nn * 4));
+    const size_t ic = size_t(r->inst_cap);
+    CUDA_TRY(r->inst_tile.ensure(ic * 4));
+    CUDA_TRY(r->inst_tile_alt.ensure(ic * 4));
+    CUDA_TRY(r->inst_gauss.ensure(ic * 4));
+    CUDA_TRY(r->inst_gauss_alt.ensure(ic * 4));
+    CUDA_TRY(r->tile_range.ensure(size_t(tiles) * 8));
+    CUDA_TRY(r->d_inst_count.ensure(8));
+    CUDA_TRY(r->d_inst_total32.ensure(4));
+    CUDA_TRY(r->visible_count.ensure(8));
+    const size_t hist = binning_scratch_elems(int64_t(nn), r->inst_cap);
+    CUDA_TRY(r->hist.ensure(hist * 4));
+    CUDA_TRY(r->hist_scanned.ensure(hist * 4));
+    const size_t scan_tiles = (std::max(hist, nn) + kScanTile - 1) / kScanTile + 1;
+    CUDA_TRY(r->scan_tiles.ensure(scan_tiles * 4));
+    CUDA_TRY(r->terminus.ensure(size_t(W) * H * 4));
+    CUDA_TRY(r->saved_means.ensure(nn * 3 * R));
+    CUDA_TRY(r->saved_k.ensure(nn * R));
+    if (r->capture & 1) {
+        CUDA_TRY(r->cap_center.ensure(nn * 2 * 8));
+        CUDA_TRY(r->cap_conic.ensure(nn * 3 * 8));
+        CUDA_TRY(r->cap_depth.ensure(nn * 8));
+        CUDA_TRY(r->cap_radius.ensure(nn * 8));
+        CUDA_TRY(r->cap_rgb.ensure(nn * 3 * 8));
+    }
+    if (r->capture & 2) CUDA_TRY(r->weight_sums.ensure(nn * R));
+    return MSPLAT_OK;
+}
+
+BinningBuffers binning_view(msplat_replay* r) {
+    BinningBuffers b{};
+    b.n = r->n;
+    b.tiles_x = r->tiles_x;
+    b.tiles_y = r->tiles_y;
+    b.inst_cap = r->inst_cap;
+    b.depth_key_bits = r->binned_explicit ? 64 : 63;
+    b.depth_key = r->depth_key.as<uint64_t>();
+    b.depth_key_alt = r->depth_key_alt.as<uint64_t>();
+    b.order = r->order.as<uint32_t>();
+    b.order_alt = r->order_alt.as<uint32_t>();
+    b.tile_count = r->tile_count.as<uint32_t>();
+    b.tile_rect = r->tile_rect.as<uint2>();
+    b.count_sorted = r->count_sorted.as<uint32_t>();
+    b.offset_sorted = r->offset_sorted.as<uint32_t>();
+    b.inst_tile = r->inst_tile.as<uint32_t>();
+    b.inst_tile_alt = r->inst_tile_alt.as<uint32_t>();
+    b.inst_gauss = r->inst_gauss.as<uint32_t>();
+    b.inst_gauss_alt = r->inst_gauss_alt.as<uint32_t>();
+    b.tile_range = r->tile_range.as<uint2>();
+    b.d_inst_count = r->d_inst_count.as<int64_t>();
+    b.d_inst_total32 = r->d_inst_total32.as<uint32_t>();
+    b.hist = r->hist.as<uint32_t>();
+    b.hist_scanned = r->hist_scanned.as<uint32_t>();
+    b.scan_tiles = r->scan_tiles.as<uint32_t>();
+    b.err = r->ctx->d_err;
+    return b;
+}
+
+// Binning with capacity management: if the device reports more instances
+// than the buffers hold, grow and redo.  When `sync` is false the capacity is
+// trusted (graph-capturable path) and an overflow surfaces as a latched error.
+msplat_status binning_with_capacity(msplat_replay* r, bool sync) {
+    msplat_context* ctx = r->ctx;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        BinningBuffers b = binning_view(r);
+        run_binning(b, ctx->stream);
+        r->sorted_gauss = b.sorted_gauss;
+        CUDA_TRY(cudaGetLastError());
+        if (!sync) return MSPLAT_OK;
+        CUDA_TRY(cudaMemcpyAsync(ctx->h_u64, b.d_inst_total32, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        const int64_t need = int64_t(*reinterpret_cast<uint32_t*>(ctx->h_u64));
+        if (need <= r->inst_cap) return MSPLAT_OK;
+        // clear the latched overflow, grow, retry
+        CUDA_TRY(cudaMemsetAsync(ctx->d_err, 0, sizeof(DeviceError), ctx->stream));
+        r->inst_cap = need + need / 4 + 1024;
+        msplat_status st = size_replay(r, r->dtype, r->n, r->C, r->deg, r->W, r->H);
+        if (st != MSPLAT_OK) return st;
+    }
+    return set_error(MSPLAT_ERR_RUNTIME, "internal: instance capacity did not converge");
+}
+
+template <typename Real>
+PreprocessArgs<Real> preprocess_args(msplat_replay* r, const msplat_scene* s, const msplat_render_config* cfg) {
+    PreprocessArgs<Real> a{};
+    a.n = s->n;
+    a.C = s->num_classes;
+    a.deg = s->sh_degree;
+    a.K = int(sh_coeffs(s->sh_degree));
+    a.means = static_cast<const Real*>(s->means);
+    a.quats = static_cast<const Real*>(s->quats);
+    a.log_scales = static_cast<const Real*>(s->log_scales);
+    a.opacity_logits = static_cast<const Real*>(s->opacity_logits);
+    a.k = static_cast<const Real*>(s->k);
+    a.sh = static_cast<const Real*>(s->sh);
+    a.semantics = static_cast<const Real*>(s->semantics);
+    a.cam = r->cam;
+    a.sigma = cfg->sigma_scale;
+    a.W = r->W;
+    a.H = r->H;
+    a.depth_key = r->depth_key.as<uint64_t>();
+    a.order = r->order.as<uint32_t>();
+    a.tile_count = r->tile_count.as<uint32_t>();
+    a.tile_rect = r->tile_rect.as<uint2>();
+    a.visible = r->visible.as<uint8_t>();
+    a.clamped_bits = r->clamped.as<uint8_t>();
+    a.arec = r->arec.as<AlphaRec<Real>>();
+    a.brec = r->brec.as<BlendRec<Real>>();
+    if (r->capture & 1) {
+        a.cap_center = r->cap_center.as<double>();
+        a.cap_conic = r->cap_conic.as<double>();
+        a.cap_depth = r->cap_depth.as<double>();
+        a.cap_radius = r->cap_radius.as<double>();
+        a.cap_rgb = r->cap_rgb.as<double>();
+    }
+    a.visible_count = r->visible_count.as<unsigned long long>();
+    a.err = r->ctx->d_err;
+    return a;
+}
+
+template <typename Real>
+msplat_status rasterize_impl(msplat_context* ctx, const msplat_scene* s, const msplat_render_config* cfg,
+                             const msplat_frame* f, msplat_replay* r, bool sync) {
+    const size_t R = sizeof(Real);
+    CUDA_TRY(cudaMemsetAsync(r->visible_count.p, 0, 8, ctx->stream));
+    launch_preprocess<Real>(preprocess_args<Real>(r, s, cfg), ctx->stream);
+    CUDA_TRY(cudaGetLastError());
+    r->binned_explicit = false;
+    msplat_status st = binning_with_capacity(r, sync);
+    if (st != MSPLAT_OK) return st;
+    // snapshot for check_replay (rasterizer_backward.cpp:40-44)
+    if (s->n > 0) {
+        CUDA_TRY(cudaMemcpyAsync(r->saved_means.p, s->means, size_t(s->n) * 3 * R, cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(r->saved_k.p, s->k, size_t(s->n) * R, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    if (r->capture & 2) CUDA_TRY(cudaMemsetAsync(r->weight_sums.p, 0, size_t(std::max<int64_t>(s->n, 1)) * R, ctx->stream));
+    ForwardArgs<Real> a{};
+    a.W = r->W;
+    a.H = r->H;
+    a.tiles_x = r->tiles_x;
+    a.C = s->num_classes;
+    a.cam = r->cam;
+    a.rp = r->rp;
+    a.tile_range = r->tile_range.as<uint2>();
+    a.inst_gauss = r->sorted_gauss;
+    a.arec = r->arec.as<AlphaRec<Real>>();
+    a.brec = r->brec.as<BlendRec<Real>>();
+    a.semantics = static_cast<const Real*>(s->semantics);
+    a.color = static_cast<Real*>(f->color);
+    a.depth = static_cast<Real*>(f->depth);
+    a.sem_out = static_cast<Real*>(f->semantics);
+    a.kmap = static_cast<Real*>(f->kmap);
+    a.T = static_cast<Real*>(f->transmittance);
+    a.contributors = f->contributors;
+    a.terminus = r->terminus.as<int32_t>();
+    a.weight_sums = (r->capture & 2) ? r->weight_sums.as<Real>() : nullptr;
+    a.err = ctx->d_err;
+    launch_forward<Real>(a, r->tiles_x * r->tiles_y, ctx->stream);
+    CUDA_TRY(cudaGetLastError());
+    r->valid = true;
+    return MSPLAT_OK;
+}
+
+template <typename Real>
+NormalArgs<Real> normal_args(const Cam& cam, const msplat_normal_config* n, const void* depth, const void* T) {
+    NormalArgs<Real> a{};
+    a.W = cam.W;
+    a.H = cam.H;
+    a.cam = cam;
+    a.step1 = n->step1;
+    a.step2 = n->step2;
+    a.lambda = n->fuse_lambda;
+    a.mask_threshold = n->mask_threshold;
+    a.depth = static_cast<const Real*>(depth);
+    a.T = static_cast<const Real*>(T);
+    return a;
+}
+
+msplat_status check_ncfg(const msplat_normal_config* n) {
+    if (!n) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "estimate_normals: null config");
+    if (n->step1 >= n->step2)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "estimate_normals: step1 must be smaller than step2");
+    if (n->fuse_lambda < 0 || n->fuse_lambda > 1)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "estimate_normals: fuse weight must be in [0,1]");
+    return MSPLAT_OK;
+}
+
+template <typename Real>
+msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const msplat_frame* f,
+                            const msplat_replay* r, const msplat_pixel_grads* pix, const void* ddepth,
+                            msplat_grads* g, int chain, int accumulate) {
+    const size_t R = sizeof(Real);
+    const int64_t n = s->n;
+    const int C = s->num_classes, K = int(sh_coeffs(s->sh_degree));
+    const size_t nn = size_t(std::max<int64_t>(n, 1));
+    CUDA_TRY(ctx->acc_dcolor.ensure(nn * 3 * R));
+    CUDA_TRY(ctx->acc_dmean.ensure(nn * 2 * R));
+    CUDA_TRY(ctx->acc_dconic.ensure(nn * 3 * R));
+    cudaStream_t st = ctx->stream;
+    CUDA_TRY(cudaMemsetAsync(ctx->acc_dcolor.p, 0, nn * 3 * R, st));
+    CUDA_TRY(cudaMemsetAsync(ctx->acc_dmean.p, 0, nn * 2 * R, st));
+    CUDA_TRY(cudaMemsetAsync(ctx->acc_dconic.p, 0, nn * 3 * R, st));
+    if (!accumulate && n > 0) {
+        CUDA_TRY(cudaMemsetAsync(g->dposition, 0, size_t(n) * 3 * R, st));
+        CUDA_TRY(cudaMemsetAsync(g->drotation, 0, size_t(n) * 4 * R, st));
+        CUDA_TRY(cudaMemsetAsync(g->dscale, 0, size_t(n) * 3 * R, st));
+        CUDA_TRY(cudaMemsetAsync(g->dopacity, 0, size_t(n) * R, st));
+        CUDA_TRY(cudaMemsetAsync(g->dk, 0, size_t(n) * R, st));
+        CUDA_TRY(cudaMemsetAsync(g->dsh, 0, size_t(n) * 3 * K * R, st));
+        if (C > 0) CUDA_TRY(cudaMemsetAsync(g->dsemantics, 0, size_t(n) * C * R, st));
+    }
+    launch_check_replay<Real>(n, static_cast<const Real*>(s->means), static_cast<const Real*>(s->k),
+                              r->saved_means.as<Real>(), r->saved_k.as<Real>(), ctx->d_err, st);
+    BackwardArgs<Real> a{};
+    a.W = r->W;
+    a.H = r->H;
+    a.tiles_x = r->tiles_x;
+    a.C = C;
+    a.n = n;
+    a.cam = r->cam;
+    a.rp = r->rp;
+    a.tile_range = r->tile_range.as<uint2>();
+    a.inst_gauss = r->sorted_gauss;
+    a.arec = r->arec.as<AlphaRec<Real>>();
+    a.brec = r->brec.as<BlendRec<Real>>();
+    a.semantics = static_cast<const Real*>(s->semantics);
+    a.T_final = static_cast<const Real*>(f->transmittance);
+    a.terminus = r->terminus.as<int32_t>();
+    a.dcolor = static_cast<const Real*>(pix->dcolor);
+    a.ddepth = static_cast<const Real*>(ddepth);
+    a.dsem = static_cast<const Real*>(pix->dsemantics);
+    a.dkmap = static_cast<const Real*>(pix->dkmap);
+    a.g_pos = static_cast<Real*>(g->dposition);
+    a.g_rot = static_cast<Real*>(g->drotation);
+    a.g_scale = static_cast<Real*>(g->dscale);
+    a.g_opac = static_cast<Real*>(g->dopacity);
+    a.g_k = static_cast<Real*>(g->dk);
+    a.g_sem = static_cast<Real*>(g->dsemantics);
+    a.acc_dcolor = ctx->acc_dcolor.as<Real>();
+    a.acc_dmean = ctx->acc_dmean.as<Real>();
+    a.acc_dconic = ctx->acc_dconic.as<Real>();
+    a.err = ctx->d_err;
+    launch_backward_blend<Real>(a, r->tiles_x * r->tiles_y, st);
+    ProjBackwardArgs<Real> p{};
+    p.n = n;
+    p.C = C;
+    p.deg = s->sh_degree;
+    p.K = K;
+    p.cam = r->cam;
+    p.means = static_cast<const Real*>(s->means);
+    p.quats = static_cast<const Real*>(s->quats);
+    p.log_scales = static_cast<const Real*>(s->log_scales);
+    p.opacity_logits = static_cast<const Real*>(s->opacity_logits);
+    p.sh = static_cast<const Real*>(s->sh);
+    p.visible = r->visible.as<uint8_t>();
+    p.clamped_bits = r->clamped.as<uint8_t>();
+    p.acc_dcolor = a.acc_dcolor;
+    p.acc_dmean = a.acc_dmean;
+    p.acc_dconic = a.acc_dconic;
+    p.g_pos = a.g_pos;
+    p.g_rot = a.g_rot;
+    p.g_scale = a.g_scale;
+    p.g_opac = a.g_opac;
+    p.g_sh = static_cast<Real*>(g->dsh);
+    p.g_k = a.g_k;
+    p.g_sem = a.g_sem;
+    // chain_activations is linear per Gaussian, so a multi-view sum is chained
+    // once by the caller (msplat_chain_activations) after the last view.
+    p.chain = chain && !accumulate;
+    p.err = ctx->d_err;
+    launch_projection_backward<Real>(p, st);
+    CUDA_TRY(cudaGetLastError());
+    return MSPLAT_OK;
+}
+
+}  // namespace
+
+// =====================================================================  ABI
+extern "C" {
+
+const char* msplat_last_error(void) { return g_error.c_str(); }
+int msplat_abi_version(void) { return MSPLAT_ABI_VERSION; }
+
+msplat_status msplat_context_create(int device, void* cuda_stream, msplat_context** out) {
+    if (!out) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null output");
+    *out = nullptr;
+    CUDA_TRY(cudaSetDevice(device));
+    auto* ctx = new msplat_context();
+    ctx->device = device;
+    if (cuda_stream) {
+        ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+    } else {
+        cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            delete ctx;
+            CUDA_TRY(e);
+        }
+        ctx->own_stream = true;
+    }
+    CUDA_TRY(cudaMalloc(&ctx->d_err, sizeof(DeviceError)));
+    CUDA_TRY(cudaMemset(ctx->d_err, 0, sizeof(DeviceError)));
+    CUDA_TRY(cudaMallocHost(&ctx->h_err, sizeof(DeviceError)));
+    CUDA_TRY(cudaMallocHost(&ctx->h_u64, 64));
+    *out = ctx;
+    return MSPLAT_OK;
+}
+
+void msplat_context_destroy(msplat_context* ctx) {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->stream);
+    for (DevBuf* b : {&ctx->acc_dcolor, &ctx->acc_dmean, &ctx->acc_dconic, &ctx->ddepth_total, &ctx->normal_dv,
+                      &ctx->kept})
+        b->release();
+    cudaFree(ctx->d_err);
+    cudaFreeHost(ctx->h_err);
+    cudaFreeHost(ctx->h_u64);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+msplat_status msplat_context_set_stream(msplat_context* ctx, void* cuda_stream) {
+    if (!ctx) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null context");
+    if (ctx->own_stream) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamDestroy(ctx->stream);
+        ctx->own_stream = false;
+    }
+    ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+    return MSPLAT_OK;
+}
+
+msplat_status msplat_context_check(msplat_context* ctx) {
+    if (!ctx) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null context");
+    CUDA_TRY(cudaGetLastError());
+    return drain_device_error(ctx, 0);
+}
+
+msplat_status msplat_replay_create(msplat_context* ctx, msplat_replay** out) {
+    if (!ctx || !out) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null argument");
+    *out = new msplat_replay();
+    (*out)->ctx = ctx;
+    return MSPLAT_OK;
+}
+
+void msplat_replay_destroy(msplat_replay* r) {
+    if (!r) return;
+    cudaStreamSynchronize(r->ctx->stream);
+    r->release_all();
+    delete r;
+}
+
+msplat_status msplat_replay_set_capture(msplat_replay* r, int flags) {
+    if (!r) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null replay");
+    r->capture = flags;
+    return MSPLAT_OK;
+}
+
+msplat_status msplat_param_layout(int64_t n, int C, int deg, int64_t off[8]) {
+    if (n < 0 || C < 0 || deg < 0 || deg > 3) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "bad layout query");
+    const int64_t sizes[7] = {3, 4, 3, 1, 1, 3 * sh_coeffs(deg), C};
+    off[0] = 0;
+    for (int i = 0; i < 7; ++i) off[i + 1] = off[i] + n * sizes[i];
+    return MSPLAT_OK;
+}
+
+static msplat_status rasterize_entry(msplat_context* ctx, const msplat_scene* s, const msplat_camera* cam,
+                                     const msplat_render_config* cfg, const msplat_frame* f, msplat_replay* replay,
+                                     bool sync) {
+    if (!ctx || !cfg || !f) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "rasterize: null argument");
+    msplat_status st = check_scene(s);
+    if (st != MSPLAT_OK) return st;
+    Cam c;
+    if ((st = make_cam(cam, c)) != MSPLAT_OK) return st;
+    if (!f->transmittance) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "rasterize: transmittance buffer required");
+    msplat_replay local;
+    local.ctx = ctx;
+    msplat_replay* r = replay ? replay : &local;
+    r->cam = c;
+    r->rp.sigma_scale = cfg->sigma_scale;
+    for (int i = 0; i < 3; ++i) r->rp.bg[i] = cfg->background[i];
+    r->rp.early_stop_T = cfg->early_stop_transmittance;
+    r->rp.early_termination = cfg->early_termination;
+    if ((st = size_replay(r, s->dtype, s->n, s->num_classes, s->sh_degree, c.W, c.H)) != MSPLAT_OK) return st;
+    st = s->dtype == MSPLAT_F64 ? rasterize_impl<double>(ctx, s, cfg, f, r, sync)
+                                : rasterize_impl<float>(ctx, s, cfg, f, r, sync);
+    if (st == MSPLAT_OK && (sync || !replay)) st = drain_device_error(ctx, c.W);
+    if (!replay) {
+        cudaStreamSynchronize(ctx->stream);
+        local.release_all();
+    }
+    return st;
+}
+
+msplat_status msplat_rasterize(msplat_context* ctx, const msplat_scene* s, const msplat_camera* cam,
+                               const msplat_render_config* cfg, const msplat_frame* f, msplat_replay* replay) {
+    return rasterize_entry(ctx, s, cam, cfg, f, replay, true);
+}
+
+msplat_status msplat_estimate_normals(msplat_context* ctx, int dtype, const void* depth, const void* T,
+                                      const msplat_camera* cam, const msplat_normal_config* ncfg, void* normals) {
+    if (!ctx || !depth || !T || !normals) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "estimate_normals: null argument");
+    msplat_status st = check_ncfg(ncfg);
+    if (st != MSPLAT_OK) return st;
+    Cam c;
+    if ((st = make_cam(cam, c)) != MSPLAT_OK) return st;
+    if (dtype == MSPLAT_F64) {
+        auto a = normal_args<double>(c, ncfg, depth, T);
+        a.normals = static_cast<double*>(normals);
+        launch_normals_forward<double>(a, ctx->stream);
+    } else {
+        auto a = normal_args<float>(c, ncfg, depth, T);
+        a.normals = static_cast<float*>(normals);
+        launch_normals_forward<float>(a, ctx->stream);
+    }
+    CUDA_TRY(cudaGetLastError());
+    return MSPLAT_OK;
+}
+
+msplat_status msplat_normals_backward(msplat_context* ctx, int dtype, const void* dN, const void* depth, const void* T,
+                                      const msplat_camera* cam, const msplat_normal_config* ncfg, double seed,
+                                      void* dD) {
+    if (!ctx || !dN || !depth || !T || !dD)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "normals_backward: gradient shape mismatch");
+    msplat_status st = check_ncfg(ncfg);
+    if (st != MSPLAT_OK) return st;
+    Cam c;
+    if ((st = make_cam(cam, c)) != MSPLAT_OK) return st;
+    const size_t HW = size_t(c.W) * c.H, R = real_size(dtype);
+    CUDA_TRY(ctx->normal_dv.ensure(12 * HW * R));
+    if (dtype == MSPLAT_F64) {
+        auto a = normal_args<double>(c, ncfg, depth, T);
+        a.dN = static_cast<const double*>(dN);
+        a.dv = ctx->normal_dv.as<double>();
+        a.dD = static_cast<double*>(dD);
+        a.seed = seed;
+        launch_normals_backward<double>(a, ctx->stream);
+    } else {
+        auto a = normal_args<float>(c, ncfg, depth, T);
+        a.dN = static_cast<const float*>(dN);
+        a.dv = ctx->normal_dv.as<float>();
+        a.dD = static_cast<float*>(dD);
+        a.seed = seed;
+        launch_normals_backward<float>(a, ctx->stream);
+    }
+    CUDA_TRY(cudaGetLastError());
+    return MSPLAT_OK;
+}
+
+static msplat_status backward_checks(const msplat_scene* s, const msplat_camera* cam, const msplat_frame* f,
+                                     const msplat_replay* r, const msplat_pixel_grads* pix, const msplat_grads* g) {
+    msplat_status st = check_scene(s);
+    if (st != MSPLAT_OK) return st;
+    if (!r || !r->valid || r->n != s->n || r->deg != s->sh_degree || r->C != s->num_classes || r->dtype != s->dtype)
+        return set_error(MSPLAT_ERR_RUNTIME, "rasterize_backward: replay state does not match the scene");
+    if (!cam || cam->width != r->W || cam->height != r->H || !f || !f->transmittance)
+        return set_error(MSPLAT_ERR_RUNTIME, "rasterize_backward: frame/view size mismatch");
+    if (!pix || !pix->dcolor || !pix->ddepth || !pix->dkmap || (s->num_classes > 0 && !pix->dsemantics))
+        return set_error(MSPLAT_ERR_RUNTIME, "rasterize_backward: pixel-gradient shape mismatch");
+    if (!g || !g->dposition || !g->drotation || !g->dscale || !g->dopacity || !g->dk || !g->dsh ||
+        (s->num_classes > 0 && !g->dsemantics))
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "rasterize_backward: null gradient buffer");
+    return MSPLAT_OK;
+}
+
+msplat_status msplat_rasterize_backward(msplat_context* ctx, const msplat_scene* s, const msplat_camera* cam,
+                                        const msplat_frame* f, const msplat_replay* r, const msplat_pixel_grads* pix,
+                                        msplat_grads* g) {
+    if (!ctx) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null context");
+    msplat_status st = backward_checks(s, cam, f, r, pix, g);
+    if (st != MSPLAT_OK) return st;
+    st = s->dtype == MSPLAT_F64 ? backward_impl<double>(ctx, s, f, r, pix, pix->ddepth, g, 0, 0)
+                                : backward_impl<float>(ctx, s, f, r, pix, pix->ddepth, g, 0, 0);
+    if (st != MSPLAT_OK) return st;
+    return drain_device_error(ctx, r->W);
+}
+
+msplat_status msplat_chain_activations(msplat_context* ctx, const msplat_scene* s, msplat_grads* g) {
+    if (!ctx || !g) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "chain_activations: null argument");
+    msplat_status st = check_scene(s);
+    if (st != MSPLAT_OK) return st;
+    if (s->dtype == MSPLAT_F64)
+        launch_chain<double>(s->n, static_cast<const double*>(s->quats), static_cast<const double*>(s->log_scales),
+                             static_cast<const double*>(s->opacity_logits), static_cast<double*>(g->drotation),
+                             static_cast<double*>(g->dscale), static_cast<double*>(g->dopacity), ctx->stream);
+    else
+        launch_chain<float>(s->n, static_cast<const float*>(s->quats), static_cast<const float*>(s->log_scales),
+                            static_cast<const float*>(s->opacity_logits), static_cast<float*>(g->drotation),
+                            static_cast<float*>(g->dscale), static_cast<float*>(g->dopacity), ctx->stream);
+    CUDA_TRY(cudaGetLastError());
+    return MSPLAT_OK;
+}
+
+msplat_status msplat_fwd_bwd(msplat_context* ctx, const msplat_scene* s, const msplat_camera* cam,
+                             const msplat_render_config* cfg, const msplat_normal_config* ncfg, const msplat_frame* f,
+                             const msplat_pixel_grads* pix, msplat_grads* g, int chain, int accumulate,
+                             msplat_replay* r) {
+    if (!ctx || !r || !f || !f->depth || !f->transmittance)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "fwd_bwd: null argument (replay, depth and T required)");
+    msplat_status st = check_ncfg(ncfg);
+    if (st != MSPLAT_OK) return st;
+    // First use of a replay sizes the instance buffers synchronously; later
+    // calls stay asynchronous (capturable in a CUDA graph).
+    const bool first = r->inst_cap == 0 || !r->valid;
+    st = rasterize_entry(ctx, s, cam, cfg, f, r, first);
+    if (st != MSPLAT_OK) return st;
+    const size_t HW = size_t(r->W) * r->H, R = real_size(s->dtype);
+    CUDA_TRY(ctx->ddepth_total.ensure(HW * R));
+    CUDA_TRY(cudaMemcpyAsync(ctx->ddepth_total.p, pix->ddepth, HW * R, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (f->normals) {
+        st = msplat_estimate_normals(ctx, s->dtype, f->depth, f->transmittance, cam, ncfg, f->normals);
+        if (st != MSPLAT_OK) return st;
+    }
+    if (pix->dnormals) {
+        st = msplat_normals_backward(ctx, s->dtype, pix->dnormals, f->depth, f->transmittance, cam, ncfg, 1.0,
+                                     ctx->ddepth_total.p);
+        if (st != MSPLAT_OK) return st;
+    }
+    st = backward_checks(s, cam, f, r, pix, g);
+    if (st != MSPLAT_OK) return st;
+    st = s->dtype == MSPLAT_F64
+             ? backward_impl<double>(ctx, s, f, r, pix, ctx->ddepth_total.p, g, chain, accumulate)
+             : backward_impl<float>(ctx, s, f, r, pix, ctx->ddepth_total.p, g, chain, accumulate);
+    return st;
+}
+
+msplat_status msplat_adam_step(msplat_context* ctx, int dtype, int64_t n, int C, int deg, void* params,
+                               const void* grads, void* m, void* v, int64_t step, const double lr[7]) {
+    if (!ctx || !params || !grads || !m || !v || !lr) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "adam_step: null argument");
+    if (step < 1) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "adam_step: step must be >= 1");
+    int64_t off[8];
+    msplat_status st = msplat_param_layout(n, C, deg, off);
+    if (st != MSPLAT_OK) return st;
+    const double bc1 = 1 - std::pow(0.9, double(step)), bc2 = 1 - std::pow(0.999, double(step));
+    if (dtype == MSPLAT_F64)
+        launch_adam<double>(off[7], off, lr, static_cast<double*>(params), static_cast<const double*>(grads),
+                            static_cast<double*>(m), static_cast<double*>(v), bc1, bc2, ctx->stream);
+    else
+        launch_adam<float>(off[7], off, lr, static_cast<float*>(params), static_cast<const float*>(grads),
+                           static_cast<float*>(m), static_cast<float*>(v), bc1, bc2, ctx->stream);
+    CUDA_TRY(cudaGetLastError());
+    return MSPLAT_OK;
+}
+
+msplat_status msplat_prune_mask(msplat_context* ctx, int dtype, int64_t n, const void* k, double threshold,
+                                int keep_small, uint8_t* keep, int64_t* kept) {
+    if (!ctx || !k || !keep) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "prune: null argument");
+    CUDA_TRY(ctx->kept.ensure(8));
+    CUDA_TRY(cudaMemsetAsync(ctx->kept.p, 0, 8, ctx->stream));
+    if (dtype == MSPLAT_F64)
+        launch_prune_mask<double>(n, static_cast<const double*>(k), threshold, keep_small, keep,
+                                  ctx->kept.as<unsigned long long>(), ctx->stream);
+    else
+        launch_prune_mask<float>(n, static_cast<const float*>(k), threshold, keep_small, keep,
+                                 ctx->kept.as<unsigned long long>(), ctx->stream);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_u64, ctx->kept.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    const int64_t kk = int64_t(ctx->h_u64[0]);
+    if (kept) *kept = kk;
+    if (kk == 0 && n > 0) {
+        char buf[128];
+        snprintf(buf, sizeof buf, "prune: threshold %f would remove every gaussian", threshold);
+        return set_error(MSPLAT_ERR_RUNTIME, buf);
+    }
+    return MSPLAT_OK;
+}
+
+msplat_status msplat_replay_counters(msplat_replay* r, msplat_counters* out) {
+    if (!r || !out || !r->valid) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "replay: no forward recorded");
+    cudaStream_t st = r->ctx->stream;
+    const int64_t tiles = int64_t(r->tiles_x) * r->tiles_y;
+    std::vector<uint2> ranges(static_cast<size_t>(tiles));
+    unsigned long long vis = 0;
+    int64_t inst = 0;
+    CUDA_TRY(cudaMemcpyAsync(&vis, r->visible_count.p, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&inst, r->d_inst_count.p, 8, cudaMemcpyDeviceToHost, st));
+    if (tiles) CUDA_TRY(cudaMemcpyAsync(ranges.data(), r->tile_range.p, size_t(tiles) * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    int64_t mx = 0;
+    for (const auto& rg : ranges) mx = std::max<int64_t>(mx, int64_t(rg.y) - int64_t(rg.x));
+    out->n = r->n;
+    out->visible = int64_t(vis);
+    out->instances = inst;
+    out->tiles = tiles;
+    out->max_tile_list = mx;
+    return MSPLAT_OK;
+}
+
+msplat_status msplat_replay_bins(msplat_replay* r, int64_t* tile_offsets, int32_t* values, int64_t capacity) {
+    if (!r || !r->valid) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "replay: no forward recorded");
+    cudaStream_t st = r->ctx->stream;
+    const int64_t tiles = int64_t(r->tiles_x) * r->tiles_y;
+    std::vector<uint2> ranges(static_cast<size_t>(tiles));
+    int64_t inst = 0;
+    CUDA_TRY(cudaMemcpyAsync(&inst, r->d_inst_count.p, 8, cudaMemcpyDeviceToHost, st));
+    if (tiles) CUDA_TRY(cudaMemcpyAsync(ranges.data(), r->tile_range.p, size_t(tiles) * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (tile_offsets) {
+        // Ranges are contiguous in tile order: offsets follow from the lengths.
+        int64_t off = 0;
+        for (int64_t t = 0; t < tiles; ++t) {
+            tile_offsets[t] = off;
+            off += int64_t(ranges[size_t(t)].y) - int64_t(ranges[size_t(t)].x);
+        }
+        tile_offsets[tiles] = off;
+    }
+    if (values && capacity >= inst && inst > 0)
+        CUDA_TRY(cudaMemcpy(values, r->sorted_gauss, size_t(inst) * 4, cudaMemcpyDeviceToHost));
+    return MSPLAT_OK;
+}
+
+msplat_status msplat_replay_splats(msplat_replay* r, uint8_t* visible, double* center, double* conic,
+                                   double* sort_depth, double* radius, double* rgb, uint8_t* clamped) {
+    if (!r || !r->valid) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "replay: no forward recorded");
+    if (!(r->capture & 1) && (center || conic || sort_depth || radius || rgb))
+        return set_error(MSPLAT_ERR_LOGIC, "replay: splat capture was not enabled (msplat_replay_set_capture)");
+    CUDA_TRY(cudaStreamSynchronize(r->ctx->stream));
+    const size_t n = size_t(r->n);
+    if (!n) return MSPLAT_OK;
+    if (visible) CUDA_TRY(cudaMemcpy(visible, r->visible.p, n, cudaMemcpyDeviceToHost));
+    if (center) CUDA_TRY(cudaMemcpy(center, r->cap_center.p, n * 16, cudaMemcpyDeviceToHost));
+    if (conic) CUDA_TRY(cudaMemcpy(conic, r->cap_conic.p, n * 24, cudaMemcpyDeviceToHost));
+    if (sort_depth) CUDA_TRY(cudaMemcpy(sort_depth, r->cap_depth.p, n * 8, cudaMemcpyDeviceToHost));
+    if (radius) CUDA_TRY(cudaMemcpy(radius, r->cap_radius.p, n * 8, cudaMemcpyDeviceToHost));
+    if (rgb) CUDA_TRY(cudaMemcpy(rgb, r->cap_rgb.p, n * 24, cudaMemcpyDeviceToHost));
+    if (clamped) {
+        std::vector<uint8_t> bits(n);
+        CUDA_TRY(cudaMemcpy(bits.data(), r->clamped.p, n, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < n; ++i)
+            for (int c = 0; c < 3; ++c) clamped[3 * i + c] = (bits[i] >> c) & 1;
+    }
+    return MSPLAT_OK;
+}
+
+msplat_status msplat_replay_terminus(msplat_replay* r, int32_t* terminus) {
+    if (!r || !r->valid || !terminus) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "replay: no forward recorded");
+    CUDA_TRY(cudaStreamSynchronize(r->ctx->stream));
+    CUDA_TRY(cudaMemcpy(terminus, r->terminus.p, size_t(r->W) * r->H * 4, cudaMemcpyDeviceToHost));
+    return MSPLAT_OK;
+}
+
+msplat_status msplat_replay_weight_sums(msplat_replay* r, double* ws) {
+    if (!r || !r->valid || !ws) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "replay: no forward recorded");
+    if (!(r->capture & 2)) return set_error(MSPLAT_ERR_LOGIC, "replay: weight-sum capture was not enabled");
+    CUDA_TRY(cudaStreamSynchronize(r->ctx->stream));
+    const size_t n = size_t(r->n);
+    if (!n) return MSPLAT_OK;
+    if (r->dtype == MSPLAT_F64) {
+        CUDA_TRY(cudaMemcpy(ws, r->weight_sums.p, n * 8, cudaMemcpyDeviceToHost));
+    } else {
+        std::vector<float> tmp(n);
+        CUDA_TRY(cudaMemcpy(tmp.data(), r->weight_sums.p, n * 4, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < n; ++i) ws[i] = tmp[i];
+    }
+    return MSPLAT_OK;
+}
+
+msplat_status msplat_bin_and_sort_host(msplat_context* ctx, int64_t n, const uint8_t* visible, const double* center,
+                                       const double* radius, const double* sort_depth, int width, int height,
+                                       int64_t* tile_offsets, int32_t* values, int64_t capacity, int64_t* count) {
+    if (!ctx || (n > 0 && (!visible || !center || !radius || !sort_depth)) || width < 1 || height < 1)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "bin_and_sort: bad argument");
+    msplat_replay r;
+    r.ctx = ctx;
+    msplat_status st = size_replay(&r, MSPLAT_F64, n, 0, 0, width, height);
+    if (st != MSPLAT_OK) return st;
+    DevBuf dv, dc, dr, dd;
+    const size_t nn = size_t(std::max<int64_t>(n, 1));
+    CUDA_TRY(dv.ensure(nn));
+    CUDA_TRY(dc.ensure(nn * 16));
+    CUDA_TRY(dr.ensure(nn * 8));
+    CUDA_TRY(dd.ensure(nn * 8));
+    if (n > 0) {
+        CUDA_TRY(cudaMemcpy(dv.p, visible, size_t(n), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(dc.p, center, size_t(n) * 16, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(dr.p, radius, size_t(n) * 8, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(dd.p, sort_depth, size_t(n) * 8, cudaMemcpyHostToDevice));
+    }
+    launch_rects_from_splats(n, dv.as<uint8_t>(), dc.as<double>(), dr.as<double>(), dd.as<double>(), width, height,
+                             r.depth_key.as<uint64_t>(), r.order.as<uint32_t>(), r.tile_count.as<uint32_t>(),
+                             r.tile_rect.as<uint2>(), ctx->stream);
+    r.binned_explicit = true;
+    st = binning_with_capacity(&r, true);
+    if (st == MSPLAT_OK) st = drain_device_error(ctx, width);
+    if (st == MSPLAT_OK) {
+        r.valid = true;
+        int64_t inst = 0;
+        cudaMemcpy(&inst, r.d_inst_count.p, 8, cudaMemcpyDeviceToHost);
+        if (count) *count = inst;
+        st = msplat_replay_bins(&r, tile_offsets, values, capacity);
+    }
+    cudaStreamSynchronize(ctx->stream);
+    r.release_all();
+    for (DevBuf* b : {&dv, &dc, &dr, &dd}) b->release();
+    return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// Shared device definitions for the sm_100a msplat kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace msplat_cuda {
+
+constexpr int kTile = 16;                     // TileBins::kTileSize (msplat/rasterizer.hpp:34)
+constexpr int kTilePixels = kTile * kTile;    // one CTA per tile, one thread per pixel
+constexpr double kNearPlane = 0.01;           // msplat/geometry.hpp:63
+constexpr double kCovFloor = 0.3;             // msplat/geometry.hpp:64
+constexpr double kMinAlpha = 1.0 / 255.0;     // msplat/geometry.hpp:65
+constexpr double kMaxAlpha = 0.99;            // msplat/geometry.hpp:66
+constexpr double kDegenerateScale = 1e-8;     // msplat/geometry.hpp:30
+
+// Device error word: first fault wins (atomicCAS on code).  Codes mirror the
+// reference exception sites.
+enum ErrCode : int {
+    kErrNone = 0,
+    kErrNonFiniteBlend = 1,    // rasterizer.cpp:148-151  (a = pixel, b = primitive)
+    kErrNonFiniteOutput = 2,   // rasterizer.cpp:179-183  (a = pixel)
+    kErrSceneModified = 3,     // rasterizer_backward.cpp:40-44 (b = primitive)
+    kErrNonFiniteGrad = 4,     // scene.cpp:97-106 (b = primitive)
+    kErrZeroQuat = 5,          // scene.cpp:49-51 (b = primitive)
+    kErrNonFiniteParam = 6,    // scene.cpp:36-38 (b = primitive)
+    kErrInstanceOverflow = 7,  // internal: tile-instance buffer too small (a = needed)
+};
+
+struct DeviceError {
+    int code;
+    int pad;
+    long long a;
+    long long b;
+};
+
+__device__ __forceinline__ void raise_error(DeviceError* e, int code, long long a, long long b) {
+    if (atomicCAS(&e->code, 0, code) == 0) {
+        e->a = a;
+        e->b = b;
+    }
+}
+
+// Camera with the derived world->cam pose, both in double (CameraView).
+struct Cam {
+    double fx, fy, cx, cy;
+    int W, H;
+    double Rc2w[9], tc2w[3], Rw2c[9], tw2c[3];
+};
+
+// Render constants passed by value to the blend kernels.
+struct RenderParams {
+    double sigma_scale;
+    double bg[3];
+    double early_stop_T;
+    int early_termination;
+};
+
+template <typename Real>
+struct Vec3T {
+    Real x, y, z;
+};
+
+// Per-visible-Gaussian records written by K1 and gathered per tile by K6/K9.
+// Alpha-test record (everything a visited pair needs), 8 Reals.
+template <typename Real>
+struct AlphaRec {
+    Real cx, cy;      // splat centre (pixels)
+    Real ca, cb, cc;  // conic (xx, xy, yy)
+    Real opacity;     // activated alpha (logistic of the logit)
+    Real log_thr;     // log(1/(255*opacity)): power >= log_thr  <=>  alpha >= 1/255 (fp32 path)
+    Real pad;
+};
+
+// Blend record (everything a blended pair needs beyond the alpha test).
+// Rt is R^T of the activated rotation, row-major; inv_axes = 1/(sigma*s).
+template <typename Real>
+struct BlendRec {
+    Real Rt[9];
+    Real axes[3];     // sigma * s (double path divides like the reference)
+    Real inv_axes[3]; // 1 / (sigma * s)
+    Real vs[3];       // v_s = R^T (o - mu) / axes   (per view constant)
+    Real csq;         // |v_s|^2 - 1
+    Real zc;          // sort depth (camera-z of the centre): no-hit fallback
+    Real rgb[3];      // view-dependent colour
+    Real k;           // gradient factor
+    Real hit_ok;      // 0 when an axis is degenerate (< 1e-8): never intersects
+    Real q[4];        // unit quaternion (w,x,y,z) of the activated rotation
+    Real pad[3];
+};
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+}  // namespace msplat_cuda

@@ -1,0 +1,172 @@
+// Kernel argument structs and launchers shared by the msplat CUDA translation
+// units (preprocess.cu, binning.cu, forward.cu, normals.cu, backward.cu,
+// optim.cu) and the C-ABI layer (cabi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace msplat_cuda {
+
+template <typename Real>
+struct PreprocessArgs {
+    int64_t n;
+    int C, deg, K;
+    const Real *means, *quats, *log_scales, *opacity_logits, *k, *sh, *semantics;
+    Cam cam;
+    double sigma;
+    int W, H;
+    // outputs
+    uint64_t* depth_key;
+    uint32_t* order;
+    uint32_t* tile_count;
+    uint2* tile_rect;
+    uint8_t* visible;
+    uint8_t* clamped_bits;
+    AlphaRec<Real>* arec;
+    BlendRec<Real>* brec;
+    double *cap_center, *cap_conic, *cap_depth, *cap_radius, *cap_rgb;  // optional
+    unsigned long long* visible_count;
+    DeviceError* err;
+};
+
+template <typename Real>
+void launch_preprocess(const PreprocessArgs<Real>& a, cudaStream_t s);
+
+// Binning (K2-K5).  Workspace is owned by the replay (cabi.cu).
+struct BinningBuffers {
+    int64_t n;            // Gaussians
+    int tiles_x, tiles_y;
+    int64_t inst_cap;     // capacity of the instance arrays
+    int depth_key_bits;   // 63 for K1 keys (z > 0.01), 64 for explicit splats
+    // per Gaussian
+    uint64_t *depth_key, *depth_key_alt;
+    uint32_t *order, *order_alt;
+    uint32_t* tile_count;  // by Gaussian id (K1 output)
+    uint2* tile_rect;      // by Gaussian id (K1 output)
+    uint32_t* count_sorted;  // tile_count in depth order
+    uint32_t* offset_sorted; // exclusive scan of count_sorted
+    // per instance
+    uint32_t *inst_tile, *inst_tile_alt;
+    uint32_t *inst_gauss, *inst_gauss_alt;
+    // per tile
+    uint2* tile_range;  // [start, end) into the sorted instance list
+    // scalars (device)
+    int64_t* d_inst_count;
+    uint32_t* d_inst_total32;
+    // scratch
+    uint32_t *hist, *hist_scanned, *scan_tiles;
+    DeviceError* err;
+    // results (which ping-pong buffer holds the final list)
+    uint32_t* sorted_gauss;  // per-instance Gaussian ids, tile-major (set by run_binning)
+};
+
+void run_binning(BinningBuffers& b, cudaStream_t s);
+
+// bin_and_sort on explicit splats: tile rects / counts / depth keys from
+// centre, radius, depth (rasterizer.cpp:30-39).
+void launch_rects_from_splats(int64_t n, const uint8_t* visible, const double* center,
+                              const double* radius, const double* depth, int W, int H,
+                              uint64_t* depth_key, uint32_t* order, uint32_t* tile_count,
+                              uint2* tile_rect, cudaStream_t s);
+size_t binning_scratch_elems(int64_t n_cap, int64_t inst_cap);
+
+// Forward blend (K6).
+template <typename Real>
+struct ForwardArgs {
+    int W, H, tiles_x, C;
+    Cam cam;
+    RenderParams rp;
+    const uint2* tile_range;
+    const uint32_t* inst_gauss;
+    const AlphaRec<Real>* arec;
+    const BlendRec<Real>* brec;
+    const Real* semantics;  // [n][C] scene parameters
+    Real *color, *depth, *sem_out, *kmap, *T;  // planar outputs (T required)
+    int32_t* contributors;
+    int32_t* terminus;
+    Real* weight_sums;  // optional
+    DeviceError* err;
+};
+template <typename Real>
+void launch_forward(const ForwardArgs<Real>& a, int ntiles, cudaStream_t s);
+
+// Normals (K7, K8).
+template <typename Real>
+struct NormalArgs {
+    int W, H;
+    Cam cam;
+    int step1, step2;
+    double lambda, mask_threshold;
+    const Real* depth;
+    const Real* T;
+    Real* normals;           // K7 output [3][H][W]
+    const Real* dN;          // K8 input [3][H][W]
+    Real* dv;                // K8 scratch [12][H][W] (per-centre adjoints)
+    Real* dD;                // K8 output (accumulated with seed)
+    double seed;
+};
+template <typename Real>
+void launch_normals_forward(const NormalArgs<Real>& a, cudaStream_t s);
+template <typename Real>
+void launch_normals_backward(const NormalArgs<Real>& a, cudaStream_t s);
+
+// Backward blend (K9) and per-Gaussian backward (K10).
+template <typename Real>
+struct BackwardArgs {
+    int W, H, tiles_x, C;
+    int64_t n;
+    Cam cam;
+    RenderParams rp;
+    const uint2* tile_range;
+    const uint32_t* inst_gauss;
+    const AlphaRec<Real>* arec;
+    const BlendRec<Real>* brec;
+    const Real* semantics;
+    const Real* T_final;
+    const int32_t* terminus;
+    const Real *dcolor, *ddepth, *dsem, *dkmap;  // planar pixel grads
+    // accumulation targets (zeroed before K9)
+    Real *g_pos, *g_rot, *g_scale, *g_opac, *g_k, *g_sem;  // output gradient buffer
+    Real *acc_dcolor, *acc_dmean, *acc_dconic;             // scratch [n][3], [n][2], [n][3]
+    DeviceError* err;
+};
+template <typename Real>
+void launch_backward_blend(const BackwardArgs<Real>& a, int ntiles, cudaStream_t s);
+
+template <typename Real>
+struct ProjBackwardArgs {
+    int64_t n;
+    int C, deg, K;
+    Cam cam;
+    const Real *means, *quats, *log_scales, *opacity_logits, *sh;
+    const uint8_t* visible;
+    const uint8_t* clamped_bits;
+    const Real *acc_dcolor, *acc_dmean, *acc_dconic;
+    Real *g_pos, *g_rot, *g_scale, *g_opac, *g_sh, *g_k, *g_sem;
+    int chain;  // fuse chain_activations (scene.cpp:108-129); only for single-view buffers
+    DeviceError* err;
+};
+template <typename Real>
+void launch_projection_backward(const ProjBackwardArgs<Real>& a, cudaStream_t s);
+
+template <typename Real>
+void launch_chain(int64_t n, const Real* quats, const Real* log_scales, const Real* opac,
+                  Real* g_rot, Real* g_scale, Real* g_opac, cudaStream_t s);
+
+template <typename Real>
+void launch_check_replay(int64_t n, const Real* means, const Real* k, const Real* saved_means,
+                         const Real* saved_k, DeviceError* err, cudaStream_t s);
+
+// Optimizer (K11).
+template <typename Real>
+void launch_adam(int64_t total, const int64_t* seg_starts /*host, 8*/, const double* lr /*7*/,
+                 Real* params, const Real* grads, Real* m, Real* v, double bc1, double bc2,
+                 cudaStream_t s);
+template <typename Real>
+void launch_prune_mask(int64_t n, const Real* k, double threshold, int keep_small, uint8_t* keep,
+                       unsigned long long* kept, cudaStream_t s);
+
+}  // namespace msplat_cuda

@@ -1,0 +1,325 @@
+// K1: per-Gaussian preprocess (one thread per Gaussian).
+//
+// Replaces prepare_view (core/src/rasterizer.cpp:55-74): activate
+// (core/src/scene.cpp:42-60), project_gaussian (core/src/geometry.cpp:107-136),
+// eval_sh_color (core/src/sh.cpp:75-84), the pixel-rect/tile-range rule of
+// bin_and_sort (core/src/rasterizer.cpp:32-39) and the per-view constant part
+// of intersect (core/src/geometry.cpp:39-52).
+//
+// Everything that decides integer binning output (centre, covariance,
+// determinant, radius, depth key, tile rect) is computed in FP64 with the
+// reference's evaluation order and WITHOUT FMA contraction: this translation
+// unit is compiled with --fmad=false, so every a*b+c below rounds twice like
+// the reference's -ffp-contract=off double arithmetic.  That is what makes the
+// tile lists, their order and the per-tile ranges bit-exact.  Blend records are
+// then rounded to the kernel precision (float or double).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace msplat_cuda {
+
+namespace {
+
+__device__ __forceinline__ double dot3(const double* a, const double* b) {
+    double s = a[0] * b[0];
+    s += a[1] * b[1];
+    s += a[2] * b[2];
+    return s;
+}
+
+// x86 cvttsd2si semantics of the reference's int(std::floor(v)): NaN and
+// out-of-range values become INT_MIN (rasterizer.cpp:32-35 on this platform).
+__device__ __forceinline__ int floor_to_int(double v) {
+    const double f = floor(v);
+    if (!(f >= -2147483648.0 && f < 2147483648.0)) return int(0x80000000u);
+    return int(f);
+}
+
+__device__ __forceinline__ void quat_to_rotation(const double* q, double* R) {
+    double n2 = q[0] * q[0];
+    n2 += q[1] * q[1];
+    n2 += q[2] * q[2];
+    n2 += q[3] * q[3];
+    const double n = sqrt(n2);
+    const double w = q[0] / n, x = q[1] / n, y = q[2] / n, z = q[3] / n;
+    R[0] = 1 - 2 * (y * y + z * z); R[1] = 2 * (x * y - w * z); R[2] = 2 * (x * z + w * y);
+    R[3] = 2 * (x * y + w * z); R[4] = 1 - 2 * (x * x + z * z); R[5] = 2 * (y * z - w * x);
+    R[6] = 2 * (x * z - w * y); R[7] = 2 * (y * z + w * x); R[8] = 1 - 2 * (x * x + y * y);
+}
+
+__device__ __forceinline__ void sh_basis(int deg, double x, double y, double z, double* b) {
+    const double C0 = 0.28209479177387814, C1 = 0.4886025119029199;
+    b[0] = C0;
+    if (deg >= 1) { b[1] = -C1 * y; b[2] = C1 * z; b[3] = -C1 * x; }
+    if (deg >= 2) {
+        const double xx = x * x, yy = y * y, zz = z * z;
+        b[4] = 1.0925484305920792 * x * y;
+        b[5] = -1.0925484305920792 * y * z;
+        b[6] = 0.31539156525252005 * (2 * zz - xx - yy);
+        b[7] = -1.0925484305920792 * x * z;
+        b[8] = 0.5462742152960396 * (xx - yy);
+    }
+    if (deg >= 3) {
+        const double xx = x * x, yy = y * y, zz = z * z;
+        b[9] = -0.5900435899266435 * y * (3 * xx - yy);
+        b[10] = 2.890611442640554 * x * y * z;
+        b[11] = -0.4570457994644658 * y * (4 * zz - xx - yy);
+        b[12] = 0.3731763325901154 * z * (2 * zz - 3 * xx - 3 * yy);
+        b[13] = -0.4570457994644658 * x * (4 * zz - xx - yy);
+        b[14] = 1.445305721320277 * z * (xx - yy);
+        b[15] = -0.5900435899266435 * x * (xx - 3 * yy);
+    }
+}
+
+template <typename Real>
+__device__ __forceinline__ bool finite_params(const PreprocessArgs<Real>& a, int64_t i) {
+    bool ok = true;
+    for (int j = 0; j < 3; ++j)
+        ok &= isfinite(double(a.means[3 * i + j])) && isfinite(double(a.log_scales[3 * i + j]));
+    for (int j = 0; j < 4; ++j) ok &= isfinite(double(a.quats[4 * i + j]));
+    ok &= isfinite(double(a.opacity_logits[i])) && isfinite(double(a.k[i]));
+    for (int j = 0; j < 3 * a.K; ++j) ok &= isfinite(double(a.sh[i * 3 * a.K + j]));
+    for (int j = 0; j < a.C; ++j) ok &= isfinite(double(a.semantics[i * a.C + j]));
+    return ok;
+}
+
+}  // namespace
+
+template <typename Real>
+__global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs<Real> a) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    const Cam& c = a.cam;
+
+    a.depth_key[i] = ~0ull;  // not binned unless proven otherwise
+    a.order[i] = uint32_t(i);
+    a.tile_count[i] = 0;
+    a.visible[i] = 0;
+
+    if (!finite_params(a, i)) {  // Scene::validate / activate (scene.cpp:36-38, 43-45)
+        raise_error(a.err, kErrNonFiniteParam, 0, i);
+        return;
+    }
+    // ---- activate (scene.cpp:42-60)
+    double q[4] = {double(a.quats[4 * i]), double(a.quats[4 * i + 1]), double(a.quats[4 * i + 2]),
+                   double(a.quats[4 * i + 3])};
+    double n2 = q[0] * q[0];
+    n2 += q[1] * q[1];
+    n2 += q[2] * q[2];
+    n2 += q[3] * q[3];
+    const double qn = sqrt(n2);
+    if (qn < 1e-12) {
+        raise_error(a.err, kErrZeroQuat, 0, i);
+        return;
+    }
+    for (int j = 0; j < 4; ++j) q[j] = q[j] / qn;
+    double R[9];
+    quat_to_rotation(q, R);
+    const double mu[3] = {double(a.means[3 * i]), double(a.means[3 * i + 1]), double(a.means[3 * i + 2])};
+    const double s[3] = {exp(double(a.log_scales[3 * i])), exp(double(a.log_scales[3 * i + 1])),
+                         exp(double(a.log_scales[3 * i + 2]))};
+    const double opacity = 1.0 / (1.0 + exp(-double(a.opacity_logits[i])));
+
+    // ---- project_gaussian (geometry.cpp:107-136)
+    double pc[3];
+    for (int r = 0; r < 3; ++r) {
+        double t = c.Rw2c[r * 3 + 0] * mu[0];
+        t += c.Rw2c[r * 3 + 1] * mu[1];
+        t += c.Rw2c[r * 3 + 2] * mu[2];
+        pc[r] = t + c.tw2c[r];
+    }
+    if (pc[2] <= kNearPlane) return;
+    const double x = pc[0], y = pc[1], z = pc[2];
+    const double cxp = c.fx * x / z + c.cx;
+    const double cyp = c.fy * y / z + c.cy;
+    const double J[6] = {c.fx / z, 0, -c.fx * x / (z * z), 0, c.fy / z, -c.fy * y / (z * z)};
+    double V[9];
+    {
+        double RD[9];
+        for (int r = 0; r < 3; ++r)
+            for (int q2 = 0; q2 < 3; ++q2) RD[r * 3 + q2] = R[r * 3 + q2] * (s[q2] * s[q2]);
+        for (int r = 0; r < 3; ++r)
+            for (int q2 = 0; q2 < 3; ++q2) {
+                double t = RD[r * 3 + 0] * R[q2 * 3 + 0];
+                t += RD[r * 3 + 1] * R[q2 * 3 + 1];
+                t += RD[r * 3 + 2] * R[q2 * 3 + 2];
+                V[r * 3 + q2] = t;
+            }
+    }
+    double T[6], TV[6], cov[4];
+    for (int r = 0; r < 2; ++r)
+        for (int q2 = 0; q2 < 3; ++q2) {
+            double t = J[r * 3 + 0] * c.Rw2c[0 * 3 + q2];
+            t += J[r * 3 + 1] * c.Rw2c[1 * 3 + q2];
+            t += J[r * 3 + 2] * c.Rw2c[2 * 3 + q2];
+            T[r * 3 + q2] = t;
+        }
+    for (int r = 0; r < 2; ++r)
+        for (int q2 = 0; q2 < 3; ++q2) {
+            double t = T[r * 3 + 0] * V[0 * 3 + q2];
+            t += T[r * 3 + 1] * V[1 * 3 + q2];
+            t += T[r * 3 + 2] * V[2 * 3 + q2];
+            TV[r * 3 + q2] = t;
+        }
+    for (int r = 0; r < 2; ++r)
+        for (int q2 = 0; q2 < 2; ++q2) {
+            double t = TV[r * 3 + 0] * T[q2 * 3 + 0];
+            t += TV[r * 3 + 1] * T[q2 * 3 + 1];
+            t += TV[r * 3 + 2] * T[q2 * 3 + 2];
+            cov[r * 2 + q2] = t;
+        }
+    cov[0] += kCovFloor;
+    cov[3] += kCovFloor;
+    const double det = cov[0] * cov[3] - cov[2] * cov[1];
+    if (det <= 0) return;
+    const double ca = cov[3] / det, cb = -cov[1] / det, cc = cov[0] / det;
+    const double mid = 0.5 * (cov[0] + cov[3]);
+    const double m2 = mid * mid - det;
+    const double lambda_max = mid + sqrt(0.1 < m2 ? m2 : 0.1);
+    const double radius = 3.0 * sqrt(lambda_max);
+    a.visible[i] = 1;
+    atomicAdd(a.visible_count, 1ull);
+
+    // ---- pixel rect -> tile rect (rasterizer.cpp:32-39)
+    int x0 = floor_to_int(cxp - radius), x1 = floor_to_int(cxp + radius);
+    int y0 = floor_to_int(cyp - radius), y1 = floor_to_int(cyp + radius);
+    x0 = x0 > 0 ? x0 : 0;
+    x1 = x1 < a.W - 1 ? x1 : a.W - 1;
+    y0 = y0 > 0 ? y0 : 0;
+    y1 = y1 < a.H - 1 ? y1 : a.H - 1;
+    if (!(x1 < x0 || y1 < y0)) {
+        const int tx0 = x0 / kTile, tx1 = x1 / kTile, ty0 = y0 / kTile, ty1 = y1 / kTile;
+        a.tile_rect[i] = make_uint2(uint32_t(tx0) | (uint32_t(tx1) << 16),
+                                    uint32_t(ty0) | (uint32_t(ty1) << 16));
+        a.tile_count[i] = uint32_t((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+        // Positive doubles order like their IEEE bit patterns (z > 0.01 here).
+        a.depth_key[i] = uint64_t(__double_as_longlong(z));
+    }
+
+    // ---- view-dependent colour (rasterizer.cpp:66-71, sh.cpp:75-84)
+    double rgb[3];
+    uint8_t clamped[3];
+    {
+        const double tg[3] = {mu[0] - c.tc2w[0], mu[1] - c.tc2w[1], mu[2] - c.tc2w[2]};
+        const double nrm = sqrt(dot3(tg, tg));
+        double dx = 0, dy = 0, dz = 1;
+        if (nrm > 1e-12) { dx = tg[0] / nrm; dy = tg[1] / nrm; dz = tg[2] / nrm; }
+        double b[16];
+        sh_basis(a.deg, dx, dy, dz, b);
+        for (int ch = 0; ch < 3; ++ch) {
+            const Real* shc = a.sh + (i * 3 + ch) * a.K;
+            double t = double(shc[0]) * b[0];
+            for (int j = 1; j < a.K; ++j) t += double(shc[j]) * b[j];
+            const double raw = t + 0.5;
+            clamped[ch] = raw < 0;
+            rgb[ch] = clamped[ch] ? 0.0 : raw;
+        }
+    }
+
+    // ---- per-view constant part of intersect (geometry.cpp:39-52)
+    const double axes[3] = {a.sigma * s[0], a.sigma * s[1], a.sigma * s[2]};
+    double amin = axes[0];
+    if (axes[1] < amin) amin = axes[1];
+    if (axes[2] < amin) amin = axes[2];
+    const double rel[3] = {c.tc2w[0] - mu[0], c.tc2w[1] - mu[1], c.tc2w[2] - mu[2]};
+    double vs[3];
+    for (int j = 0; j < 3; ++j) {
+        double t = R[0 * 3 + j] * rel[0];
+        t += R[1 * 3 + j] * rel[1];
+        t += R[2 * 3 + j] * rel[2];
+        vs[j] = t / axes[j];
+    }
+    const double csq = dot3(vs, vs) - 1.0;
+
+    AlphaRec<Real> ar;
+    ar.cx = Real(cxp);
+    ar.cy = Real(cyp);
+    ar.ca = Real(ca);
+    ar.cb = Real(cb);
+    ar.cc = Real(cc);
+    ar.opacity = Real(opacity);
+    ar.log_thr = Real(log(1.0 / (255.0 * opacity)));
+    ar.pad = Real(0);
+    a.arec[i] = ar;
+
+    BlendRec<Real> br;
+    for (int r = 0; r < 3; ++r)
+        for (int q2 = 0; q2 < 3; ++q2) br.Rt[r * 3 + q2] = Real(R[q2 * 3 + r]);
+    for (int j = 0; j < 3; ++j) {
+        br.axes[j] = Real(axes[j]);
+        br.inv_axes[j] = Real(1.0 / axes[j]);
+        br.vs[j] = Real(vs[j]);
+        br.rgb[j] = Real(rgb[j]);
+        br.pad[j] = Real(0);
+    }
+    br.csq = Real(csq);
+    br.zc = Real(z);
+    br.k = a.k[i];
+    br.hit_ok = Real(amin < kDegenerateScale ? 0 : 1);
+    for (int j = 0; j < 4; ++j) br.q[j] = Real(q[j]);
+    a.brec[i] = br;
+
+    a.clamped_bits[i] = uint8_t(clamped[0] | (clamped[1] << 1) | (clamped[2] << 2));
+    if (a.cap_center) {  // replay capture for parity checks (msplat_replay_splats)
+        a.cap_center[2 * i] = cxp;
+        a.cap_center[2 * i + 1] = cyp;
+        a.cap_conic[3 * i] = ca;
+        a.cap_conic[3 * i + 1] = cb;
+        a.cap_conic[3 * i + 2] = cc;
+        a.cap_depth[i] = z;
+        a.cap_radius[i] = radius;
+        for (int j = 0; j < 3; ++j) a.cap_rgb[3 * i + j] = rgb[j];
+    }
+}
+
+template <typename Real>
+void launch_preprocess(const PreprocessArgs<Real>& a, cudaStream_t s) {
+    if (a.n == 0) return;
+    const int threads = 256;
+    const int64_t blocks = (a.n + threads - 1) / threads;
+    preprocess_kernel<Real><<<unsigned(blocks), threads, 0, s>>>(a);
+}
+
+__global__ void rects_from_splats_kernel(int64_t n, const uint8_t* __restrict__ visible,
+                                         const double* __restrict__ center,
+                                         const double* __restrict__ radius,
+                                         const double* __restrict__ depth, int W, int H,
+                                         uint64_t* depth_key, uint32_t* order, uint32_t* tile_count,
+                                         uint2* tile_rect) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    order[i] = uint32_t(i);
+    depth_key[i] = ~0ull;
+    tile_count[i] = 0;
+    if (!visible[i]) return;
+    const double cx = center[2 * i], cy = center[2 * i + 1], r = radius[i];
+    int x0 = floor_to_int(cx - r), x1 = floor_to_int(cx + r);
+    int y0 = floor_to_int(cy - r), y1 = floor_to_int(cy + r);
+    x0 = x0 > 0 ? x0 : 0;
+    x1 = x1 < W - 1 ? x1 : W - 1;
+    y0 = y0 > 0 ? y0 : 0;
+    y1 = y1 < H - 1 ? y1 : H - 1;
+    if (x1 < x0 || y1 < y0) return;
+    const int tx0 = x0 / kTile, tx1 = x1 / kTile, ty0 = y0 / kTile, ty1 = y1 / kTile;
+    tile_rect[i] = make_uint2(uint32_t(tx0) | (uint32_t(tx1) << 16), uint32_t(ty0) | (uint32_t(ty1) << 16));
+    tile_count[i] = uint32_t((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+    // Arbitrary doubles: map to an order-preserving unsigned key (negative
+    // values flip all bits, positive set the sign bit) -- the explicit-splat
+    // entry point is not restricted to z > 0.
+    const uint64_t b = uint64_t(__double_as_longlong(depth[i]));
+    depth_key[i] = (b >> 63) ? ~b : (b | (1ull << 63));
+}
+
+void launch_rects_from_splats(int64_t n, const uint8_t* visible, const double* center,
+                              const double* radius, const double* depth, int W, int H,
+                              uint64_t* depth_key, uint32_t* order, uint32_t* tile_count,
+                              uint2* tile_rect, cudaStream_t s) {
+    if (n == 0) return;
+    rects_from_splats_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(
+        n, visible, center, radius, depth, W, H, depth_key, order, tile_count, tile_rect);
+}
+
+template void launch_preprocess<float>(const PreprocessArgs<float>&, cudaStream_t);
+template void launch_preprocess<double>(const PreprocessArgs<double>&, cudaStream_t);
+
+}  // namespace msplat_cuda
