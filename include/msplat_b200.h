@@ -235,6 +235,28 @@ MSPLAT_API msplat_status msplat_prune_mask(msplat_context* ctx, int dtype, int64
                                 double threshold, int keep_small, uint8_t* keep_device,
                                 int64_t* kept);
 
+/* ------------------------------------------------------ instrumentation */
+/* Stage ids for msplat_context_timings. */
+enum {
+    MSPLAT_STAGE_PREPROCESS = 0,  /* K1 */
+    MSPLAT_STAGE_BINNING = 1,     /* K2-K5 */
+    MSPLAT_STAGE_FORWARD = 2,     /* K6 */
+    MSPLAT_STAGE_NORMALS = 3,     /* K7 */
+    MSPLAT_STAGE_NORMALS_BWD = 4, /* K8 */
+    MSPLAT_STAGE_BACKWARD = 5,    /* K9 */
+    MSPLAT_STAGE_PROJ_BWD = 6,    /* K10 (+chain) */
+    MSPLAT_STAGE_OPTIM = 7,       /* K11 */
+    MSPLAT_STAGE_COUNT = 8
+};
+/* When enabled, every stage is bracketed by CUDA events on the context's
+ * stream; msplat_context_timings (synchronizing) returns the summed device
+ * milliseconds and launch counts per stage since the last call and resets. */
+MSPLAT_API msplat_status msplat_context_set_timing(msplat_context* ctx, int enable);
+MSPLAT_API msplat_status msplat_context_timings(msplat_context* ctx, double ms[MSPLAT_STAGE_COUNT],
+                                     int64_t calls[MSPLAT_STAGE_COUNT]);
+/* Total kernel launches issued by this library (process-wide counter). */
+MSPLAT_API int64_t msplat_kernel_launches(void);
+
 /* ------------------------------------------------------- replay access */
 /* Synchronizing copies of the replay state to HOST memory (parity tests and
  * the C++ drop-in's ReplayState fields).  NULL outputs are skipped. */

@@ -21,6 +21,7 @@ MSPLAT_ERR_CUDA = 4
 MSPLAT_ERR_OUT_OF_MEMORY = 5
 MSPLAT_F32 = 0
 MSPLAT_F64 = 1
+STAGES = ("preprocess", "binning", "forward", "normals", "normals_bwd", "backward", "proj_bwd", "optim")
 
 _vp = ct.c_void_p
 _i64 = ct.c_int64
@@ -109,6 +110,9 @@ def _sig(lib):
         ("msplat_replay_weight_sums", ct.c_int, [_vp, P(ct.c_double)]),
         ("msplat_bin_and_sort_host", ct.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, ct.c_int, ct.c_int,
                                                 P(_i64), P(ct.c_int32), _i64, P(_i64)]),
+        ("msplat_context_set_timing", ct.c_int, [_vp, ct.c_int]),
+        ("msplat_context_timings", ct.c_int, [_vp, P(ct.c_double), P(_i64)]),
+        ("msplat_kernel_launches", _i64, []),
     ]
     for name, res, args in S:
         f = getattr(lib, name)

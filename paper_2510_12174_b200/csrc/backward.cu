@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(kThreads) backward_kernel(const BackwardArgs<R
                 // Depth chain (rasterizer_backward.cpp:205-218).
                 const Real dd = dD * w;
                 if (dd != Real(0)) {
-                    const HitEval<Real> h = intersect<Real>(br, ray);
+                    const HitEval<Real> h = intersect<Real>(br, ray, a.cam, a.raw, g);
                     if (h.hit) {
                         if (!(fabs(double(h.a)) < 1e-12)) {
                             const Real g_t = dd * ray.dz;
@@ -495,12 +495,14 @@ void launch_backward_blend(const BackwardArgs<Real>& a, int ntiles, cudaStream_t
         configured = true;
     }
     backward_kernel<Real><<<ntiles, kThreads, backward_smem_bytes<Real>(a.C), s>>>(a);
+    count_launches(1);
 }
 
 template <typename Real>
 void launch_projection_backward(const ProjBackwardArgs<Real>& a, cudaStream_t s) {
     if (a.n == 0) return;
     projection_backward_kernel<Real><<<unsigned((a.n + 255) / 256), 256, 0, s>>>(a);
+    count_launches(1);
 }
 
 template <typename Real>
@@ -508,6 +510,7 @@ void launch_chain(int64_t n, const Real* quats, const Real* log_scales, const Re
                   Real* g_scale, Real* g_opac, cudaStream_t s) {
     if (n == 0) return;
     chain_kernel<Real><<<unsigned((n + 255) / 256), 256, 0, s>>>(n, quats, log_scales, opac, g_rot, g_scale, g_opac);
+    count_launches(1);
 }
 
 template <typename Real>
@@ -515,6 +518,7 @@ void launch_check_replay(int64_t n, const Real* means, const Real* k, const Real
                          const Real* saved_k, DeviceError* err, cudaStream_t s) {
     if (n == 0) return;
     check_replay_kernel<Real><<<unsigned((n + 255) / 256), 256, 0, s>>>(n, means, k, saved_means, saved_k, err);
+    count_launches(1);
 }
 
 #define MSPLAT_INST(R)                                                                                  \

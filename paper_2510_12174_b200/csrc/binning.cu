@@ -110,16 +110,19 @@ void run_binning(BinningBuffers& b, cudaStream_t s) {
     if (n > 0) {
         gather_counts_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(n, order_sorted, b.tile_count,
                                                                        b.count_sorted);
+        count_launches(1);
         device_exclusive_scan<uint32_t>(b.count_sorted, b.offset_sorted, nullptr, n, b.scan_tiles,
                                         b.d_inst_total32, s);
     } else {
         cudaMemsetAsync(b.d_inst_total32, 0, sizeof(uint32_t), s);
     }
     finalize_count_kernel<<<1, 1, 0, s>>>(b.d_inst_total32, b.inst_cap, b.d_inst_count, b.err);
+    count_launches(1);
     if (n > 0)
         emit_instances_kernel<<<unsigned((n * 32 + 255) / 256), 256, 0, s>>>(
             n, order_sorted, b.tile_rect, b.count_sorted, b.offset_sorted, b.tiles_x,
             b.d_inst_count, b.inst_tile, b.inst_gauss);
+        count_launches(1);
 
     // K4: stable sort of the instances by tile id.
     const bool tile_in_b = radix_sort_pairs<uint32_t, kTileBits>(
@@ -133,6 +136,7 @@ void run_binning(BinningBuffers& b, cudaStream_t s) {
     if (b.inst_cap > 0)
         tile_ranges_kernel<<<unsigned((b.inst_cap + 255) / 256), 256, 0, s>>>(b.d_inst_count,
                                                                               tile_sorted, b.tile_range);
+        count_launches(1);
 }
 
 }  // namespace msplat_cuda

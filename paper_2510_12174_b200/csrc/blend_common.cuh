@@ -84,14 +84,110 @@ struct HitEval {
     bool hit;
     Real t_mid, a, b;
     Real ds[3];
+    Real depth_fp64;  // set when the FP64 re-decision ran (< 0 otherwise)
 };
 
-// intersect (core/src/geometry.cpp:37-64) with the per-view constant v_s and
-// |v_s|^2 - 1 precomputed by K1.
+// Raw scene parameters, for the FP64 re-decision of near-silhouette pairs.
 template <typename Real>
-__device__ __forceinline__ HitEval<Real> intersect(const BlendRec<Real>& g, const PixelRay<Real>& r) {
+struct RawParams {
+    const Real *means, *quats, *log_scales;
+    double sigma;
+};
+
+// intersect() exactly as the reference evaluates it, in FP64 from the raw
+// parameters (activate: scene.cpp:42-60; compute_ray: geometry.cpp:31-35;
+// intersect: geometry.cpp:37-64).  Used by the FP32 kernels when the FP32
+// discriminant or t_mid is too close to zero to decide reliably, so hit/miss
+// decisions match the FP64 oracle.  Not inlined: it runs for a tiny fraction
+// of blended pairs (grazing rays).
+template <typename Real>
+__device__ __noinline__ bool intersect_fp64(const Cam& c, const RawParams<Real>& rp, uint32_t g, Real px,
+                                            Real py, double* t_out, double* a_out, double* b_out,
+                                            double* ds_out, double* depth_out) {
+    const double pd[3] = {(double(px) - c.cx) / c.fx, (double(py) - c.cy) / c.fy, 1.0};
+    double d[3];
+    for (int i = 0; i < 3; ++i) {
+        double t = c.Rc2w[i * 3] * pd[0];
+        t += c.Rc2w[i * 3 + 1] * pd[1];
+        t += c.Rc2w[i * 3 + 2] * pd[2];
+        d[i] = t;
+    }
+    {
+        double z = d[0] * d[0];
+        z += d[1] * d[1];
+        z += d[2] * d[2];
+        const double n = sqrt(z);
+        for (int i = 0; i < 3; ++i) d[i] = d[i] / n;
+    }
+    double q[4], n2 = 0;
+    for (int j = 0; j < 4; ++j) q[j] = double(rp.quats[4 * size_t(g) + j]);
+    n2 = q[0] * q[0];
+    n2 += q[1] * q[1];
+    n2 += q[2] * q[2];
+    n2 += q[3] * q[3];
+    double qn = sqrt(n2);
+    for (int j = 0; j < 4; ++j) q[j] = q[j] / qn;
+    n2 = q[0] * q[0];
+    n2 += q[1] * q[1];
+    n2 += q[2] * q[2];
+    n2 += q[3] * q[3];
+    qn = sqrt(n2);
+    const double w = q[0] / qn, x = q[1] / qn, y = q[2] / qn, z = q[3] / qn;
+    const double R[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                         2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                         2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+    double axes[3], rel[3], vs[3], ds[3];
+    for (int j = 0; j < 3; ++j) {
+        axes[j] = rp.sigma * exp(double(rp.log_scales[3 * size_t(g) + j]));
+        rel[j] = c.tc2w[j] - double(rp.means[3 * size_t(g) + j]);
+    }
+    if (fmin(axes[0], fmin(axes[1], axes[2])) < kDegenerateScale) return false;
+    for (int j = 0; j < 3; ++j) {
+        double tv = R[0 * 3 + j] * rel[0];
+        tv += R[1 * 3 + j] * rel[1];
+        tv += R[2 * 3 + j] * rel[2];
+        double td = R[0 * 3 + j] * d[0];
+        td += R[1 * 3 + j] * d[1];
+        td += R[2 * 3 + j] * d[2];
+        vs[j] = tv / axes[j];
+        ds[j] = td / axes[j];
+    }
+    double a = ds[0] * ds[0];
+    a += ds[1] * ds[1];
+    a += ds[2] * ds[2];
+    double bb = vs[0] * ds[0];
+    bb += vs[1] * ds[1];
+    bb += vs[2] * ds[2];
+    const double b = 2.0 * bb;
+    double cc = vs[0] * vs[0];
+    cc += vs[1] * vs[1];
+    cc += vs[2] * vs[2];
+    cc = cc - 1.0;
+    const double disc = b * b - 4.0 * a * cc;
+    if (disc < 0 || a <= 0) return false;
+    const double t = -b / (2.0 * a);
+    if (t <= 0) return false;
+    *t_out = t;
+    *a_out = a;
+    *b_out = b;
+    for (int j = 0; j < 3; ++j) ds_out[j] = ds[j];
+    double p0 = c.tc2w[0] + t * d[0], p1 = c.tc2w[1] + t * d[1], p2 = c.tc2w[2] + t * d[2];
+    double dz = c.Rw2c[6] * p0;
+    dz += c.Rw2c[7] * p1;
+    dz += c.Rw2c[8] * p2;
+    *depth_out = dz + c.tw2c[2];
+    return true;
+}
+
+// intersect (core/src/geometry.cpp:37-64) with the per-view constant v_s and
+// |v_s|^2 - 1 precomputed by K1.  In FP32, a discriminant or t_mid within a
+// relative 1e-4 of zero is re-decided in FP64 (intersect_fp64).
+template <typename Real>
+__device__ __forceinline__ HitEval<Real> intersect(const BlendRec<Real>& g, const PixelRay<Real>& r,
+                                                   const Cam& cam, const RawParams<Real>& rp, uint32_t gid) {
     HitEval<Real> h;
     h.hit = false;
+    h.depth_fp64 = Real(-1);
     if (g.hit_ok == Real(0)) return h;
     Real dl[3];
 #pragma unroll
@@ -104,8 +200,24 @@ __device__ __forceinline__ HitEval<Real> intersect(const BlendRec<Real>& g, cons
             h.ds[i] = dl[i] * g.inv_axes[i];
     }
     h.a = h.ds[0] * h.ds[0] + h.ds[1] * h.ds[1] + h.ds[2] * h.ds[2];
-    h.b = Real(2) * (g.vs[0] * h.ds[0] + g.vs[1] * h.ds[1] + g.vs[2] * h.ds[2]);
+    const Real vd = g.vs[0] * h.ds[0] + g.vs[1] * h.ds[1] + g.vs[2] * h.ds[2];
+    h.b = Real(2) * vd;
     const Real disc = h.b * h.b - Real(4) * h.a * g.csq;
+    if constexpr (sizeof(Real) == 4) {
+        const Real mag = h.b * h.b + fabsf(Real(4) * h.a * g.csq);
+        const Real vmag = sqrtf((g.vs[0] * g.vs[0] + g.vs[1] * g.vs[1] + g.vs[2] * g.vs[2]) * h.a);
+        if (fabsf(disc) <= Real(1e-4) * mag || fabsf(vd) <= Real(1e-4) * vmag) {
+            double t, a, b, ds[3], dep;
+            if (!intersect_fp64<Real>(cam, rp, gid, r.px, r.py, &t, &a, &b, ds, &dep)) return h;
+            h.hit = true;
+            h.t_mid = Real(t);
+            h.a = Real(a);
+            h.b = Real(b);
+            for (int i = 0; i < 3; ++i) h.ds[i] = Real(ds[i]);
+            h.depth_fp64 = Real(dep);
+            return h;
+        }
+    }
     if (disc < Real(0) || h.a <= Real(0)) return h;
     h.t_mid = -h.b / (Real(2) * h.a);
     if (h.t_mid <= Real(0)) return h;

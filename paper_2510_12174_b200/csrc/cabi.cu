@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -61,7 +62,78 @@ struct DevBuf {
 int64_t sh_coeffs(int deg) { return int64_t(deg + 1) * (deg + 1); }
 size_t real_size(int dtype) { return dtype == MSPLAT_F64 ? 8 : 4; }
 
+std::atomic<long long> g_launches{0};
+
+// CUDA-event brackets per stage (msplat_context_set_timing).  Events come from
+// a grow-only pool; elapsed times are summed when the caller asks.
+struct StageTimer {
+    bool enabled = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    struct Mark {
+        int stage;
+        cudaEvent_t a, b;
+    };
+    std::vector<Mark> marks;
+    int open_stage = -1;
+    cudaEvent_t open_ev = nullptr;
+
+    cudaEvent_t next() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+    // Inside CUDA-graph capture a plain record is only a dependency edge; an
+    // external record becomes an event-record node that timestamps each replay.
+    static void record(cudaEvent_t e, cudaStream_t s) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cs);
+        if (cs == cudaStreamCaptureStatusActive)
+            cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+        else
+            cudaEventRecord(e, s);
+    }
+    void begin(int stage, cudaStream_t s) {
+        if (!enabled) return;
+        open_stage = stage;
+        open_ev = next();
+        record(open_ev, s);
+    }
+    void end(cudaStream_t s) {
+        if (!enabled || open_stage < 0) return;
+        cudaEvent_t e = next();
+        record(e, s);
+        marks.push_back({open_stage, open_ev, e});
+        open_stage = -1;
+    }
+    void collect(double* ms, int64_t* calls) {
+        for (int i = 0; i < MSPLAT_STAGE_COUNT; ++i) {
+            ms[i] = 0;
+            if (calls) calls[i] = 0;
+        }
+        for (const Mark& m : marks) {
+            cudaEventSynchronize(m.b);
+            float t = 0;
+            cudaEventElapsedTime(&t, m.a, m.b);
+            ms[m.stage] += t;
+            if (calls) calls[m.stage] += 1;
+        }
+        marks.clear();
+        used = 0;
+    }
+    ~StageTimer() {
+        for (cudaEvent_t e : pool) cudaEventDestroy(e);
+    }
+};
+
 }  // namespace
+
+namespace msplat_cuda {
+void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace msplat_cuda
 
 struct msplat_context {
     int device = 0;
@@ -72,6 +144,7 @@ struct msplat_context {
     unsigned long long* h_u64 = nullptr;  // pinned scratch
     // scratch owned by the context (shared by calls on its stream)
     DevBuf acc_dcolor, acc_dmean, acc_dconic, ddepth_total, normal_dv, kept;
+    StageTimer timer;
 };
 
 struct msplat_replay {
@@ -348,10 +421,14 @@ msplat_status rasterize_impl(msplat_context* ctx, const msplat_scene* s, const m
                              const msplat_frame* f, msplat_replay* r, bool sync) {
     const size_t R = sizeof(Real);
     CUDA_TRY(cudaMemsetAsync(r->visible_count.p, 0, 8, ctx->stream));
+    ctx->timer.begin(MSPLAT_STAGE_PREPROCESS, ctx->stream);
     launch_preprocess<Real>(preprocess_args<Real>(r, s, cfg), ctx->stream);
+    ctx->timer.end(ctx->stream);
     CUDA_TRY(cudaGetLastError());
     r->binned_explicit = false;
+    ctx->timer.begin(MSPLAT_STAGE_BINNING, ctx->stream);
     msplat_status st = binning_with_capacity(r, sync);
+    ctx->timer.end(ctx->stream);
     if (st != MSPLAT_OK) return st;
     // snapshot for check_replay (rasterizer_backward.cpp:40-44)
     if (s->n > 0) {
@@ -372,6 +449,8 @@ msplat_status rasterize_impl(msplat_context* ctx, const msplat_scene* s, const m
     a.arec = r->arec.as<AlphaRec<Real>>();
     a.brec = r->brec.as<BlendRec<Real>>();
     a.semantics = static_cast<const Real*>(s->semantics);
+    a.raw = RawParams<Real>{static_cast<const Real*>(s->means), static_cast<const Real*>(s->quats),
+                            static_cast<const Real*>(s->log_scales), cfg->sigma_scale};
     a.color = static_cast<Real*>(f->color);
     a.depth = static_cast<Real*>(f->depth);
     a.sem_out = static_cast<Real*>(f->semantics);
@@ -381,7 +460,9 @@ msplat_status rasterize_impl(msplat_context* ctx, const msplat_scene* s, const m
     a.terminus = r->terminus.as<int32_t>();
     a.weight_sums = (r->capture & 2) ? r->weight_sums.as<Real>() : nullptr;
     a.err = ctx->d_err;
+    ctx->timer.begin(MSPLAT_STAGE_FORWARD, ctx->stream);
     launch_forward<Real>(a, r->tiles_x * r->tiles_y, ctx->stream);
+    ctx->timer.end(ctx->stream);
     CUDA_TRY(cudaGetLastError());
     r->valid = true;
     return MSPLAT_OK;
@@ -450,6 +531,8 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
     a.arec = r->arec.as<AlphaRec<Real>>();
     a.brec = r->brec.as<BlendRec<Real>>();
     a.semantics = static_cast<const Real*>(s->semantics);
+    a.raw = RawParams<Real>{static_cast<const Real*>(s->means), static_cast<const Real*>(s->quats),
+                            static_cast<const Real*>(s->log_scales), r->rp.sigma_scale};
     a.T_final = static_cast<const Real*>(f->transmittance);
     a.terminus = r->terminus.as<int32_t>();
     a.dcolor = static_cast<const Real*>(pix->dcolor);
@@ -466,7 +549,9 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
     a.acc_dmean = ctx->acc_dmean.as<Real>();
     a.acc_dconic = ctx->acc_dconic.as<Real>();
     a.err = ctx->d_err;
+    ctx->timer.begin(MSPLAT_STAGE_BACKWARD, st);
     launch_backward_blend<Real>(a, r->tiles_x * r->tiles_y, st);
+    ctx->timer.end(st);
     ProjBackwardArgs<Real> p{};
     p.n = n;
     p.C = C;
@@ -494,7 +579,9 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
     // once by the caller (msplat_chain_activations) after the last view.
     p.chain = chain && !accumulate;
     p.err = ctx->d_err;
+    ctx->timer.begin(MSPLAT_STAGE_PROJ_BWD, st);
     launch_projection_backward<Real>(p, st);
+    ctx->timer.end(st);
     CUDA_TRY(cudaGetLastError());
     return MSPLAT_OK;
 }
@@ -629,6 +716,7 @@ msplat_status msplat_estimate_normals(msplat_context* ctx, int dtype, const void
     if (st != MSPLAT_OK) return st;
     Cam c;
     if ((st = make_cam(cam, c)) != MSPLAT_OK) return st;
+    ctx->timer.begin(MSPLAT_STAGE_NORMALS, ctx->stream);
     if (dtype == MSPLAT_F64) {
         auto a = normal_args<double>(c, ncfg, depth, T);
         a.normals = static_cast<double*>(normals);
@@ -638,6 +726,7 @@ msplat_status msplat_estimate_normals(msplat_context* ctx, int dtype, const void
         a.normals = static_cast<float*>(normals);
         launch_normals_forward<float>(a, ctx->stream);
     }
+    ctx->timer.end(ctx->stream);
     CUDA_TRY(cudaGetLastError());
     return MSPLAT_OK;
 }
@@ -653,6 +742,7 @@ msplat_status msplat_normals_backward(msplat_context* ctx, int dtype, const void
     if ((st = make_cam(cam, c)) != MSPLAT_OK) return st;
     const size_t HW = size_t(c.W) * c.H, R = real_size(dtype);
     CUDA_TRY(ctx->normal_dv.ensure(12 * HW * R));
+    ctx->timer.begin(MSPLAT_STAGE_NORMALS_BWD, ctx->stream);
     if (dtype == MSPLAT_F64) {
         auto a = normal_args<double>(c, ncfg, depth, T);
         a.dN = static_cast<const double*>(dN);
@@ -668,6 +758,7 @@ msplat_status msplat_normals_backward(msplat_context* ctx, int dtype, const void
         a.seed = seed;
         launch_normals_backward<float>(a, ctx->stream);
     }
+    ctx->timer.end(ctx->stream);
     CUDA_TRY(cudaGetLastError());
     return MSPLAT_OK;
 }
@@ -757,15 +848,33 @@ msplat_status msplat_adam_step(msplat_context* ctx, int dtype, int64_t n, int C,
     msplat_status st = msplat_param_layout(n, C, deg, off);
     if (st != MSPLAT_OK) return st;
     const double bc1 = 1 - std::pow(0.9, double(step)), bc2 = 1 - std::pow(0.999, double(step));
+    ctx->timer.begin(MSPLAT_STAGE_OPTIM, ctx->stream);
     if (dtype == MSPLAT_F64)
         launch_adam<double>(off[7], off, lr, static_cast<double*>(params), static_cast<const double*>(grads),
                             static_cast<double*>(m), static_cast<double*>(v), bc1, bc2, ctx->stream);
     else
         launch_adam<float>(off[7], off, lr, static_cast<float*>(params), static_cast<const float*>(grads),
                            static_cast<float*>(m), static_cast<float*>(v), bc1, bc2, ctx->stream);
+    ctx->timer.end(ctx->stream);
     CUDA_TRY(cudaGetLastError());
     return MSPLAT_OK;
 }
+
+msplat_status msplat_context_set_timing(msplat_context* ctx, int enable) {
+    if (!ctx) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null context");
+    ctx->timer.enabled = enable != 0;
+    return MSPLAT_OK;
+}
+
+msplat_status msplat_context_timings(msplat_context* ctx, double ms[MSPLAT_STAGE_COUNT],
+                                     int64_t calls[MSPLAT_STAGE_COUNT]) {
+    if (!ctx || !ms) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null argument");
+    ctx->timer.collect(ms, calls);
+    CUDA_TRY(cudaGetLastError());
+    return MSPLAT_OK;
+}
+
+int64_t msplat_kernel_launches(void) { return int64_t(g_launches.load()); }
 
 msplat_status msplat_prune_mask(msplat_context* ctx, int dtype, int64_t n, const void* k, double threshold,
                                 int keep_small, uint8_t* keep, int64_t* kept) {

@@ -80,8 +80,10 @@ __global__ void __launch_bounds__(kThreads) forward_kernel(const ForwardArgs<Rea
             const uint32_t g = s_gid[j];
             if (ae.pass) {
                 const BlendRec<Real> br = a.brec[g];
-                const HitEval<Real> h = intersect<Real>(br, ray);
-                const Real d = h.hit ? midpoint_depth<Real>(a.cam, ray, h.t_mid) : br.zc;
+                const HitEval<Real> h = intersect<Real>(br, ray, a.cam, a.raw, g);
+                const Real d = !h.hit ? br.zc
+                                      : (h.depth_fp64 >= Real(0) ? h.depth_fp64
+                                                                 : midpoint_depth<Real>(a.cam, ray, h.t_mid));
                 if (!isfinite(double(ae.alpha)) || !isfinite(double(d))) {
                     raise_error(a.err, kErrNonFiniteBlend, (long long)y * a.W + x, g);
                     done = true;
@@ -151,6 +153,7 @@ void launch_forward(const ForwardArgs<Real>& a, int ntiles, cudaStream_t s) {
         configured = true;
     }
     forward_kernel<Real><<<ntiles, kThreads, smem, s>>>(a);
+    count_launches(1);
 }
 
 template void launch_forward<float>(const ForwardArgs<float>&, int, cudaStream_t);

@@ -7,8 +7,13 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "blend_common.cuh"
 
 namespace msplat_cuda {
+
+// Process-wide kernel launch counter (msplat_kernel_launches); every launch
+// site calls count_launches with the number of kernels it enqueued.
+void count_launches(int n);
 
 template <typename Real>
 struct PreprocessArgs {
@@ -84,6 +89,7 @@ struct ForwardArgs {
     const AlphaRec<Real>* arec;
     const BlendRec<Real>* brec;
     const Real* semantics;  // [n][C] scene parameters
+    RawParams<Real> raw;    // means/quats/log_scales for the FP64 re-decision
     Real *color, *depth, *sem_out, *kmap, *T;  // planar outputs (T required)
     int32_t* contributors;
     int32_t* terminus;
@@ -125,6 +131,7 @@ struct BackwardArgs {
     const AlphaRec<Real>* arec;
     const BlendRec<Real>* brec;
     const Real* semantics;
+    RawParams<Real> raw;
     const Real* T_final;
     const int32_t* terminus;
     const Real *dcolor, *ddepth, *dsem, *dkmap;  // planar pixel grads

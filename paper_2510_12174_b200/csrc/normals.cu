@@ -5,6 +5,11 @@
 // needs straight from the depth map (no P_world buffer), applies the
 // two-scale cross products, sign alignment, fusion, normalisation and the
 // view-facing flip, and writes planar unit normals (zero when invalid).
+// The stencil runs in CAMERA space: P_world = R P_cam + t, so edge vectors,
+// cross products, norms and the facing test are rotation-covariant/invariant
+// and t cancels exactly; only the output normal is rotated to world space
+// (and the incoming gradient rotated back).  Same values as the reference in
+// exact arithmetic, without FP32 cancellation against t.
 //
 // K8 replaces normals_backward (core/src/normals.cpp:103-152).  The reference
 // scatters each centre's four edge adjoints onto 8 stencil pixels; a scatter
@@ -23,16 +28,13 @@ namespace {
 template <typename Real>
 struct NormalCtx {
     const NormalArgs<Real>* a;
+    // Camera-space backprojection pixel_dir_cam * d (normals.cpp:10-12, 16-26).
     __device__ void point(int x, int y, Real* P) const {
         const Cam& c = a->cam;
         const Real d = a->depth[size_t(y) * a->W + x];
-        const Real pd0 = (Real(x) + Real(0.5) - Real(c.cx)) / Real(c.fx);
-        const Real pd1 = (Real(y) + Real(0.5) - Real(c.cy)) / Real(c.fy);
-        const Real p0 = pd0 * d, p1 = pd1 * d, p2 = d;
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-            P[i] = Real(c.Rc2w[i * 3]) * p0 + Real(c.Rc2w[i * 3 + 1]) * p1 + Real(c.Rc2w[i * 3 + 2]) * p2 +
-                   Real(c.tc2w[i]);
+        P[0] = ((Real(x) + Real(0.5) - Real(c.cx)) / Real(c.fx)) * d;
+        P[1] = ((Real(y) + Real(0.5) - Real(c.cy)) / Real(c.fy)) * d;
+        P[2] = d;
     }
     __device__ bool covered(int x, int y) const {
         return a->T[size_t(y) * a->W + x] < Real(a->mask_threshold);
@@ -82,7 +84,7 @@ __device__ bool centre_state(const NormalCtx<Real>& nc, int x, int y, Stencil<Re
     if (st.norm < Real(1e-12)) return false;
     Real P[3];
     nc.point(x, y, P);
-    Real dv[3] = {Real(a.cam.tc2w[0]) - P[0], Real(a.cam.tc2w[1]) - P[1], Real(a.cam.tc2w[2]) - P[2]};
+    Real dv[3] = {-P[0], -P[1], -P[2]};  // camera centre minus the point, camera frame
     const Real dn = sqrt(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]);
     Real ndot = Real(0);
     for (int i = 0; i < 3; ++i) ndot += (st.nf[i] / st.norm) * (dn > Real(0) ? dv[i] / dn : dv[i]);
@@ -99,7 +101,11 @@ __global__ void normals_forward_kernel(const NormalArgs<Real> a) {
     Real N[3] = {0, 0, 0};
     if (centre_state(nc, x, y, st)) {
         const Real s = st.flipped ? Real(-1) : Real(1);
-        for (int i = 0; i < 3; ++i) N[i] = s * (st.nf[i] / st.norm);
+        Real Nc[3];
+        for (int i = 0; i < 3; ++i) Nc[i] = s * (st.nf[i] / st.norm);
+        for (int i = 0; i < 3; ++i)
+            N[i] = Real(a.cam.Rc2w[i * 3]) * Nc[0] + Real(a.cam.Rc2w[i * 3 + 1]) * Nc[1] +
+                   Real(a.cam.Rc2w[i * 3 + 2]) * Nc[2];
     }
     const size_t HW = size_t(a.W) * a.H, p = size_t(y) * a.W + x;
     for (int i = 0; i < 3; ++i) a.normals[i * HW + p] = N[i];
@@ -112,7 +118,10 @@ __global__ void normals_adjoint_kernel(const NormalArgs<Real> a) {
     const size_t HW = size_t(a.W) * a.H, p = size_t(y) * a.W + x;
     Real out[12];
     for (int i = 0; i < 12; ++i) out[i] = Real(0);
-    Real g[3] = {a.dN[p], a.dN[HW + p], a.dN[2 * HW + p]};
+    const Real gw[3] = {a.dN[p], a.dN[HW + p], a.dN[2 * HW + p]};
+    Real g[3];  // camera-frame gradient R^T gw
+    for (int i = 0; i < 3; ++i)
+        g[i] = Real(a.cam.Rc2w[i]) * gw[0] + Real(a.cam.Rc2w[3 + i]) * gw[1] + Real(a.cam.Rc2w[6 + i]) * gw[2];
     const NormalCtx<Real> nc{&a};
     Stencil<Real> st;
     if ((g[0] != Real(0) || g[1] != Real(0) || g[2] != Real(0)) && centre_state(nc, x, y, st)) {
@@ -156,12 +165,11 @@ __global__ void normals_gather_kernel(const NormalArgs<Real> a) {
         const size_t q = size_t(py) * a.W + px;
         for (int i = 0; i < 3; ++i) dP[i] += sg[k] * a.dv[size_t(blk[k] + i) * HW + q];
     }
+    // dD += dP_world . (R pd) = dP_cam . pd   (normals.cpp:110-113)
     const Cam& c = a.cam;
     const Real pd0 = (Real(x) + Real(0.5) - Real(c.cx)) / Real(c.fx);
     const Real pd1 = (Real(y) + Real(0.5) - Real(c.cy)) / Real(c.fy);
-    Real dd = Real(0);
-    for (int i = 0; i < 3; ++i)
-        dd += dP[i] * (Real(c.Rc2w[i * 3]) * pd0 + Real(c.Rc2w[i * 3 + 1]) * pd1 + Real(c.Rc2w[i * 3 + 2]));
+    const Real dd = dP[0] * pd0 + dP[1] * pd1 + dP[2];
     const size_t p = size_t(y) * a.W + x;
     a.dD[p] += Real(a.seed) * dd;
 }
@@ -172,13 +180,16 @@ template <typename Real>
 void launch_normals_forward(const NormalArgs<Real>& a, cudaStream_t s) {
     const dim3 blk(32, 8), grd((a.W + 31) / 32, (a.H + 7) / 8);
     normals_forward_kernel<Real><<<grd, blk, 0, s>>>(a);
+    count_launches(1);
 }
 
 template <typename Real>
 void launch_normals_backward(const NormalArgs<Real>& a, cudaStream_t s) {
     const dim3 blk(32, 8), grd((a.W + 31) / 32, (a.H + 7) / 8);
     normals_adjoint_kernel<Real><<<grd, blk, 0, s>>>(a);
+    count_launches(1);
     normals_gather_kernel<Real><<<grd, blk, 0, s>>>(a);
+    count_launches(1);
 }
 
 template void launch_normals_forward<float>(const NormalArgs<float>&, cudaStream_t);

@@ -59,6 +59,7 @@ void launch_adam(int64_t total, const int64_t* seg_starts, const double* lr, Rea
     for (int i = 0; i < 8; ++i) seg.start[i] = seg_starts[i];
     for (int i = 0; i < 7; ++i) seg.lr[i] = lr[i];
     adam_kernel<Real><<<unsigned((total + 255) / 256), 256, 0, s>>>(total, seg, params, grads, m, v, bc1, bc2);
+    count_launches(1);
 }
 
 template <typename Real>
@@ -66,6 +67,7 @@ void launch_prune_mask(int64_t n, const Real* k, double threshold, int keep_smal
                        unsigned long long* kept, cudaStream_t s) {
     if (n == 0) return;
     prune_mask_kernel<Real><<<unsigned((n + 255) / 256), 256, 0, s>>>(n, k, threshold, keep_small, keep, kept);
+    count_launches(1);
 }
 
 template void launch_adam<float>(int64_t, const int64_t*, const double*, float*, const float*, float*, float*,

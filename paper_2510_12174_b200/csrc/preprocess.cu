@@ -278,6 +278,7 @@ void launch_preprocess(const PreprocessArgs<Real>& a, cudaStream_t s) {
     const int threads = 256;
     const int64_t blocks = (a.n + threads - 1) / threads;
     preprocess_kernel<Real><<<unsigned(blocks), threads, 0, s>>>(a);
+    count_launches(1);
 }
 
 __global__ void rects_from_splats_kernel(int64_t n, const uint8_t* __restrict__ visible,
@@ -317,6 +318,7 @@ void launch_rects_from_splats(int64_t n, const uint8_t* visible, const double* c
     if (n == 0) return;
     rects_from_splats_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(
         n, visible, center, radius, depth, W, H, depth_key, order, tile_count, tile_rect);
+    count_launches(1);
 }
 
 template void launch_preprocess<float>(const PreprocessArgs<float>&, cudaStream_t);

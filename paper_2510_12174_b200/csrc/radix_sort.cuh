@@ -240,8 +240,11 @@ inline void device_exclusive_scan(const T* in, T* out, const int64_t* d_n, int64
     const int ntiles = int((n_cap + kScanTile - 1) / kScanTile);
     if (ntiles == 0) return;
     scan_reduce_kernel<T><<<ntiles, kScanThreads, 0, s>>>(in, d_n, n_cap, tile_sums);
+    count_launches(1);
     scan_tiles_kernel<T><<<1, 1024, 0, s>>>(tile_sums, ntiles, d_total);
+    count_launches(1);
     scan_apply_kernel<T><<<ntiles, kScanThreads, 0, s>>>(in, d_n, n_cap, tile_sums, out);
+    count_launches(1);
 }
 
 // Sorts (keys, vals) by bits [0, total_bits) of the key.  Ping-pongs between
@@ -261,10 +264,12 @@ inline bool radix_sort_pairs(Key* keys_a, uint32_t* vals_a, Key* keys_b, uint32_
         uint32_t* vout = in_b ? vals_a : vals_b;
         radix_upsweep_kernel<Key, BITS><<<ntiles, kSortThreads, 0, s>>>(kin, d_n, n_cap, shift,
                                                                        sc.hist, ntiles);
+        count_launches(1);
         device_exclusive_scan<uint32_t>(sc.hist, sc.hist_scanned, nullptr, int64_t(RADIX) * ntiles,
                                         sc.scan_tiles, nullptr, s);
         radix_downsweep_kernel<Key, BITS><<<ntiles, kSortThreads, 0, s>>>(
             kin, vin, kout, vout, d_n, n_cap, shift, sc.hist_scanned, ntiles);
+        count_launches(1);
         in_b = !in_b;
     }
     return in_b;

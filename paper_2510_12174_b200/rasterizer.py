@@ -494,6 +494,24 @@ def check_device_errors(device=None):
     check(_lib.lib().msplat_context_check(_Context.get(device).h))
 
 
+def set_stage_timing(enable: bool, device=None):
+    """Bracket every stage with CUDA events on the launching stream."""
+    check(_lib.lib().msplat_context_set_timing(_Context.get(device).h, int(enable)))
+
+
+def stage_timings(device=None) -> dict:
+    """{stage: (device ms summed since the last call, launches of the stage)}; synchronizing."""
+    ms = (ct.c_double * 8)()
+    calls = (ct.c_int64 * 8)()
+    check(_lib.lib().msplat_context_timings(_Context.get(device).h, ms, calls))
+    return {name: (ms[i], int(calls[i])) for i, name in enumerate(_lib.STAGES)}
+
+
+def kernel_launches() -> int:
+    """Process-wide count of kernels this library has launched."""
+    return int(_lib.lib().msplat_kernel_launches())
+
+
 # ------------------------------------------------------------ optimizer
 @dataclass
 class TrainConfig:

@@ -1,0 +1,279 @@
+"""Parity of the CUDA path (through the public API / C ABI) against the CPU
+oracle on identical inputs.
+
+Bars (BASELINE.json north star):
+  * tile key lists, per-tile order and ranges, prune masks: bit-exact;
+  * FP64 kernels: images ~1e-10, gradients ~1e-8 (rounding-order only);
+  * FP32 kernels: rendered channels max-abs <= 1e-4 relative to the channel's
+    range, gradients <= 1e-3 relative; pixels whose blend decisions flip
+    between FP32 and FP64 (alpha >= 1/255, T < 1e-4; visible as a different
+    contributor count or terminus) are counted and bounded separately.
+"""
+import numpy as np
+import pytest
+
+from helpers import GRAD_NAMES, frame_np, gpu_forward, grads_np, hwc_pix, rel_l2_err, rel_max_err, torch_pix
+from paper_2510_12174_b200 import scenes
+
+pytestmark = pytest.mark.gpu
+
+BG = {"background": (0.1, 0.2, 0.3)}
+
+
+def small_cases():
+    cams = [
+        {"fx": 30.0, "fy": 30.0, "cx": 16.0, "cy": 16.0, "width": 32, "height": 32, "R_c2w": np.eye(3),
+         "t_c2w": np.array([0.1, 0.0, -0.5])},
+        {"fx": 40.0, "fy": 36.0, "cx": 33.0, "cy": 21.0, "width": 70, "height": 45,
+         "R_c2w": scenes._rot_y(0.1) @ scenes._rot_x(-0.05), "t_c2w": np.array([-0.1, 0.05, -0.4])},
+    ]
+    out = []
+    for i, (n, C, deg) in enumerate([(150, 3, 1), (400, 5, 2), (250, 0, 0), (300, 2, 3)]):
+        out.append((scenes.make_random_scene(n, C, deg, seed=100 + i), cams[i % 2]))
+    return out
+
+
+CASES = small_cases()
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_preprocess_and_binning_bit_exact(port, case, dtype):
+    s, cam = CASES[case]
+    _, _, _, replay, _ = gpu_forward(s, cam, BG, dtype)
+    ref = port.preprocess(s, cam)
+    got = replay.splats()
+    assert np.array_equal(got["visible"], ref["visible"])
+    vis = ref["visible"].astype(bool)
+    # centre and depth involve no transcendental: identical FP64 op order -> identical bits
+    for k in ("center", "depth"):
+        assert np.array_equal(got[k][vis], ref[k][vis]), k
+    # radius and conic go through s = exp(log_scale): CUDA's and glibc's exp may
+    # round the last bit differently, so allow a few ulp (a tile-rect flip would
+    # need centre +- radius within 1 ulp of an integer; binning is checked exactly below)
+    for k in ("radius", "conic"):
+        a, b = got[k][vis], ref[k][vis]
+        ulps = np.abs(a - b) / np.spacing(np.abs(b))
+        print(f"{k}: {np.count_nonzero(ulps)} of {ulps.size} differ, max {ulps.max():.1f} ulp")
+        assert ulps.max() <= 8, k
+    off, vals = port.bin(ref["visible"], ref["center"], ref["radius"], ref["depth"], cam["width"], cam["height"])
+    goff, gvals = replay.bins()
+    assert np.array_equal(goff, off)
+    assert np.array_equal(gvals, vals)
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_forward_fp64_matches_oracle(port, case):
+    s, cam = CASES[case]
+    _, _, _, replay, frame = gpu_forward(s, cam, BG, "float64")
+    ref = port.render(s, cam, BG)
+    got = frame_np(frame)
+    assert np.array_equal(got["contributors"], ref["contributors"])
+    assert np.array_equal(replay.terminus(), ref["terminus"])
+    for k in ("color", "depth", "semantics", "kmap", "transmittance"):
+        assert rel_max_err(got[k], ref[k]) < 1e-10, k
+    ws = replay.weight_sums()
+    assert rel_max_err(ws, ref["weight_sums"]) < 1e-10
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_forward_fp32_within_tolerance(port, case):
+    s, cam = CASES[case]
+    _, _, _, replay, frame = gpu_forward(s, cam, BG, "float32")
+    ref = port.render(s, cam, BG)
+    got = frame_np(frame)
+    same = (got["contributors"] == ref["contributors"]) & (replay.terminus() == ref["terminus"])
+    flips = 1.0 - same.mean()
+    print(f"case {case}: decision-flip pixels {flips:.4%}")
+    assert flips < 0.01
+    for k in ("color", "depth", "kmap", "transmittance"):
+        e = rel_max_err(got[k], ref[k], same)
+        print(f"  {k}: {e:.2e}")
+        assert e < 1e-4, k
+    if s["num_classes"]:
+        e = rel_max_err(got["semantics"], ref["semantics"], np.broadcast_to(same[..., None], got["semantics"].shape))
+        assert e < 1e-4
+
+
+@pytest.mark.parametrize("dtype,tol", [("float64", 1e-8), ("float32", 1e-3)])
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_backward_matches_oracle(port, case, dtype, tol):
+    import torch
+    import paper_2510_12174_b200 as M
+    s, cam = CASES[case]
+    scene, view, rc, replay, frame = gpu_forward(s, cam, BG, dtype)
+    pix = scenes.pixel_grads(cam["width"], cam["height"], s["num_classes"], seed=case, scale=1.0)
+    dt = torch.float64 if dtype == "float64" else torch.float32
+    g = grads_np(M.rasterize_backward(scene, view, frame, replay, torch_pix(pix, dt)))
+    ref = port.backward(s, cam, hwc_pix(pix), BG)
+    for k in GRAD_NAMES:
+        if ref[k].size == 0:
+            continue
+        e = rel_l2_err(g[k], ref[k])
+        print(f"case {case} {dtype} {k}: rel L2 {e:.2e}")
+        assert e < tol, k
+
+
+@pytest.mark.parametrize("dtype,tol", [("float64", 1e-10), ("float32", 1e-4)])
+def test_normals_forward_and_backward(port, dtype, tol):
+    import torch
+    import paper_2510_12174_b200 as M
+    s = scenes.make_room_scene(20000, 3, 1, seed=5, width=96, height=64, f=60.0)
+    cam = scenes.view_camera(0, 96, 64, 60.0)
+    scene, view, rc, replay, frame = gpu_forward(s, cam, BG, dtype)
+    ref = port.render(s, cam, BG)
+    # feed the oracle's own depth/T so the comparison isolates the normal kernels
+    dt = torch.float64 if dtype == "float64" else torch.float32
+    depth = torch.as_tensor(ref["depth"], dtype=dt, device="cuda")
+    T = torch.as_tensor(ref["transmittance"], dtype=dt, device="cuda")
+    nc = M.NormalConfig()
+    nrm = torch.zeros(3, 64, 96, dtype=dt, device="cuda")
+    M.estimate_normals(depth, T, view, nc, nrm)
+    rn, valid, flipped = port.normals(ref["depth"], ref["transmittance"], cam)
+    got = scenes.planar_to_hwc(nrm.double().cpu().numpy())
+    assert valid.sum() > 1000
+    assert np.array_equal(np.abs(got).sum(-1) > 0, valid.astype(bool))
+    assert np.abs(got - rn).max() < (1e-10 if dtype == "float64" else 2e-4)
+    dN = scenes.pixel_grads(96, 64, 0, seed=3, scale=1.0)["dnormals"]
+    dD = M.normals_backward(torch.as_tensor(dN, dtype=dt, device="cuda"), depth, T, view, nc)
+    rdD = port.normals_backward(scenes.planar_to_hwc(dN).astype(np.float64), ref["depth"], ref["transmittance"], cam)
+    assert rel_max_err(dD.double().cpu().numpy(), rdD) < tol
+
+
+@pytest.mark.parametrize("dtype,tol", [("float64", 1e-8), ("float32", 1e-3)])
+def test_fused_fwd_bwd_unit(port, dtype, tol):
+    """msplat_fwd_bwd == rasterize, estimate_normals, normals_backward merged
+    into ddepth, rasterize_backward, chain_activations (trainer.cpp:295-309)."""
+    import torch
+    import paper_2510_12174_b200 as M
+    s = scenes.make_room_scene(30000, 6, 2, seed=11, width=128, height=96, f=90.0)
+    cam = scenes.view_camera(1, 128, 96, 90.0)
+    dt = torch.float64 if dtype == "float64" else torch.float32
+    scene = M.Scene.from_numpy(s, dtype=dt)
+    view = M.make_camera(cam["fx"], cam["fy"], cam["cx"], cam["cy"], 128, 96, cam["R_c2w"], cam["t_c2w"])
+    pix = scenes.pixel_grads(128, 96, 6, seed=4, scale=1.0)
+    frame = M.MultimodalFrame.empty(128, 96, 6, dt, "cuda")
+    grads = M.GradientBuffer.zeros_like_scene(scene)
+    replay = M.ReplayState()
+    for _ in range(2):  # second call takes the asynchronous path
+        M.fwd_bwd(scene, view, M.RenderConfig(**BG), M.NormalConfig(), frame, torch_pix(pix, dt), grads, replay)
+    M.rasterizer.check_device_errors()
+    fr, g_ref, _ = port.fwd_bwd(s, cam, hwc_pix(pix), BG)
+    g = grads_np(grads)
+    for k in GRAD_NAMES:
+        e = rel_l2_err(g[k], g_ref[k])
+        print(f"{dtype} {k}: rel L2 {e:.2e}")
+        assert e < tol, k
+    got_n = scenes.planar_to_hwc(frame.normals.double().cpu().numpy())
+    same = frame.contributors.cpu().numpy() == port.render(s, cam, BG)["contributors"]
+    assert np.abs(got_n - fr["normals"])[same].max() < (1e-9 if dtype == "float64" else 5e-3)
+
+
+def test_multiview_accumulation_is_sum_of_views(port):
+    """cfg4 semantics: the step gradient is the sum over views of per-view
+    rasterize_backward, chained once (chain_activations is linear)."""
+    import torch
+    import paper_2510_12174_b200 as M
+    s = scenes.make_room_scene(20000, 4, 1, seed=2, views=(0, 1, 2), width=96, height=64, f=70.0)
+    scene = M.Scene.from_numpy(s, dtype=torch.float64)
+    frame = M.MultimodalFrame.empty(96, 64, 4, torch.float64, "cuda")
+    grads = M.GradientBuffer.zeros_like_scene(scene)
+    replay = M.ReplayState()
+    total = None
+    for v in range(3):
+        cam = scenes.view_camera(v, 96, 64, 70.0)
+        view = M.make_camera(cam["fx"], cam["fy"], cam["cx"], cam["cy"], 96, 64, cam["R_c2w"], cam["t_c2w"])
+        pix = scenes.pixel_grads(96, 64, 4, seed=v, scale=1.0)
+        M.fwd_bwd(scene, view, M.RenderConfig(), M.NormalConfig(), frame, torch_pix(pix, torch.float64), grads,
+                  replay, chain=False, accumulate=v > 0)
+        _, gv, _ = port.fwd_bwd(s, cam, hwc_pix(pix), {})
+        gv = {k: x for k, x in gv.items()}
+        total = gv if total is None else {k: total[k] + gv[k] for k in total}
+    M.chain_activations(grads, scene)
+    g = grads_np(grads)
+    # oracle: per-view fwd_bwd already chained; chain is linear so sums agree
+    for k in GRAD_NAMES:
+        assert rel_l2_err(g[k], total[k]) < 1e-8, k
+
+
+def test_bin_and_sort_reference_kat():
+    """tests/test_rasterizer.cpp:35-88 on the device binning path."""
+    import paper_2510_12174_b200 as M
+    splats = [{"center": (16.0, 16.0), "radius": 100.0, "sort_depth": 2.0},
+              {"center": (4.0, 4.0), "radius": 2.0, "sort_depth": 1.0}]
+    bins = M.bin_and_sort(splats, 32, 32)
+    assert (bins.tiles_x, bins.tiles_y) == (2, 2)
+    assert all(0 in b for b in bins.bins)
+    assert bins.tile(0, 0) == [1, 0]
+    rng = np.random.default_rng(7)
+    rs = [{"center": (40 * rng.random() - 4, 40 * rng.random() - 4), "radius": 6 * rng.random(),
+           "sort_depth": rng.random()} for _ in range(100)]
+    rb = M.bin_and_sort(rs, 32, 32)
+    for ty in range(2):
+        for tx in range(2):
+            exp = []
+            for i, s in enumerate(rs):
+                x0 = max(0, int(np.floor(s["center"][0] - s["radius"])))
+                x1 = min(31, int(np.floor(s["center"][0] + s["radius"])))
+                y0 = max(0, int(np.floor(s["center"][1] - s["radius"])))
+                y1 = min(31, int(np.floor(s["center"][1] + s["radius"])))
+                if x1 < x0 or y1 < y0:
+                    continue
+                if x0 // 16 <= tx <= x1 // 16 and y0 // 16 <= ty <= y1 // 16:
+                    exp.append(i)
+            exp.sort(key=lambda i: (rs[i]["sort_depth"], i))
+            assert rb.tile(tx, ty) == exp
+
+
+def test_scene_modified_since_forward_is_detected():
+    import torch
+    import paper_2510_12174_b200 as M
+    s = scenes.make_random_scene(5, 1, 0, seed=117)
+    cam = scenes.simple_camera()
+    scene, view, rc, replay, frame = gpu_forward(s, cam, {}, "float64")
+    scene.means[2, 0] += 0.5
+    pix = M.PixelGradients.zero(16, 16, 1, dtype=torch.float64)
+    with pytest.raises(RuntimeError, match="modified"):
+        M.rasterize_backward(scene, view, frame, replay, pix)
+
+
+def test_non_finite_and_zero_quaternion_primitives_raise():
+    import paper_2510_12174_b200 as M
+    s = scenes.make_random_scene(10, 2, 1, seed=1)
+    s["means"][7, 2] = np.nan
+    with pytest.raises(ValueError, match="primitive 7"):
+        gpu_forward(s, scenes.simple_camera(), {}, "float32")
+    s = scenes.make_random_scene(10, 2, 1, seed=1)
+    s["quats"][3] = 0
+    with pytest.raises(ValueError, match="primitive 3"):
+        gpu_forward(s, scenes.simple_camera(), {}, "float32")
+    with pytest.raises(ValueError, match="sh_degree"):
+        M.Scene.from_numpy(dict(scenes.make_random_scene(3, 1, 1), sh_degree=4))._abi()
+
+
+def test_adam_and_prune_match_oracle(port):
+    import torch
+    import paper_2510_12174_b200 as M
+    s = scenes.make_random_scene(500, 5, 2, seed=9)
+    scene = M.Scene.from_numpy(s, dtype=torch.float64)
+    rng = np.random.default_rng(0)
+    gd = {k: rng.normal(size=getattr(scene, f).shape) for k, f in
+          zip(GRAD_NAMES, ("means", "quats", "log_scales", "opacity_logits", "sh", "semantics", "k"))}
+    g = M.GradientBuffer(*(torch.as_tensor(gd[k], device="cuda") for k in GRAD_NAMES), raw_space=True)
+    st = M.OptimizerState.init(scene)
+    tc = M.TrainConfig()
+    zeros = {k: np.zeros_like(v) for k, v in gd.items()}
+    p_ref, m_ref, v_ref = port.adam(s, gd, zeros, zeros, 1, [tc.lr_position, tc.lr_rotation, tc.lr_scale,
+                                                             tc.lr_opacity, tc.lr_sh, tc.lr_semantics, tc.lr_k])
+    M.adam_step(scene, g, st, tc)
+    for f in ("means", "quats", "log_scales", "opacity_logits", "sh", "semantics", "k"):
+        assert np.allclose(getattr(scene, f).cpu().numpy(), p_ref[f], rtol=1e-13, atol=1e-15), f
+    k = rng.uniform(0, 2, 5000)
+    for keep_small in (False, True):
+        sc = M.Scene.from_numpy(dict(scenes.make_random_scene(5000, 1, 0, seed=3), k=k), dtype=torch.float64)
+        st2 = M.OptimizerState.init(sc)
+        mask_ref = port.prune_mask(k, 0.5, keep_small)
+        removed = M.prune(sc, st2, M.TrainConfig(prune_keep_small=keep_small))
+        assert removed == int((~mask_ref).sum())
+        assert sc.size() == int(mask_ref.sum())
+        assert np.all(sc.k.cpu().numpy() == 0.9)
