@@ -154,7 +154,41 @@ __global__ void __launch_bounds__(kThreads) backward_kernel(const BackwardArgs<R
                 if (dd != Real(0)) {
                     const HitEval<Real> h = intersect<Real>(br, ray, a.cam, a.raw, g);
                     if (h.hit) {
-                        if (!(fabs(double(h.a)) < 1e-12)) {
+                        if constexpr (sizeof(Real) == 4) {
+                            // Same adjoint, rewritten around the small midpoint offset
+                            // p_l = v_l + t d_l (p_s = p_l / axes) so nothing cancels:
+                            //   g_vs = -k d_s, g_ds = -k (p_s + t d_s), k = g_t / a
+                            //   dscale = 2k (d_s o p_s) / s
+                            //   dR = v g_vl^T + d g_dl^T = -k [(R p_l)(d_s/axes)^T + d (p_s/axes)^T]
+                            if (!(fabsf(h.a) < 1e-12f)) {
+                                const Real kk = dd * ray.dz / h.a;
+                                const Real t = h.t_mid;
+                                Real ps[3], pl[3], ga[3], gb[3];
+#pragma unroll
+                                for (int i = 0; i < 3; ++i) {
+                                    pl[i] = br.vl[i] + t * h.dl[i];
+                                    ps[i] = pl[i] * br.inv_axes[i];
+                                    v[13 + i] = Real(2) * kk * h.ds[i] * ps[i] * sigma * br.inv_axes[i];
+                                    ga[i] = h.ds[i] * br.inv_axes[i];  // -g_vl / k
+                                    gb[i] = ps[i] * br.inv_axes[i];
+                                }
+                                Real Rp[3];
+#pragma unroll
+                                for (int i = 0; i < 3; ++i) {
+                                    // dposition = -(R g_vl) = k R (d_s/axes); R = Rt^T
+                                    v[6 + i] = kk * (br.Rt[0 * 3 + i] * ga[0] + br.Rt[1 * 3 + i] * ga[1] +
+                                                     br.Rt[2 * 3 + i] * ga[2]);
+                                    Rp[i] = br.Rt[0 * 3 + i] * pl[0] + br.Rt[1 * 3 + i] * pl[1] +
+                                            br.Rt[2 * 3 + i] * pl[2];
+                                }
+                                Real G[9];
+#pragma unroll
+                                for (int r = 0; r < 3; ++r)
+#pragma unroll
+                                    for (int c = 0; c < 3; ++c) G[r * 3 + c] = -kk * (Rp[r] * ga[c] + ray.d[r] * gb[c]);
+                                quat_rotation_backward<Real>(br.q, G, v + 9);
+                            }
+                        } else if (!(fabs(double(h.a)) < 1e-12)) {
                             const Real g_t = dd * ray.dz;
                             Real gvs[3], gds[3], gvl[3], gdl[3];
                             const Real inv_a = Real(1) / h.a;

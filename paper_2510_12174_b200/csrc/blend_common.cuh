@@ -83,7 +83,8 @@ template <typename Real>
 struct HitEval {
     bool hit;
     Real t_mid, a, b;
-    Real ds[3];
+    Real ds[3];       // d_s = d_l / axes
+    Real dl[3];       // d_l = R^T d (unscaled local direction)
     Real depth_fp64;  // set when the FP64 re-decision ran (< 0 otherwise)
 };
 
@@ -199,14 +200,32 @@ __device__ __forceinline__ HitEval<Real> intersect(const BlendRec<Real>& g, cons
         else
             h.ds[i] = dl[i] * g.inv_axes[i];
     }
+    for (int i = 0; i < 3; ++i) h.dl[i] = dl[i];
     h.a = h.ds[0] * h.ds[0] + h.ds[1] * h.ds[1] + h.ds[2] * h.ds[2];
-    const Real vd = g.vs[0] * h.ds[0] + g.vs[1] * h.ds[1] + g.vs[2] * h.ds[2];
-    h.b = Real(2) * vd;
-    const Real disc = h.b * h.b - Real(4) * h.a * g.csq;
-    if constexpr (sizeof(Real) == 4) {
-        const Real mag = h.b * h.b + fabsf(Real(4) * h.a * g.csq);
-        const Real vmag = sqrtf((g.vs[0] * g.vs[0] + g.vs[1] * g.vs[1] + g.vs[2] * g.vs[2]) * h.a);
-        if (fabsf(disc) <= Real(1e-4) * mag || fabsf(vd) <= Real(1e-4) * vmag) {
+    if constexpr (sizeof(Real) == 8) {
+        // The reference's own formulation (geometry.cpp:44-58).
+        const Real vd = g.vs[0] * h.ds[0] + g.vs[1] * h.ds[1] + g.vs[2] * h.ds[2];
+        h.b = Real(2) * vd;
+        const Real disc = h.b * h.b - Real(4) * h.a * g.csq;
+        if (disc < Real(0) || h.a <= Real(0)) return h;
+        h.t_mid = -h.b / (Real(2) * h.a);
+    } else {
+        // disc/4 = (v_s.d_s)^2 - |d_s|^2 (|v_s|^2 - 1) = |d_s|^2 - |v_s x d_s|^2 (Lagrange
+        // identity).  For flat splats |v_s| ~ 1e3, so b^2 and 4ac agree to ~1e-7
+        // and the textbook form has no correct FP32 digit; the cross product is
+        // taken in unscaled local space (v_l x d_l) where it is well conditioned:
+        //   (v_s x d_s)_i = (v_l x d_l)_i / (axes_j axes_k).
+        const Real* ia = g.inv_axes;
+        const Real w0 = g.vl[1] * dl[2] - g.vl[2] * dl[1];
+        const Real w1 = g.vl[2] * dl[0] - g.vl[0] * dl[2];
+        const Real w2 = g.vl[0] * dl[1] - g.vl[1] * dl[0];
+        const Real c0 = w0 * ia[1] * ia[2], c1 = w1 * ia[0] * ia[2], c2 = w2 * ia[0] * ia[1];
+        const Real disc4 = h.a - (c0 * c0 + c1 * c1 + c2 * c2);
+        const Real vd = g.vl[0] * dl[0] * ia[0] * ia[0] + g.vl[1] * dl[1] * ia[1] * ia[1] +
+                        g.vl[2] * dl[2] * ia[2] * ia[2];
+        // Decisions within FP32 noise of the boundary are re-taken in FP64 exactly
+        // as the reference computes them (rare: grazing rays / camera on the shell).
+        if (fabsf(disc4) <= Real(1e-4) * h.a || fabsf(vd) <= Real(1e-4) * sqrtf(h.a * (g.csq + Real(1)))) {
             double t, a, b, ds[3], dep;
             if (!intersect_fp64<Real>(cam, rp, gid, r.px, r.py, &t, &a, &b, ds, &dep)) return h;
             h.hit = true;
@@ -217,9 +236,10 @@ __device__ __forceinline__ HitEval<Real> intersect(const BlendRec<Real>& g, cons
             h.depth_fp64 = Real(dep);
             return h;
         }
+        h.b = Real(2) * vd;
+        if (disc4 < Real(0) || h.a <= Real(0)) return h;
+        h.t_mid = -vd / h.a;
     }
-    if (disc < Real(0) || h.a <= Real(0)) return h;
-    h.t_mid = -h.b / (Real(2) * h.a);
     if (h.t_mid <= Real(0)) return h;
     h.hit = true;
     return h;

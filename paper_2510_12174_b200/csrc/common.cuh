@@ -86,7 +86,7 @@ struct BlendRec {
     Real k;           // gradient factor
     Real hit_ok;      // 0 when an axis is degenerate (< 1e-8): never intersects
     Real q[4];        // unit quaternion (w,x,y,z) of the activated rotation
-    Real pad[3];
+    Real vl[3];       // v_l = R^T (o - mu), unscaled local camera offset (per view)
 };
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }

@@ -222,11 +222,12 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs<Real> a)
     if (axes[1] < amin) amin = axes[1];
     if (axes[2] < amin) amin = axes[2];
     const double rel[3] = {c.tc2w[0] - mu[0], c.tc2w[1] - mu[1], c.tc2w[2] - mu[2]};
-    double vs[3];
+    double vs[3], vl[3];
     for (int j = 0; j < 3; ++j) {
         double t = R[0 * 3 + j] * rel[0];
         t += R[1 * 3 + j] * rel[1];
         t += R[2 * 3 + j] * rel[2];
+        vl[j] = t;
         vs[j] = t / axes[j];
     }
     const double csq = dot3(vs, vs) - 1.0;
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs<Real> a)
         br.inv_axes[j] = Real(1.0 / axes[j]);
         br.vs[j] = Real(vs[j]);
         br.rgb[j] = Real(rgb[j]);
-        br.pad[j] = Real(0);
+        br.vl[j] = Real(vl[j]);
     }
     br.csq = Real(csq);
     br.zc = Real(z);
