@@ -1,305 +1,12 @@
-// K9: per-tile reverse blend (rasterize_backward's tile loop,
-// core/src/rasterizer_backward.cpp:140-255, with intersection_backward
-// core/src/geometry.cpp:70-105 and quat_rotation_backward :17-29).
 // K10: per-Gaussian projection / SH adjoint (projection_backward,
-// rasterizer_backward.cpp:57-123; eval_sh_color_backward, sh.cpp:86-99) with
-// chain_activations (scene.cpp:108-129) and check_finite (scene.cpp:97-106)
-// fused.  Plus check_replay's scene comparison (rasterizer_backward.cpp:40-44).
-//
-// K9 layout: one CTA per tile, one thread per pixel (8x4 pixel block per warp).
-// Each pixel replays its list from terminus-1 down to 0 with the forward's
-// alpha test, restores T by division, and forms the reference's per-pair
-// gradients.  Two reductions replace the reference's per-thread accumulators:
-//   * "seed-linear" gradients (dcolor, dk, dsemantics = w * seed of the pixel)
-//     are reduced channel-parallel: lane ch sums w_L * seed_L[ch] over the
-//     blending lanes L of the warp (seeds staged once per tile in shared
-//     memory, pixel-major rows), then one coalesced atomic per channel;
-//   * the 16 "geometric" gradients (dopacity, dmean2d, dconic, and the depth
-//     chain's dposition/drotation/dscale) are written per lane to a per-warp
-//     shared scratch row and summed by lanes 0..15, one atomic each.
-// Per (warp, Gaussian) event that is O(active lanes) work instead of a
-// 5-level shuffle tree per value.
-// The semantic part of dalpha uses the scalar recursion
-//   A <- a_last * (sem_last . dO) + (1 - a_last) * A
-// which equals sum_ch accum_sem[ch] * dO[ch] of the reference (:224-231).
+// core/src/rasterizer_backward.cpp:57-123; eval_sh_color_backward, sh.cpp:86-99)
+// with chain_activations (scene.cpp:108-129) and check_finite
+// (scene.cpp:97-106) fused; the standalone chain kernel; check_replay's scene
+// comparison (rasterizer_backward.cpp:40-44).  K9 lives in backward_blend.cu.
 #include "blend_common.cuh"
 #include "kernels.h"
 
 namespace msplat_cuda {
-
-namespace {
-
-constexpr int kBatch = 256;
-constexpr int kThreads = 256;
-constexpr int kGeo = 16;         // geometric values per pair
-constexpr int kRedPitch = kGeo + 1;  // + w, odd pitch
-
-__host__ __device__ inline int seed_pitch(int C) { return (C + 4) | 1; }
-
-template <typename Real>
-size_t backward_smem_bytes(int C) {
-    return sizeof(AlphaRec<Real>) * kBatch + sizeof(uint32_t) * kBatch +
-           sizeof(Real) * size_t(kTilePixels) * seed_pitch(C) +
-           sizeof(Real) * 8 * 32 * kRedPitch + 16;
-}
-
-template <typename Real>
-__device__ __forceinline__ void quat_rotation_backward(const Real* q, const Real* G, Real* dq) {
-    const Real w = q[0], x = q[1], y = q[2], z = q[3];
-#define g(i, j) G[(i)*3 + (j)]
-    dq[0] = Real(2) * (g(0, 1) * (-z) + g(0, 2) * y + g(1, 0) * z + g(1, 2) * (-x) + g(2, 0) * (-y) +
-                       g(2, 1) * x);
-    dq[1] = Real(2) * (g(0, 1) * y + g(0, 2) * z + g(1, 0) * y + g(1, 1) * (-2 * x) + g(1, 2) * (-w) +
-                       g(2, 0) * z + g(2, 1) * w + g(2, 2) * (-2 * x));
-    dq[2] = Real(2) * (g(0, 0) * (-2 * y) + g(0, 1) * x + g(0, 2) * w + g(1, 0) * x + g(1, 2) * z +
-                       g(2, 0) * (-w) + g(2, 1) * z + g(2, 2) * (-2 * y));
-    dq[3] = Real(2) * (g(0, 0) * (-2 * z) + g(0, 1) * (-w) + g(0, 2) * x + g(1, 0) * w +
-                       g(1, 1) * (-2 * z) + g(1, 2) * y + g(2, 0) * x + g(2, 1) * y);
-#undef g
-}
-
-}  // namespace
-
-template <typename Real>
-__global__ void __launch_bounds__(kThreads) backward_kernel(const BackwardArgs<Real> a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    AlphaRec<Real>* s_rec = reinterpret_cast<AlphaRec<Real>*>(smem_raw);
-    uint32_t* s_gid = reinterpret_cast<uint32_t*>(s_rec + kBatch);
-    Real* s_seed = reinterpret_cast<Real*>(s_gid + kBatch);      // [256][seed_pitch]
-    const int C = a.C, sp = seed_pitch(C), S = C + 4;
-    Real* s_red = s_seed + size_t(kTilePixels) * sp;              // [8][32][kRedPitch]
-    int* s_maxterm = reinterpret_cast<int*>(s_red + 8 * 32 * kRedPitch);
-
-    const int tile = blockIdx.x;
-    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int x = tx * kTile + tile_pixel_x(warp, lane);
-    const int y = ty * kTile + tile_pixel_y(warp, lane);
-    const int pl = tile_pixel_index(warp, lane);
-    const bool inside = x < a.W && y < a.H;
-    const size_t HW = size_t(a.W) * a.H, p = size_t(y) * a.W + x;
-    if (threadIdx.x == 0) *s_maxterm = 0;
-
-    // Per-pixel seeds: dC, dK and dO into shared memory; dD in a register.
-    Real* my_seed = s_seed + size_t(pl) * sp;
-    int term = 0;
-    Real T_final = Real(1), dD = Real(0);
-    bool any = false;
-    if (inside) {
-        term = a.terminus[p];
-        T_final = a.T_final[p];
-        dD = a.ddepth[p];
-        for (int ch = 0; ch < 3; ++ch) {
-            my_seed[ch] = a.dcolor[ch * HW + p];
-            any |= my_seed[ch] != Real(0);
-        }
-        my_seed[3] = a.dkmap[p];
-        any |= my_seed[3] != Real(0) || dD != Real(0);
-        for (int ch = 0; ch < C; ++ch) {
-            my_seed[4 + ch] = a.dsem[size_t(ch) * HW + p];
-            any |= my_seed[4 + ch] != Real(0);
-        }
-    } else {
-        for (int ch = 0; ch < S; ++ch) my_seed[ch] = Real(0);
-    }
-    // rasterize_backward.cpp:156-171: nothing to do without blends or seeds.
-    const bool active_px = inside && term > 0 && any;
-    if (!active_px) term = 0;
-    __syncthreads();
-    if (term > 0) atomicMax(s_maxterm, term);
-    __syncthreads();
-    const int maxterm = *s_maxterm;
-    if (maxterm == 0) return;
-
-    const PixelRay<Real> ray = make_ray<Real>(a.cam, x, y);
-    const Real dC0 = my_seed[0], dC1 = my_seed[1], dC2 = my_seed[2], dK = my_seed[3];
-    const Real bg_dot = Real(a.rp.bg[0]) * dC0 + Real(a.rp.bg[1]) * dC1 + Real(a.rp.bg[2]) * dC2;
-    const Real sigma = Real(a.rp.sigma_scale);
-    Real T = T_final;
-    Real ac0 = 0, ac1 = 0, ac2 = 0, lc0 = 0, lc1 = 0, lc2 = 0;
-    Real acc_k = 0, last_k = 0, acc_sd = 0, last_sd = 0, last_alpha = 0;
-    Real* my_red = s_red + size_t(warp * 32 + lane) * kRedPitch;
-    const Real* warp_red = s_red + size_t(warp * 32) * kRedPitch;
-
-    const uint2 range = a.tile_range[tile];
-    const uint32_t list_end = range.x + uint32_t(maxterm);
-    for (int64_t bend = int64_t(list_end); bend > int64_t(range.x); bend -= kBatch) {
-        const uint32_t bstart = uint32_t(max(int64_t(range.x), bend - kBatch));
-        const int nb = int(uint32_t(bend) - bstart);
-        __syncthreads();
-        if (int(threadIdx.x) < nb) {
-            const uint32_t g = a.inst_gauss[bstart + threadIdx.x];
-            s_gid[threadIdx.x] = g;
-            s_rec[threadIdx.x] = a.arec[g];
-        }
-        __syncthreads();
-        for (int j = nb - 1; j >= 0; --j) {
-            const int pos = int(bstart - range.x) + j;  // index in the tile list
-            AlphaEval<Real> ae;
-            ae.pass = false;
-            if (pos < term) ae = eval_alpha<Real>(s_rec[j], ray.px, ray.py);
-            const unsigned mask = __ballot_sync(0xffffffffu, ae.pass);
-            if (mask == 0) continue;
-            const uint32_t g = s_gid[j];
-            if (ae.pass) {
-                Real v[kRedPitch];
-#pragma unroll
-                for (int i = 0; i < kRedPitch; ++i) v[i] = Real(0);
-                T = T / (Real(1) - ae.alpha);
-                const Real w = ae.alpha * T;
-                v[kGeo] = w;
-                const BlendRec<Real> br = a.brec[g];
-                // Depth chain (rasterizer_backward.cpp:205-218).
-                const Real dd = dD * w;
-                if (dd != Real(0)) {
-                    const HitEval<Real> h = intersect<Real>(br, ray, a.cam, a.raw, g);
-                    if (h.hit) {
-                        if constexpr (sizeof(Real) == 4) {
-                            // Same adjoint, rewritten around the small midpoint offset
-                            // p_l = v_l + t d_l (p_s = p_l / axes) so nothing cancels:
-                            //   g_vs = -k d_s, g_ds = -k (p_s + t d_s), k = g_t / a
-                            //   dscale = 2k (d_s o p_s) / s
-                            //   dR = v g_vl^T + d g_dl^T = -k [(R p_l)(d_s/axes)^T + d (p_s/axes)^T]
-                            if (!(fabsf(h.a) < 1e-12f)) {
-                                const Real kk = dd * ray.dz / h.a;
-                                const Real t = h.t_mid;
-                                Real ps[3], pl[3], ga[3], gb[3];
-#pragma unroll
-                                for (int i = 0; i < 3; ++i) {
-                                    pl[i] = br.vl[i] + t * h.dl[i];
-                                    ps[i] = pl[i] * br.inv_axes[i];
-                                    v[13 + i] = Real(2) * kk * h.ds[i] * ps[i] * sigma * br.inv_axes[i];
-                                    ga[i] = h.ds[i] * br.inv_axes[i];  // -g_vl / k
-                                    gb[i] = ps[i] * br.inv_axes[i];
-                                }
-                                Real Rp[3];
-#pragma unroll
-                                for (int i = 0; i < 3; ++i) {
-                                    // dposition = -(R g_vl) = k R (d_s/axes); R = Rt^T
-                                    v[6 + i] = kk * (br.Rt[0 * 3 + i] * ga[0] + br.Rt[1 * 3 + i] * ga[1] +
-                                                     br.Rt[2 * 3 + i] * ga[2]);
-                                    Rp[i] = br.Rt[0 * 3 + i] * pl[0] + br.Rt[1 * 3 + i] * pl[1] +
-                                            br.Rt[2 * 3 + i] * pl[2];
-                                }
-                                Real G[9];
-#pragma unroll
-                                for (int r = 0; r < 3; ++r)
-#pragma unroll
-                                    for (int c = 0; c < 3; ++c) G[r * 3 + c] = -kk * (Rp[r] * ga[c] + ray.d[r] * gb[c]);
-                                quat_rotation_backward<Real>(br.q, G, v + 9);
-                            }
-                        } else if (!(fabs(double(h.a)) < 1e-12)) {
-                            const Real g_t = dd * ray.dz;
-                            Real gvs[3], gds[3], gvl[3], gdl[3];
-                            const Real inv_a = Real(1) / h.a;
-                            const Real ba2 = h.b / (h.a * h.a);
-#pragma unroll
-                            for (int i = 0; i < 3; ++i) {
-                                gvs[i] = g_t * (-h.ds[i] * inv_a);
-                                gds[i] = g_t * (ba2 * h.ds[i] - br.vs[i] * inv_a);
-                                // ds = -(g_vs o v_s + g_ds o d_s) / s,  s = axes / sigma
-                                v[13 + i] = -((gvs[i] * br.vs[i] + gds[i] * h.ds[i]) * sigma * br.inv_axes[i]);
-                                gvl[i] = gvs[i] * br.inv_axes[i];
-                                gdl[i] = gds[i] * br.inv_axes[i];
-                            }
-                            // dposition = -(R g_vl); R = Rt^T.
-                            Real vv[3];
-#pragma unroll
-                            for (int i = 0; i < 3; ++i) {
-                                v[6 + i] = -(br.Rt[0 * 3 + i] * gvl[0] + br.Rt[1 * 3 + i] * gvl[1] +
-                                             br.Rt[2 * 3 + i] * gvl[2]);
-                                // v = o - mu = R (v_s o axes)
-                                vv[i] = br.Rt[0 * 3 + i] * (br.vs[0] * br.axes[0]) +
-                                        br.Rt[1 * 3 + i] * (br.vs[1] * br.axes[1]) +
-                                        br.Rt[2 * 3 + i] * (br.vs[2] * br.axes[2]);
-                            }
-                            Real G[9];
-#pragma unroll
-                            for (int r = 0; r < 3; ++r)
-#pragma unroll
-                                for (int c = 0; c < 3; ++c) G[r * 3 + c] = vv[r] * gvl[c] + ray.d[r] * gdl[c];
-                            quat_rotation_backward<Real>(br.q, G, v + 9);
-                        }
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 3; ++i) v[6 + i] = dd * Real(a.cam.Rw2c[6 + i]);
-                    }
-                }
-                // Alpha gradient (rasterizer_backward.cpp:222-244); depth excluded.
-                ac0 = last_alpha * lc0 + (Real(1) - last_alpha) * ac0;
-                ac1 = last_alpha * lc1 + (Real(1) - last_alpha) * ac1;
-                ac2 = last_alpha * lc2 + (Real(1) - last_alpha) * ac2;
-                acc_k = last_alpha * last_k + (Real(1) - last_alpha) * acc_k;
-                acc_sd = last_alpha * last_sd + (Real(1) - last_alpha) * acc_sd;
-                Real sd = Real(0);
-                {
-                    const Real* semg = a.semantics + size_t(g) * C;
-                    const Real* dO = my_seed + 4;
-                    for (int ch = 0; ch < C; ++ch) sd += semg[ch] * dO[ch];
-                }
-                Real dalpha = ((br.rgb[0] - ac0) * dC0 + (br.rgb[1] - ac1) * dC1 + (br.rgb[2] - ac2) * dC2) * T;
-                dalpha += (br.k - acc_k) * dK * T;
-                dalpha += (sd - acc_sd) * T;
-                dalpha -= (T_final / (Real(1) - ae.alpha)) * bg_dot;
-                if (!ae.clamped) {
-                    v[0] = ae.gauss * dalpha;
-                    const Real dpower = ae.alpha * dalpha;
-                    const AlphaRec<Real>& ar = s_rec[j];
-                    v[1] = dpower * (ar.ca * ae.dx + ar.cb * ae.dy);
-                    v[2] = dpower * (ar.cb * ae.dx + ar.cc * ae.dy);
-                    v[3] = dpower * (Real(-0.5) * ae.dx * ae.dx);
-                    v[4] = dpower * (Real(-0.5) * ae.dx * ae.dy);
-                    v[5] = dpower * (Real(-0.5) * ae.dy * ae.dy);
-                }
-                lc0 = br.rgb[0];
-                lc1 = br.rgb[1];
-                lc2 = br.rgb[2];
-                last_k = br.k;
-                last_sd = sd;
-                last_alpha = ae.alpha;
-#pragma unroll
-                for (int i = 0; i < kRedPitch; ++i) my_red[i] = v[i];
-            }
-            __syncwarp();
-            // Geometric reduction: lane i < 16 sums value i over blending lanes.
-            if (lane < kGeo) {
-                Real s = Real(0);
-                unsigned m = mask;
-                while (m) {
-                    const int L = __ffs(m) - 1;
-                    m &= m - 1;
-                    s += warp_red[L * kRedPitch + lane];
-                }
-                if (s != Real(0)) {
-                    Real* dst;
-                    if (lane == 0) dst = a.g_opac + g;
-                    else if (lane < 3) dst = a.acc_dmean + size_t(g) * 2 + (lane - 1);
-                    else if (lane < 6) dst = a.acc_dconic + size_t(g) * 3 + (lane - 3);
-                    else if (lane < 9) dst = a.g_pos + size_t(g) * 3 + (lane - 6);
-                    else if (lane < 13) dst = a.g_rot + size_t(g) * 4 + (lane - 9);
-                    else dst = a.g_scale + size_t(g) * 3 + (lane - 13);
-                    atomicAdd(dst, s);
-                }
-            }
-            // Seed-linear reduction, channel-parallel.
-            for (int ch = lane; ch < S; ch += 32) {
-                Real s = Real(0);
-                unsigned m = mask;
-                while (m) {
-                    const int L = __ffs(m) - 1;
-                    m &= m - 1;
-                    s += warp_red[L * kRedPitch + kGeo] * s_seed[size_t(tile_pixel_index(warp, L)) * sp + ch];
-                }
-                if (s != Real(0)) {
-                    Real* dst = ch < 3 ? a.acc_dcolor + size_t(g) * 3 + ch
-                                       : (ch == 3 ? a.g_k + g : a.g_sem + size_t(g) * C + (ch - 4));
-                    atomicAdd(dst, s);
-                }
-            }
-            __syncwarp();
-        }
-    }
-}
 
 // ------------------------------------------------------------------ K10
 template <typename Real>
@@ -521,18 +228,6 @@ __global__ void check_replay_kernel(int64_t n, const Real* __restrict__ means, c
 }
 
 template <typename Real>
-void launch_backward_blend(const BackwardArgs<Real>& a, int ntiles, cudaStream_t s) {
-    if (ntiles == 0) return;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(backward_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        configured = true;
-    }
-    backward_kernel<Real><<<ntiles, kThreads, backward_smem_bytes<Real>(a.C), s>>>(a);
-    count_launches(1);
-}
-
-template <typename Real>
 void launch_projection_backward(const ProjBackwardArgs<Real>& a, cudaStream_t s) {
     if (a.n == 0) return;
     projection_backward_kernel<Real><<<unsigned((a.n + 255) / 256), 256, 0, s>>>(a);
@@ -556,7 +251,6 @@ void launch_check_replay(int64_t n, const Real* means, const Real* k, const Real
 }
 
 #define MSPLAT_INST(R)                                                                                  \
-    template void launch_backward_blend<R>(const BackwardArgs<R>&, int, cudaStream_t);                 \
     template void launch_projection_backward<R>(const ProjBackwardArgs<R>&, cudaStream_t);             \
     template void launch_chain<R>(int64_t, const R*, const R*, const R*, R*, R*, R*, cudaStream_t);     \
     template void launch_check_replay<R>(int64_t, const R*, const R*, const R*, const R*, DeviceError*, \

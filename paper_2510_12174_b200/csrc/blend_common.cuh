@@ -256,6 +256,23 @@ __device__ __forceinline__ Real midpoint_depth(const Cam& c, const PixelRay<Real
     }
 }
 
+// quat_rotation_backward (core/src/geometry.cpp:17-29): dL/dR -> dL/d(unit q),
+// before the tangent projection of chain_activations.
+template <typename Real>
+__device__ __forceinline__ void quat_rotation_backward(const Real* q, const Real* G, Real* dq) {
+    const Real w = q[0], x = q[1], y = q[2], z = q[3];
+#define g(i, j) G[(i)*3 + (j)]
+    dq[0] = Real(2) * (g(0, 1) * (-z) + g(0, 2) * y + g(1, 0) * z + g(1, 2) * (-x) + g(2, 0) * (-y) +
+                       g(2, 1) * x);
+    dq[1] = Real(2) * (g(0, 1) * y + g(0, 2) * z + g(1, 0) * y + g(1, 1) * (-2 * x) + g(1, 2) * (-w) +
+                       g(2, 0) * z + g(2, 1) * w + g(2, 2) * (-2 * x));
+    dq[2] = Real(2) * (g(0, 0) * (-2 * y) + g(0, 1) * x + g(0, 2) * w + g(1, 0) * x + g(1, 2) * z +
+                       g(2, 0) * (-w) + g(2, 1) * z + g(2, 2) * (-2 * y));
+    dq[3] = Real(2) * (g(0, 0) * (-2 * z) + g(0, 1) * (-w) + g(0, 2) * x + g(1, 0) * w +
+                       g(1, 1) * (-2 * z) + g(1, 2) * y + g(2, 0) * x + g(2, 1) * y);
+#undef g
+}
+
 // Tile-local pixel coordinates: warps cover 8x4 pixel blocks, 2 across x 4 down.
 __device__ __forceinline__ int tile_pixel_x(int warp, int lane) { return (warp & 1) * 8 + (lane & 7); }
 __device__ __forceinline__ int tile_pixel_y(int warp, int lane) { return (warp >> 1) * 4 + (lane >> 3); }

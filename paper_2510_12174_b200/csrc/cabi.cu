@@ -285,7 +285,7 @@ msplat_status size_replay(msplat_replay* r, int dtype, int64_t n, int C, int deg
     const int64_t tiles = int64_t(r->tiles_x) * r->tiles_y;
     const size_t nn = size_t(std::max<int64_t>(n, 1));
     if (r->inst_cap == 0) r->inst_cap = std::max<int64_t>(int64_t(1) << 20, 4 * n);
-    CUDA_TRY(r->arec.ensure(nn * 8 * R));
+    CUDA_TRY(r->arec.ensure(nn * sizeof(AlphaRec<double>) / 8 * R));
     CUDA_TRY(r->brec.ensure(nn * 32 * R));
     CUDA_TRY(r->visible.ensure(nn));
     CUDA_TRY(r->clamped.ensure(nn));

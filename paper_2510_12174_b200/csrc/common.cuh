@@ -62,14 +62,18 @@ struct Vec3T {
 };
 
 // Per-visible-Gaussian records written by K1 and gathered per tile by K6/K9.
-// Alpha-test record (everything a visited pair needs), 8 Reals.
+// Alpha-test record (everything a visited pair needs), 12 Reals.
 template <typename Real>
 struct AlphaRec {
     Real cx, cy;      // splat centre (pixels)
     Real ca, cb, cc;  // conic (xx, xy, yy)
     Real opacity;     // activated alpha (logistic of the logit)
-    Real log_thr;     // log(1/(255*opacity)): power >= log_thr  <=>  alpha >= 1/255 (fp32 path)
+    Real log_thr;     // log(1/(255*opacity)): power >= log_thr  <=>  alpha >= 1/255
     Real pad;
+    // Conservative pixel-space box of the alpha >= 1/255 support (the ellipse
+    // power >= log_thr - 1e-3 grown by 0.1% + 1e-3 px).  Used only to skip
+    // pairs that would fail the alpha test anyway: results are unchanged.
+    Real bx0, bx1, by0, by1;
 };
 
 // Blend record (everything a blended pair needs beyond the alpha test).

@@ -239,8 +239,24 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs<Real> a)
     ar.cb = Real(cb);
     ar.cc = Real(cc);
     ar.opacity = Real(opacity);
-    ar.log_thr = Real(log(1.0 / (255.0 * opacity)));
+    const double log_thr = log(1.0 / (255.0 * opacity));
+    ar.log_thr = Real(log_thr);
     ar.pad = Real(0);
+    {
+        // d^T conic d <= r2 with r2 = -2 (log_thr - 1e-3); the tight box of that
+        // ellipse has half-widths sqrt(r2 cov_xx), sqrt(r2 cov_yy) (cov = conic^-1).
+        const double r2 = -2.0 * (log_thr - 1e-3);
+        if (r2 > 0) {
+            const double hx = sqrt(r2 * cov[0]) * 1.001 + 1e-3, hy = sqrt(r2 * cov[3]) * 1.001 + 1e-3;
+            ar.bx0 = Real(cxp - hx);
+            ar.bx1 = Real(cxp + hx);
+            ar.by0 = Real(cyp - hy);
+            ar.by1 = Real(cyp + hy);
+        } else {  // opacity < 1/255: no pixel can pass
+            ar.bx0 = ar.by0 = Real(1e30);
+            ar.bx1 = ar.by1 = Real(-1e30);
+        }
+    }
     a.arec[i] = ar;
 
     BlendRec<Real> br;
