@@ -205,7 +205,7 @@ def cpu_baseline(args):
     total = float(sum(ms))
     return {"value": 1000.0 / total, "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"1 full fwd+bwd render (view 0) of the same scene, {total / 1000:.1f} s; stage ms "
-                      f"rasterize/normals/normals_bwd/backward/chain = {[round(x, 1) for x in ms]}"}
+                      f"rasterize/normals/normals_bwd/backward/chain = {[round(float(x), 1) for x in ms]}"}
 
 
 def workload_config(args, world, graph):

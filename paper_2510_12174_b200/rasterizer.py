@@ -83,6 +83,8 @@ class Scene:
                 what = "SH coefficient count" if name == "sh" else (
                     "semantic channel count" if name == "semantics" else name + " shape")
                 raise ValueError(f"Scene: wrong {what}: {tuple(t.shape)} != {shp}")
+        for name in expect:
+            t = getattr(self, name)
             if t.dtype != self.dtype or not t.is_cuda or not t.is_contiguous():
                 raise ValueError(f"Scene: {name} must be a contiguous CUDA tensor of one dtype")
         if self.dtype not in (torch.float32, torch.float64):
