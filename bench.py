@@ -268,14 +268,11 @@ def run_ours(args, rank, world, local_rank):
     frame = M.MultimodalFrame.empty(Wd, Ht, C, torch.float32, dev)
     replay = M.ReplayState(device=local_rank)
 
+    from paper_2510_12174_b200.distributed import ViewShardedStep
+    sharded = ViewShardedStep(scene, flat, gflat, grads, opt, tc, rc, nc, cams, pixs, frame, replay, world)
+
     def step(pix_list):
-        for j in range(V):
-            M.fwd_bwd(scene, cams[j], rc, nc, frame, pix_list[j], grads, replay, chain=False, accumulate=j > 0)
-        grads.raw_space = False
-        M.chain_activations(grads, scene)
-        if world > 1:
-            dist.all_reduce(gflat)
-        M.adam_step(scene, grads, opt, tc, packed_params=flat, packed_grads=gflat)
+        sharded(pix_list)
 
     stream = torch.cuda.current_stream(dev)
     for _ in range(max(args.warmup, 1)):
