@@ -2,29 +2,26 @@
 // (core/src/rasterizer_backward.cpp:140-255) with intersection_backward
 // (core/src/geometry.cpp:70-105) and quat_rotation_backward (:17-29).
 //
-// One CTA per 16x16 tile, one thread per pixel, warps own 8x4 pixel blocks.
-// Each pixel replays its list from terminus-1 down to 0 with the forward's
-// alpha test (same code, same decisions), restores T by division, and forms
-// the reference's per-pair gradients.  As in K6, each warp culls every batch
-// with the alpha-support boxes and walks only surviving entries (now back to
-// front).
+// One CTA per 16x16 tile, one thread per pixel, warps own 8x4 pixel blocks and
+// run INDEPENDENTLY (no block barrier after setup): each warp walks the tile
+// list back to front in 32-entry chunks up to its own max terminus, culls each
+// chunk with the alpha-support boxes (one ballot), and replays its pixels.
 //
-// dalpha without per-channel accumulators.  With the per-pair feature vector
-// F_j = [rgb, k, sem] and the pixel seed s_p = [dC, dK, dO], the reference's
-//   dalpha = (rgb - acc_c).dC T + (k - acc_k) dK T + sum_ch (sem - acc_s).dO T - bg term
-// equals (F_j.s_p - A) T - bg term, where A = acc_c.dC + acc_k dK + acc_s.dO
-// obeys the same linear recursion A <- a_last (F_last.s_p) + (1 - a_last) A
-// (rasterizer_backward.cpp:222-231).  F_j is staged once per (warp, Gaussian)
-// event in shared memory and dotted with the pixel's seed row (128-bit LDS).
-//
-// Reductions, fused into one loop over the blending lanes L of an event:
-//   * seed-linear gradients (dcolor, dk, dsem = w_L * s_L): channel-parallel,
-//     lane ch accumulates w_L * s_L[ch] and w_L * s_L[ch+32];
-//   * 16 geometric gradients (dopacity, dmean2d, dconic, depth-chain
-//     dposition / drotation / dscale): each blending lane wrote them to its
-//     shared scratch row; lane i < 16 sums column i;
-// then one atomic per non-zero value.  O(active lanes) per event, no shuffle
-// trees.
+// Two phases per chunk:
+//  A (sequential per pixel, the reference's recursion): alpha test (same code
+//    and decisions as K6), T restore by division, w = alpha T and dalpha.  With
+//    F_j = [rgb, k, sem] and the pixel seed s_p = [dC, dK, dO], the reference's
+//      dalpha = (rgb - acc_c).dC T + (k - acc_k) dK T + sum (sem - acc_s).dO T - bg
+//    is (F_j.s_p - A) T - bg with A <- a_last (F_last.s_p) + (1 - a_last) A
+//    (rasterizer_backward.cpp:222-232); F_j is staged once per (warp, Gaussian)
+//    event and dotted with the pixel's seed row.  Each blended pair is then
+//    ENQUEUED (pixel, chunk slot, w, dalpha, alpha, gauss, clamped).
+//  B (flush, 32 pairs per warp vector, all lanes busy): the per-pair geometric
+//    gradients -- dopacity, dmean2d, dconic and the depth chain's
+//    dposition / drotation / dscale -- then a segmented warp reduction by
+//    Gaussian (queue entries of one Gaussian are contiguous) and one atomic per
+//    value per segment; the seed-linear gradients (dcolor, dk, dsem = w s_p)
+//    are reduced channel-parallel over the same segments.
 #include "blend_common.cuh"
 #include "kernels.h"
 
@@ -32,14 +29,11 @@ namespace msplat_cuda {
 
 namespace {
 
-constexpr int kBatch = 256;
 constexpr int kThreads = 256;
-constexpr int kMaskWords = kBatch / 32;
-constexpr int kGeo = 16;             // geometric values per pair
-constexpr int kRedPitch = kGeo + 1;  // + w; odd pitch
+constexpr int kQueue = 64;  // per-warp pair queue (flushed at >= 32)
 
 // Seed rows [dC0 dC1 dC2 dK dO...]: multiple of 4 (128-bit loads) with an odd
-// number of 16-byte units per row (conflict-free when every lane reads its own row).
+// number of 16-byte units per row (conflict-free when each lane reads its row).
 __host__ __device__ inline int seed_pitch(int C) {
     int p = ((C + 4 + 3) / 4) * 4;
     if (((p / 4) & 1) == 0) p += 4;
@@ -47,10 +41,18 @@ __host__ __device__ inline int seed_pitch(int C) {
 }
 
 template <typename Real>
+struct WarpSmem {
+    AlphaRec<Real> rec[32];
+    uint32_t gid[32];
+    Real dD[32];
+    uint32_t q_meta[kQueue];  // lane | slot << 8 | clamped << 16
+    Real q_w[kQueue], q_da[kQueue], q_al[kQueue], q_gs[kQueue];
+};
+
+template <typename Real>
 size_t backward_smem_bytes(int C) {
     const int sp = seed_pitch(C);
-    return sizeof(AlphaRec<Real>) * kBatch + sizeof(uint32_t) * kBatch + sizeof(Real) * size_t(kTilePixels) * sp +
-           sizeof(Real) * 8 * 32 * kRedPitch + sizeof(Real) * 8 * sp + 16;
+    return 8 * (sizeof(WarpSmem<Real>) + sizeof(Real) * size_t(32 + 1) * sp) + 64;
 }
 
 template <typename Real>
@@ -59,6 +61,7 @@ __device__ __forceinline__ Real dot_rows(const Real* a, const Real* b, int n) {
     if constexpr (sizeof(Real) == 4) {
         const float4* a4 = reinterpret_cast<const float4*>(a);
         const float4* b4 = reinterpret_cast<const float4*>(b);
+#pragma unroll 4
         for (int i = 0; i < n / 4; ++i) {
             const float4 x = a4[i], y = b4[i];
             s += x.x * y.x + x.y * y.y + x.z * y.z + x.w * y.w;
@@ -69,40 +72,44 @@ __device__ __forceinline__ Real dot_rows(const Real* a, const Real* b, int n) {
     return s;
 }
 
+// Segmented sum toward the first lane of each run of equal keys (runs are
+// contiguous).  same[k] = (key of lane + 2^k == my key) precomputed.
+template <typename Real>
+__device__ __forceinline__ Real seg_sum(Real v, const bool* same) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const Real o = __shfl_down_sync(0xffffffffu, v, 1 << k);
+        if (same[k]) v += o;
+    }
+    return v;
+}
+
 }  // namespace
 
 template <typename Real>
 __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArgs<Real> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int C = a.C, sp = seed_pitch(C), S = C + 4;
-    AlphaRec<Real>* s_rec = reinterpret_cast<AlphaRec<Real>*>(smem_raw);
-    Real* s_seed = reinterpret_cast<Real*>(s_rec + kBatch);          // [256][sp], row = warp*32 + lane
-    Real* s_red = s_seed + size_t(kTilePixels) * sp;                  // [8][32][kRedPitch]
-    Real* s_F = s_red + 8 * 32 * kRedPitch;                           // [8][sp] staged F_j per warp
-    uint32_t* s_gid = reinterpret_cast<uint32_t*>(s_F + 8 * sp);
-    int* s_maxterm = reinterpret_cast<int*>(s_gid + kBatch);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WarpSmem<Real>* ws = reinterpret_cast<WarpSmem<Real>*>(smem_raw) + warp;
+    Real* const warp_seed = reinterpret_cast<Real*>(reinterpret_cast<WarpSmem<Real>*>(smem_raw) + 8) +
+                            size_t(warp) * (32 + 1) * sp;
+    Real* const my_seed = warp_seed + size_t(lane) * sp;
+    Real* const warp_F = warp_seed + size_t(32) * sp;  // staged F_j
 
     const int tile = blockIdx.x;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int x = tx * kTile + tile_pixel_x(warp, lane);
-    const int y = ty * kTile + tile_pixel_y(warp, lane);
+    const int bx = tx * kTile + (warp & 1) * 8, by = ty * kTile + (warp >> 1) * 4;
+    const int x = bx + (lane & 7), y = by + (lane >> 3);
     const bool inside = x < a.W && y < a.H;
     const size_t HW = size_t(a.W) * a.H, p = size_t(y) * a.W + x;
-    if (threadIdx.x == 0) *s_maxterm = 0;
 
-    Real* const warp_seed = s_seed + size_t(warp * 32) * sp;
-    Real* const my_seed = warp_seed + size_t(lane) * sp;
-    Real* const warp_red = s_red + size_t(warp * 32) * kRedPitch;
-    Real* const my_red = warp_red + lane * kRedPitch;
-    Real* const warp_F = s_F + warp * sp;
-    for (int i = lane; i < sp; i += 32) warp_F[i] = Real(0);
-
-    // Per-pixel seeds into shared memory (dD, T_final, terminus in registers).
+    // Per-pixel seeds -> this warp's shared rows; dD for the flush.
     int term = 0;
     Real T_final = Real(1), dD = Real(0);
     bool any = false;
     for (int ch = 0; ch < sp; ++ch) my_seed[ch] = Real(0);
+    for (int i = lane; i < sp; i += 32) warp_F[i] = Real(0);
     if (inside) {
         term = a.terminus[p];
         T_final = a.T_final[p];
@@ -120,211 +127,241 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
     }
     // rasterize_backward.cpp:156-171: nothing to do without blends or seeds.
     if (!(inside && term > 0 && any)) term = 0;
-    __syncthreads();
-    if (term > 0) atomicMax(s_maxterm, term);
-    __syncthreads();
-    const int maxterm = *s_maxterm;
-    if (maxterm == 0) return;
+    ws->dD[lane] = dD;
+    int wmax = term;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    if (wmax == 0) return;
+    __syncwarp();
 
-    const PixelRay<Real> ray = make_ray<Real>(a.cam, x, y);
+    const Real pxf = Real(x) + Real(0.5), pyf = Real(y) + Real(0.5);
     const Real bg_dot = Real(a.rp.bg[0]) * my_seed[0] + Real(a.rp.bg[1]) * my_seed[1] + Real(a.rp.bg[2]) * my_seed[2];
     const Real sigma = Real(a.rp.sigma_scale);
-    Real T = T_final;
-    Real accA = 0, lastFS = 0, last_alpha = 0;
+    Real T = T_final, accA = 0, lastFS = 0, last_alpha = 0;
+    const Real rx0 = Real(bx) + Real(0.5), rx1 = rx0 + Real(7);
+    const Real ry0 = Real(by) + Real(0.5), ry1 = ry0 + Real(3);
+    const uint32_t list0 = a.tile_range[tile].x;
+    int qn = 0;
 
-    const Real rx0 = Real(tx * kTile + (warp & 1) * 8) + Real(0.5), rx1 = rx0 + Real(7);
-    const Real ry0 = Real(ty * kTile + (warp >> 1) * 4) + Real(0.5), ry1 = ry0 + Real(3);
-
-    const uint2 range = a.tile_range[tile];
-    const uint32_t list_end = range.x + uint32_t(maxterm);
-    for (int64_t bend = int64_t(list_end); bend > int64_t(range.x); bend -= kBatch) {
-        const uint32_t bstart = uint32_t(max(int64_t(range.x), bend - kBatch));
-        const int nb = int(uint32_t(bend) - bstart);
-        const int pos0 = int(bstart - range.x);
-        __syncthreads();
-        if (int(threadIdx.x) < nb) {
-            const uint32_t g = a.inst_gauss[bstart + threadIdx.x];
-            s_gid[threadIdx.x] = g;
-            s_rec[threadIdx.x] = a.arec[g];
-        }
-        __syncthreads();
-        if (!__any_sync(0xffffffffu, term > pos0)) continue;
-        uint32_t wm[kMaskWords];
+    // ------------------------------------------------------------- flush
+    auto flush = [&](int n) {
+        const bool act = lane < n;
+        uint32_t meta = act ? ws->q_meta[lane] : 0u;
+        const int L = int(meta & 0xffu), slot = int((meta >> 8) & 0xffu);
+        const bool clamped = (meta >> 16) & 1u;
+        const int key = act ? slot : 64 + lane;  // padding lanes: unique keys
+        bool same[5];
 #pragma unroll
-        for (int r = 0; r < kMaskWords; ++r) {
-            const int i = r * 32 + lane;
-            bool hit = false;
-            if (i < nb) {
-                const AlphaRec<Real>& g = s_rec[i];
-                hit = !(g.bx1 < rx0 || g.bx0 > rx1 || g.by1 < ry0 || g.by0 > ry1);
+        for (int k = 0; k < 5; ++k) {
+            const int o = __shfl_down_sync(0xffffffffu, key, 1 << k);
+            same[k] = (lane + (1 << k) < 32) && o == key;
+        }
+        const int key_prev = __shfl_up_sync(0xffffffffu, key, 1);  // all lanes: no short-circuit
+        const bool head = act && (lane == 0 || key_prev != key);
+        const uint32_t g = act ? ws->gid[slot] : 0u;
+        Real v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = Real(0);
+        Real w = Real(0);
+        if (act) {
+            w = ws->q_w[lane];
+            const Real dalpha = ws->q_da[lane], alpha = ws->q_al[lane], gauss = ws->q_gs[lane];
+            const AlphaRec<Real>& ar = ws->rec[slot];
+            const int xL = bx + (L & 7), yL = by + (L >> 3);
+            const Real dx = Real(xL) + Real(0.5) - ar.cx, dy = Real(yL) + Real(0.5) - ar.cy;
+            if (!clamped) {  // rasterizer_backward.cpp:234-244
+                v[0] = gauss * dalpha;
+                const Real dpower = alpha * dalpha;
+                v[1] = dpower * (ar.ca * dx + ar.cb * dy);
+                v[2] = dpower * (ar.cb * dx + ar.cc * dy);
+                v[3] = dpower * (Real(-0.5) * dx * dx);
+                v[4] = dpower * (Real(-0.5) * dx * dy);
+                v[5] = dpower * (Real(-0.5) * dy * dy);
             }
-            wm[r] = __ballot_sync(0xffffffffu, hit);
-        }
-#pragma unroll
-        for (int r = kMaskWords - 1; r >= 0; --r) {
-            unsigned bits = wm[r];
-            while (bits) {
-                const int bit = 31 - __clz(bits);
-                bits &= ~(1u << bit);
-                const int j = r * 32 + bit;
-                AlphaEval<Real> ae;
-                ae.pass = false;
-                if (pos0 + j < term) ae = eval_alpha<Real>(s_rec[j], ray.px, ray.py);
-                const unsigned mask = __ballot_sync(0xffffffffu, ae.pass);
-                if (mask == 0) continue;
-                const uint32_t g = s_gid[j];
+            // Depth chain (rasterizer_backward.cpp:205-218).
+            const Real dd = ws->dD[L] * w;
+            if (dd != Real(0)) {
                 const BlendRec<Real>& br = a.brec[g];
-                // Stage F_j = [rgb, k, sem] for the dot products.
-                if (lane < 3) warp_F[lane] = br.rgb[lane];
-                else if (lane == 3) warp_F[3] = br.k;
-                {
-                    const Real* semg = a.semantics + size_t(g) * C;
-                    for (int ch = lane; ch < C; ch += 32) warp_F[4 + ch] = semg[ch];
-                }
-                __syncwarp();
-                if (ae.pass) {
-                    Real v[kRedPitch];
+                const PixelRay<Real> ray = make_ray<Real>(a.cam, xL, yL);
+                const HitEval<Real> h = intersect<Real>(br, ray, a.cam, a.raw, g);
+                if (h.hit) {
+                    if constexpr (sizeof(Real) == 4) {
+                        // Adjoint around the small midpoint offset p_l = v_l + t d_l
+                        // (p_s = p_l / axes), algebraically the reference's:
+                        //   g_vs = -k d_s, g_ds = -k (p_s + t d_s), k = g_t / a
+                        //   dscale = 2k (d_s o p_s) / s
+                        //   dR = -k [(R p_l)(d_s/axes)^T + d (p_s/axes)^T]
+                        if (!(fabsf(h.a) < 1e-12f)) {
+                            const Real kk = dd * ray.dz / h.a;
+                            const Real t = h.t_mid;
+                            Real ps[3], pl[3], ga[3], gb[3];
 #pragma unroll
-                    for (int i = 0; i < kRedPitch; ++i) v[i] = Real(0);
-                    T = T / (Real(1) - ae.alpha);
-                    const Real w = ae.alpha * T;
-                    v[kGeo] = w;
-                    // Depth chain (rasterizer_backward.cpp:205-218).
-                    const Real dd = dD * w;
-                    if (dd != Real(0)) {
-                        const HitEval<Real> h = intersect<Real>(br, ray, a.cam, a.raw, g);
-                        if (h.hit) {
-                            if constexpr (sizeof(Real) == 4) {
-                                // Adjoint around the small midpoint offset p_l = v_l + t d_l
-                                // (p_s = p_l / axes), algebraically the reference's:
-                                //   g_vs = -k d_s, g_ds = -k (p_s + t d_s), k = g_t / a
-                                //   dscale = 2k (d_s o p_s) / s
-                                //   dR = -k [(R p_l)(d_s/axes)^T + d (p_s/axes)^T]
-                                if (!(fabsf(h.a) < 1e-12f)) {
-                                    const Real kk = dd * ray.dz / h.a;
-                                    const Real t = h.t_mid;
-                                    Real ps[3], pl[3], ga[3], gb[3];
-#pragma unroll
-                                    for (int i = 0; i < 3; ++i) {
-                                        pl[i] = br.vl[i] + t * h.dl[i];
-                                        ps[i] = pl[i] * br.inv_axes[i];
-                                        v[13 + i] = Real(2) * kk * h.ds[i] * ps[i] * sigma * br.inv_axes[i];
-                                        ga[i] = h.ds[i] * br.inv_axes[i];
-                                        gb[i] = ps[i] * br.inv_axes[i];
-                                    }
-                                    Real Rp[3];
-#pragma unroll
-                                    for (int i = 0; i < 3; ++i) {
-                                        v[6 + i] = kk * (br.Rt[0 * 3 + i] * ga[0] + br.Rt[1 * 3 + i] * ga[1] +
-                                                         br.Rt[2 * 3 + i] * ga[2]);
-                                        Rp[i] = br.Rt[0 * 3 + i] * pl[0] + br.Rt[1 * 3 + i] * pl[1] +
-                                                br.Rt[2 * 3 + i] * pl[2];
-                                    }
-                                    Real G[9];
-#pragma unroll
-                                    for (int rr = 0; rr < 3; ++rr)
-#pragma unroll
-                                        for (int cc = 0; cc < 3; ++cc)
-                                            G[rr * 3 + cc] = -kk * (Rp[rr] * ga[cc] + ray.d[rr] * gb[cc]);
-                                    quat_rotation_backward<Real>(br.q, G, v + 9);
-                                }
-                            } else if (!(fabs(h.a) < 1e-12)) {
-                                // The reference's formulation (geometry.cpp:70-105).
-                                const Real g_t = dd * ray.dz;
-                                Real gvs[3], gds[3], gvl[3], gdl[3];
-                                const Real ba2 = h.b / (h.a * h.a);
-#pragma unroll
-                                for (int i = 0; i < 3; ++i) {
-                                    gvs[i] = g_t * (-h.ds[i] / h.a);
-                                    gds[i] = g_t * (ba2 * h.ds[i] - br.vs[i] / h.a);
-                                    v[13 + i] = -((gvs[i] * br.vs[i] + gds[i] * h.ds[i]) * sigma / br.axes[i]);
-                                    gvl[i] = gvs[i] / br.axes[i];
-                                    gdl[i] = gds[i] / br.axes[i];
-                                }
-                                Real vv[3];
-#pragma unroll
-                                for (int i = 0; i < 3; ++i) {
-                                    v[6 + i] = -(br.Rt[0 * 3 + i] * gvl[0] + br.Rt[1 * 3 + i] * gvl[1] +
-                                                 br.Rt[2 * 3 + i] * gvl[2]);
-                                    vv[i] = br.Rt[0 * 3 + i] * br.vl[0] + br.Rt[1 * 3 + i] * br.vl[1] +
-                                            br.Rt[2 * 3 + i] * br.vl[2];
-                                }
-                                Real G[9];
-#pragma unroll
-                                for (int rr = 0; rr < 3; ++rr)
-#pragma unroll
-                                    for (int cc = 0; cc < 3; ++cc)
-                                        G[rr * 3 + cc] = vv[rr] * gvl[cc] + ray.d[rr] * gdl[cc];
-                                quat_rotation_backward<Real>(br.q, G, v + 9);
+                            for (int i = 0; i < 3; ++i) {
+                                pl[i] = br.vl[i] + t * h.dl[i];
+                                ps[i] = pl[i] * br.inv_axes[i];
+                                v[13 + i] = Real(2) * kk * h.ds[i] * ps[i] * sigma * br.inv_axes[i];
+                                ga[i] = h.ds[i] * br.inv_axes[i];
+                                gb[i] = ps[i] * br.inv_axes[i];
                             }
-                        } else {
+                            Real Rp[3];
 #pragma unroll
-                            for (int i = 0; i < 3; ++i) v[6 + i] = dd * Real(a.cam.Rw2c[6 + i]);
+                            for (int i = 0; i < 3; ++i) {
+                                v[6 + i] = kk * (br.Rt[0 * 3 + i] * ga[0] + br.Rt[1 * 3 + i] * ga[1] +
+                                                 br.Rt[2 * 3 + i] * ga[2]);
+                                Rp[i] = br.Rt[0 * 3 + i] * pl[0] + br.Rt[1 * 3 + i] * pl[1] + br.Rt[2 * 3 + i] * pl[2];
+                            }
+                            Real G[9];
+#pragma unroll
+                            for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+                                for (int cc = 0; cc < 3; ++cc) G[rr * 3 + cc] = -kk * (Rp[rr] * ga[cc] + ray.d[rr] * gb[cc]);
+                            quat_rotation_backward<Real>(br.q, G, v + 9);
                         }
-                    }
-                    // Alpha gradient (rasterizer_backward.cpp:222-244); depth excluded.
-                    const Real FS = dot_rows<Real>(warp_F, my_seed, sp);
-                    accA = last_alpha * lastFS + (Real(1) - last_alpha) * accA;
-                    const Real dalpha = (FS - accA) * T - (T_final / (Real(1) - ae.alpha)) * bg_dot;
-                    if (!ae.clamped) {
-                        v[0] = ae.gauss * dalpha;
-                        const Real dpower = ae.alpha * dalpha;
-                        const AlphaRec<Real>& ar = s_rec[j];
-                        v[1] = dpower * (ar.ca * ae.dx + ar.cb * ae.dy);
-                        v[2] = dpower * (ar.cb * ae.dx + ar.cc * ae.dy);
-                        v[3] = dpower * (Real(-0.5) * ae.dx * ae.dx);
-                        v[4] = dpower * (Real(-0.5) * ae.dx * ae.dy);
-                        v[5] = dpower * (Real(-0.5) * ae.dy * ae.dy);
-                    }
-                    lastFS = FS;
-                    last_alpha = ae.alpha;
+                    } else if (!(fabs(h.a) < 1e-12)) {
+                        // The reference's formulation (geometry.cpp:70-105).
+                        const Real g_t = dd * ray.dz;
+                        Real gvs[3], gds[3], gvl[3], gdl[3];
+                        const Real ba2 = h.b / (h.a * h.a);
 #pragma unroll
-                    for (int i = 0; i < kRedPitch; ++i) my_red[i] = v[i];
+                        for (int i = 0; i < 3; ++i) {
+                            gvs[i] = g_t * (-h.ds[i] / h.a);
+                            gds[i] = g_t * (ba2 * h.ds[i] - br.vs[i] / h.a);
+                            v[13 + i] = -((gvs[i] * br.vs[i] + gds[i] * h.ds[i]) * sigma / br.axes[i]);
+                            gvl[i] = gvs[i] / br.axes[i];
+                            gdl[i] = gds[i] / br.axes[i];
+                        }
+                        Real vv[3];
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) {
+                            v[6 + i] = -(br.Rt[0 * 3 + i] * gvl[0] + br.Rt[1 * 3 + i] * gvl[1] + br.Rt[2 * 3 + i] * gvl[2]);
+                            vv[i] = br.Rt[0 * 3 + i] * br.vl[0] + br.Rt[1 * 3 + i] * br.vl[1] + br.Rt[2 * 3 + i] * br.vl[2];
+                        }
+                        Real G[9];
+#pragma unroll
+                        for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+                            for (int cc = 0; cc < 3; ++cc) G[rr * 3 + cc] = vv[rr] * gvl[cc] + ray.d[rr] * gdl[cc];
+                        quat_rotation_backward<Real>(br.q, G, v + 9);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) v[6 + i] = dd * Real(a.cam.Rw2c[6 + i]);
                 }
-                __syncwarp();
-                // Fused reductions over the blending lanes.
-                Real acc0 = Real(0), acc1 = Real(0), geo = Real(0);
-                const int gl = lane & (kGeo - 1);
-                const int c1 = lane + 32 < sp ? lane + 32 : lane;  // clamp: acc1 unused then
-                unsigned m = mask;
-                while (m) {
-                    const int L = __ffs(m) - 1;
-                    m &= m - 1;
-                    const Real* redL = warp_red + L * kRedPitch;
-                    const Real* seedL = warp_seed + L * sp;
-                    const Real wL = redL[kGeo];
-                    acc0 += wL * seedL[lane];
-                    acc1 += wL * seedL[c1];
-                    geo += redL[gl];
-                }
-                if (lane < kGeo && geo != Real(0)) {
-                    Real* dst;
-                    if (lane == 0) dst = a.g_opac + g;
-                    else if (lane < 3) dst = a.acc_dmean + size_t(g) * 2 + (lane - 1);
-                    else if (lane < 6) dst = a.acc_dconic + size_t(g) * 3 + (lane - 3);
-                    else if (lane < 9) dst = a.g_pos + size_t(g) * 3 + (lane - 6);
-                    else if (lane < 13) dst = a.g_rot + size_t(g) * 4 + (lane - 9);
-                    else dst = a.g_scale + size_t(g) * 3 + (lane - 13);
-                    atomicAdd(dst, geo);
-                }
+            }
+        }
+        // Geometric gradients: segmented sums, one atomic per value per Gaussian.
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const Real s = seg_sum<Real>(v[i], same);
+            if (head && s != Real(0)) {
+                Real* dst;
+                if (i == 0) dst = a.g_opac + g;
+                else if (i < 3) dst = a.acc_dmean + size_t(g) * 2 + (i - 1);
+                else if (i < 6) dst = a.acc_dconic + size_t(g) * 3 + (i - 3);
+                else if (i < 9) dst = a.g_pos + size_t(g) * 3 + (i - 6);
+                else if (i < 13) dst = a.g_rot + size_t(g) * 4 + (i - 9);
+                else dst = a.g_scale + size_t(g) * 3 + (i - 13);
+                atomicAdd(dst, s);
+            }
+        }
+        // Seed-linear gradients (dcolor, dk, dsem += w s_p), channel-parallel.
+        // Clamped channel indices keep every shared read inside the row (C may be 0).
+        const int c0 = lane < sp ? lane : 0, c1 = lane + 32 < sp ? lane + 32 : 0;
+        Real acc0 = Real(0), acc1 = Real(0);
+        for (int e = 0; e < n; ++e) {
+            const uint32_t me = ws->q_meta[e];
+            const Real we = ws->q_w[e];
+            const Real* seedL = warp_seed + int(me & 0xffu) * sp;
+            acc0 += we * seedL[c0];
+            acc1 += we * seedL[c1];
+            for (int ch = lane + 64; ch < S; ch += 32) {  // C > 60: direct atomics
+                const Real sv = we * seedL[ch];
+                if (sv != Real(0)) atomicAdd(a.g_sem + size_t(ws->gid[(me >> 8) & 0xffu]) * C + (ch - 4), sv);
+            }
+            const bool last = e == n - 1 || ((ws->q_meta[e + 1] >> 8) & 0xffu) != ((me >> 8) & 0xffu);
+            if (last) {
+                const uint32_t ge = ws->gid[(me >> 8) & 0xffu];
                 if (lane < S && acc0 != Real(0)) {
-                    Real* dst = lane < 3 ? a.acc_dcolor + size_t(g) * 3 + lane
-                                         : (lane == 3 ? a.g_k + g : a.g_sem + size_t(g) * C + (lane - 4));
+                    Real* dst = lane < 3 ? a.acc_dcolor + size_t(ge) * 3 + lane
+                                         : (lane == 3 ? a.g_k + ge : a.g_sem + size_t(ge) * C + (lane - 4));
                     atomicAdd(dst, acc0);
                 }
-                if (lane + 32 < S && acc1 != Real(0)) atomicAdd(a.g_sem + size_t(g) * C + (lane + 28), acc1);
-                for (int ch = lane + 64; ch < S; ch += 32) {  // C > 60
-                    Real s = Real(0);
-                    unsigned m2 = mask;
-                    while (m2) {
-                        const int L = __ffs(m2) - 1;
-                        m2 &= m2 - 1;
-                        s += warp_red[L * kRedPitch + kGeo] * warp_seed[L * sp + ch];
-                    }
-                    if (s != Real(0)) atomicAdd(a.g_sem + size_t(g) * C + (ch - 4), s);
+                if (lane + 32 < S && acc1 != Real(0)) atomicAdd(a.g_sem + size_t(ge) * C + (lane + 28), acc1);
+                acc0 = acc1 = Real(0);
+            }
+        }
+        __syncwarp();
+    };
+
+    // ------------------------------------------------------- main loop
+    for (int c = (wmax - 1) >> 5; c >= 0; --c) {
+        const int pos = c * 32 + lane;
+        bool hit = false;
+        if (pos < wmax) {
+            const uint32_t g = a.inst_gauss[list0 + pos];
+            const AlphaRec<Real> r = a.arec[g];
+            ws->rec[lane] = r;
+            ws->gid[lane] = g;
+            hit = !(r.bx1 < rx0 || r.bx0 > rx1 || r.by1 < ry0 || r.by0 > ry1);
+        }
+        unsigned bits = __ballot_sync(0xffffffffu, hit);
+        __syncwarp();
+        while (bits) {
+            const int slot = 31 - __clz(bits);
+            bits &= ~(1u << slot);
+            AlphaEval<Real> ae;
+            ae.pass = false;
+            if (c * 32 + slot < term) ae = eval_alpha<Real>(ws->rec[slot], pxf, pyf);
+            const unsigned mask = __ballot_sync(0xffffffffu, ae.pass);
+            if (mask == 0) continue;
+            const uint32_t g = ws->gid[slot];
+            // Stage F_j = [rgb, k, sem] for the dot products.
+            if (lane < 4) {
+                const BlendRec<Real>& br = a.brec[g];
+                warp_F[lane] = lane < 3 ? br.rgb[lane] : br.k;
+            }
+            {
+                const Real* semg = a.semantics + size_t(g) * C;
+                for (int ch = lane; ch < C; ch += 32) warp_F[4 + ch] = semg[ch];
+            }
+            __syncwarp();
+            if (ae.pass) {
+                T = T / (Real(1) - ae.alpha);
+                const Real w = ae.alpha * T;
+                const Real FS = dot_rows<Real>(warp_F, my_seed, sp);
+                accA = last_alpha * lastFS + (Real(1) - last_alpha) * accA;
+                const Real dalpha = (FS - accA) * T - (T_final / (Real(1) - ae.alpha)) * bg_dot;
+                lastFS = FS;
+                last_alpha = ae.alpha;
+                const int q = qn + __popc(mask & ((1u << lane) - 1u));
+                ws->q_meta[q] = uint32_t(lane) | (uint32_t(slot) << 8) | (ae.clamped ? (1u << 16) : 0u);
+                ws->q_w[q] = w;
+                ws->q_da[q] = dalpha;
+                ws->q_al[q] = ae.alpha;
+                ws->q_gs[q] = ae.gauss;
+            }
+            qn += __popc(mask);
+            __syncwarp();
+            if (qn >= 32) {
+                flush(32);
+                const int rest = qn - 32;
+                if (lane < rest) {
+                    const uint32_t m2 = ws->q_meta[32 + lane];
+                    const Real w2 = ws->q_w[32 + lane], d2 = ws->q_da[32 + lane];
+                    const Real a2 = ws->q_al[32 + lane], g2 = ws->q_gs[32 + lane];
+                    ws->q_meta[lane] = m2;  // reads >= 32, writes < 32: no overlap
+                    ws->q_w[lane] = w2;
+                    ws->q_da[lane] = d2;
+                    ws->q_al[lane] = a2;
+                    ws->q_gs[lane] = g2;
                 }
+                qn = rest;
                 __syncwarp();
             }
+        }
+        if (qn > 0) {  // chunk records are about to be replaced
+            flush(qn);
+            qn = 0;
         }
     }
 }
