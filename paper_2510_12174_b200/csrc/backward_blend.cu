@@ -7,21 +7,22 @@
 // list back to front in 32-entry chunks up to its own max terminus, culls each
 // chunk with the alpha-support boxes (one ballot), and replays its pixels.
 //
-// Two phases per chunk:
-//  A (sequential per pixel, the reference's recursion): alpha test (same code
-//    and decisions as K6), T restore by division, w = alpha T and dalpha.  With
-//    F_j = [rgb, k, sem] and the pixel seed s_p = [dC, dK, dO], the reference's
-//      dalpha = (rgb - acc_c).dC T + (k - acc_k) dK T + sum (sem - acc_s).dO T - bg
-//    is (F_j.s_p - A) T - bg with A <- a_last (F_last.s_p) + (1 - a_last) A
-//    (rasterizer_backward.cpp:222-232); F_j is staged once per (warp, Gaussian)
-//    event and dotted with the pixel's seed row.  Each blended pair is then
-//    ENQUEUED (pixel, chunk slot, w, dalpha, alpha, gauss, clamped).
-//  B (flush, 32 pairs per warp vector, all lanes busy): the per-pair geometric
-//    gradients -- dopacity, dmean2d, dconic and the depth chain's
-//    dposition / drotation / dscale -- then a segmented warp reduction by
-//    Gaussian (queue entries of one Gaussian are contiguous) and one atomic per
-//    value per segment; the seed-linear gradients (dcolor, dk, dsem = w s_p)
-//    are reduced channel-parallel over the same segments.
+// Phase A (per (warp, Gaussian) event, the reference's sequential recursion):
+//   alpha test (same code and decisions as K6), T restore by division,
+//   w = alpha T and dalpha.  With F_j = [rgb, k, sem] and the pixel seed
+//   s_p = [dC, dK, dO], the reference's
+//     dalpha = (rgb - acc_c).dC T + (k - acc_k) dK T + sum (sem - acc_s).dO T - bg
+//   is (F_j.s_p - A) T - bg with A <- a_last (F_last.s_p) + (1 - a_last) A
+//   (rasterizer_backward.cpp:222-232).  F_j is staged once per event and
+//   dotted with the pixel's seed row (128-bit shared loads).  The seed-linear
+//   gradients (dcolor, dk, dsem = sum_p w s_p) are accumulated channel-parallel
+//   over the event's blending lanes, one atomic per channel.  Each blended pair
+//   is ENQUEUED with everything phase B needs (self-contained entries, so the
+//   queue spans chunks).
+// Phase B (flush, 32 pairs per warp vector, every lane busy): dopacity,
+//   dmean2d, dconic and the depth chain's dposition / drotation / dscale, then
+//   a segmented warp reduction keyed by Gaussian (an event's entries are
+//   contiguous) and one atomic per value per Gaussian.
 #include "blend_common.cuh"
 #include "kernels.h"
 
@@ -41,12 +42,19 @@ __host__ __device__ inline int seed_pitch(int C) {
 }
 
 template <typename Real>
+struct PairQueue {
+    uint32_t meta[kQueue];  // pixel lane | clamped << 8
+    uint32_t gid[kQueue];
+    Real w[kQueue], da[kQueue], al[kQueue], gs[kQueue];
+    Real cx[kQueue], cy[kQueue], ca[kQueue], cb[kQueue], cc[kQueue];
+};
+
+template <typename Real>
 struct WarpSmem {
     AlphaRec<Real> rec[32];
     uint32_t gid[32];
     Real dD[32];
-    uint32_t q_meta[kQueue];  // lane | slot << 8 | clamped << 16
-    Real q_w[kQueue], q_da[kQueue], q_al[kQueue], q_gs[kQueue];
+    PairQueue<Real> q;
 };
 
 template <typename Real>
@@ -73,7 +81,7 @@ __device__ __forceinline__ Real dot_rows(const Real* a, const Real* b, int n) {
 }
 
 // Segmented sum toward the first lane of each run of equal keys (runs are
-// contiguous).  same[k] = (key of lane + 2^k == my key) precomputed.
+// contiguous).  same[k] = (key of lane + 2^k == my key).
 template <typename Real>
 __device__ __forceinline__ Real seg_sum(Real v, const bool* same) {
 #pragma unroll
@@ -82,6 +90,131 @@ __device__ __forceinline__ Real seg_sum(Real v, const bool* same) {
         if (same[k]) v += o;
     }
     return v;
+}
+
+// Phase B on the first n queue entries (n <= 32): per-pair geometric
+// gradients, segmented by Gaussian, one atomic per value per Gaussian.
+template <typename Real>
+__device__ __noinline__ void flush_pairs(const BackwardArgs<Real>& a, const PairQueue<Real>& q, const Real* dDw,
+                                         int n, int bx, int by) {
+    const int lane = threadIdx.x & 31;
+    const bool act = lane < n;
+    const uint32_t meta = act ? q.meta[lane] : 0u;
+    const uint32_t g = act ? q.gid[lane] : 0xffffffffu - lane;  // padding lanes: unique keys
+    bool same[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const uint32_t o = __shfl_down_sync(0xffffffffu, g, 1 << k);
+        same[k] = (lane + (1 << k) < 32) && o == g;
+    }
+    const uint32_t g_prev = __shfl_up_sync(0xffffffffu, g, 1);
+    const bool head = act && (lane == 0 || g_prev != g);
+    Real v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = Real(0);
+    if (act) {
+        const int L = int(meta & 0xffu);
+        const bool clamped = (meta >> 8) & 1u;
+        const Real w = q.w[lane], dalpha = q.da[lane], alpha = q.al[lane], gauss = q.gs[lane];
+        const int xL = bx + (L & 7), yL = by + (L >> 3);
+        const Real dx = Real(xL) + Real(0.5) - q.cx[lane], dy = Real(yL) + Real(0.5) - q.cy[lane];
+        if (!clamped) {  // rasterizer_backward.cpp:234-244
+            const Real ca = q.ca[lane], cb = q.cb[lane], cc = q.cc[lane];
+            v[0] = gauss * dalpha;
+            const Real dpower = alpha * dalpha;
+            v[1] = dpower * (ca * dx + cb * dy);
+            v[2] = dpower * (cb * dx + cc * dy);
+            v[3] = dpower * (Real(-0.5) * dx * dx);
+            v[4] = dpower * (Real(-0.5) * dx * dy);
+            v[5] = dpower * (Real(-0.5) * dy * dy);
+        }
+        // Depth chain (rasterizer_backward.cpp:205-218).
+        const Real dd = dDw[L] * w;
+        if (dd != Real(0)) {
+            const Real sigma = Real(a.rp.sigma_scale);
+            const BlendRec<Real>& br = a.brec[g];
+            const PixelRay<Real> ray = make_ray<Real>(a.cam, xL, yL);
+            const HitEval<Real> h = intersect<Real>(br, ray, a.cam, a.raw, g);
+            if (h.hit) {
+                if constexpr (sizeof(Real) == 4) {
+                    // Adjoint around the small midpoint offset p_l = v_l + t d_l
+                    // (p_s = p_l / axes), algebraically the reference's:
+                    //   g_vs = -k d_s, g_ds = -k (p_s + t d_s), k = g_t / a
+                    //   dscale = 2k (d_s o p_s) / s
+                    //   dR = -k [(R p_l)(d_s/axes)^T + d (p_s/axes)^T]
+                    if (!(fabsf(h.a) < 1e-12f)) {
+                        const Real kk = dd * ray.dz / h.a;
+                        const Real t = h.t_mid;
+                        Real ps[3], pl[3], ga[3], gb[3];
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) {
+                            pl[i] = br.vl[i] + t * h.dl[i];
+                            ps[i] = pl[i] * br.inv_axes[i];
+                            v[13 + i] = Real(2) * kk * h.ds[i] * ps[i] * sigma * br.inv_axes[i];
+                            ga[i] = h.ds[i] * br.inv_axes[i];
+                            gb[i] = ps[i] * br.inv_axes[i];
+                        }
+                        Real Rp[3];
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) {
+                            v[6 + i] = kk * (br.Rt[0 * 3 + i] * ga[0] + br.Rt[1 * 3 + i] * ga[1] + br.Rt[2 * 3 + i] * ga[2]);
+                            Rp[i] = br.Rt[0 * 3 + i] * pl[0] + br.Rt[1 * 3 + i] * pl[1] + br.Rt[2 * 3 + i] * pl[2];
+                        }
+                        Real G[9];
+#pragma unroll
+                        for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+                            for (int cc2 = 0; cc2 < 3; ++cc2)
+                                G[rr * 3 + cc2] = -kk * (Rp[rr] * ga[cc2] + ray.d[rr] * gb[cc2]);
+                        quat_rotation_backward<Real>(br.q, G, v + 9);
+                    }
+                } else if (!(fabs(h.a) < 1e-12)) {
+                    // The reference's formulation (geometry.cpp:70-105).
+                    const Real g_t = dd * ray.dz;
+                    Real gvs[3], gds[3], gvl[3], gdl[3];
+                    const Real ba2 = h.b / (h.a * h.a);
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        gvs[i] = g_t * (-h.ds[i] / h.a);
+                        gds[i] = g_t * (ba2 * h.ds[i] - br.vs[i] / h.a);
+                        v[13 + i] = -((gvs[i] * br.vs[i] + gds[i] * h.ds[i]) * sigma / br.axes[i]);
+                        gvl[i] = gvs[i] / br.axes[i];
+                        gdl[i] = gds[i] / br.axes[i];
+                    }
+                    Real vv[3];
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        v[6 + i] = -(br.Rt[0 * 3 + i] * gvl[0] + br.Rt[1 * 3 + i] * gvl[1] + br.Rt[2 * 3 + i] * gvl[2]);
+                        vv[i] = br.Rt[0 * 3 + i] * br.vl[0] + br.Rt[1 * 3 + i] * br.vl[1] + br.Rt[2 * 3 + i] * br.vl[2];
+                    }
+                    Real G[9];
+#pragma unroll
+                    for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+                        for (int cc2 = 0; cc2 < 3; ++cc2) G[rr * 3 + cc2] = vv[rr] * gvl[cc2] + ray.d[rr] * gdl[cc2];
+                    quat_rotation_backward<Real>(br.q, G, v + 9);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 3; ++i) v[6 + i] = dd * Real(a.cam.Rw2c[6 + i]);
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const Real s = seg_sum<Real>(v[i], same);
+        if (head && s != Real(0)) {
+            Real* dst;
+            if (i == 0) dst = a.g_opac + g;
+            else if (i < 3) dst = a.acc_dmean + size_t(g) * 2 + (i - 1);
+            else if (i < 6) dst = a.acc_dconic + size_t(g) * 3 + (i - 3);
+            else if (i < 9) dst = a.g_pos + size_t(g) * 3 + (i - 6);
+            else if (i < 13) dst = a.g_rot + size_t(g) * 4 + (i - 9);
+            else dst = a.g_scale + size_t(g) * 3 + (i - 13);
+            atomicAdd(dst, s);
+        }
+    }
+    __syncwarp();
 }
 
 }  // namespace
@@ -96,6 +229,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
                             size_t(warp) * (32 + 1) * sp;
     Real* const my_seed = warp_seed + size_t(lane) * sp;
     Real* const warp_F = warp_seed + size_t(32) * sp;  // staged F_j
+    PairQueue<Real>& Q = ws->q;
 
     const int tile = blockIdx.x;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
@@ -136,164 +270,14 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
 
     const Real pxf = Real(x) + Real(0.5), pyf = Real(y) + Real(0.5);
     const Real bg_dot = Real(a.rp.bg[0]) * my_seed[0] + Real(a.rp.bg[1]) * my_seed[1] + Real(a.rp.bg[2]) * my_seed[2];
-    const Real sigma = Real(a.rp.sigma_scale);
     Real T = T_final, accA = 0, lastFS = 0, last_alpha = 0;
     const Real rx0 = Real(bx) + Real(0.5), rx1 = rx0 + Real(7);
     const Real ry0 = Real(by) + Real(0.5), ry1 = ry0 + Real(3);
     const uint32_t list0 = a.tile_range[tile].x;
+    // Clamped channel indices keep every shared read inside a seed row (C may be 0).
+    const int c0 = lane < sp ? lane : 0, c1 = lane + 32 < sp ? lane + 32 : 0;
     int qn = 0;
 
-    // ------------------------------------------------------------- flush
-    auto flush = [&](int n) {
-        const bool act = lane < n;
-        uint32_t meta = act ? ws->q_meta[lane] : 0u;
-        const int L = int(meta & 0xffu), slot = int((meta >> 8) & 0xffu);
-        const bool clamped = (meta >> 16) & 1u;
-        const int key = act ? slot : 64 + lane;  // padding lanes: unique keys
-        bool same[5];
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {
-            const int o = __shfl_down_sync(0xffffffffu, key, 1 << k);
-            same[k] = (lane + (1 << k) < 32) && o == key;
-        }
-        const int key_prev = __shfl_up_sync(0xffffffffu, key, 1);  // all lanes: no short-circuit
-        const bool head = act && (lane == 0 || key_prev != key);
-        const uint32_t g = act ? ws->gid[slot] : 0u;
-        Real v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = Real(0);
-        Real w = Real(0);
-        if (act) {
-            w = ws->q_w[lane];
-            const Real dalpha = ws->q_da[lane], alpha = ws->q_al[lane], gauss = ws->q_gs[lane];
-            const AlphaRec<Real>& ar = ws->rec[slot];
-            const int xL = bx + (L & 7), yL = by + (L >> 3);
-            const Real dx = Real(xL) + Real(0.5) - ar.cx, dy = Real(yL) + Real(0.5) - ar.cy;
-            if (!clamped) {  // rasterizer_backward.cpp:234-244
-                v[0] = gauss * dalpha;
-                const Real dpower = alpha * dalpha;
-                v[1] = dpower * (ar.ca * dx + ar.cb * dy);
-                v[2] = dpower * (ar.cb * dx + ar.cc * dy);
-                v[3] = dpower * (Real(-0.5) * dx * dx);
-                v[4] = dpower * (Real(-0.5) * dx * dy);
-                v[5] = dpower * (Real(-0.5) * dy * dy);
-            }
-            // Depth chain (rasterizer_backward.cpp:205-218).
-            const Real dd = ws->dD[L] * w;
-            if (dd != Real(0)) {
-                const BlendRec<Real>& br = a.brec[g];
-                const PixelRay<Real> ray = make_ray<Real>(a.cam, xL, yL);
-                const HitEval<Real> h = intersect<Real>(br, ray, a.cam, a.raw, g);
-                if (h.hit) {
-                    if constexpr (sizeof(Real) == 4) {
-                        // Adjoint around the small midpoint offset p_l = v_l + t d_l
-                        // (p_s = p_l / axes), algebraically the reference's:
-                        //   g_vs = -k d_s, g_ds = -k (p_s + t d_s), k = g_t / a
-                        //   dscale = 2k (d_s o p_s) / s
-                        //   dR = -k [(R p_l)(d_s/axes)^T + d (p_s/axes)^T]
-                        if (!(fabsf(h.a) < 1e-12f)) {
-                            const Real kk = dd * ray.dz / h.a;
-                            const Real t = h.t_mid;
-                            Real ps[3], pl[3], ga[3], gb[3];
-#pragma unroll
-                            for (int i = 0; i < 3; ++i) {
-                                pl[i] = br.vl[i] + t * h.dl[i];
-                                ps[i] = pl[i] * br.inv_axes[i];
-                                v[13 + i] = Real(2) * kk * h.ds[i] * ps[i] * sigma * br.inv_axes[i];
-                                ga[i] = h.ds[i] * br.inv_axes[i];
-                                gb[i] = ps[i] * br.inv_axes[i];
-                            }
-                            Real Rp[3];
-#pragma unroll
-                            for (int i = 0; i < 3; ++i) {
-                                v[6 + i] = kk * (br.Rt[0 * 3 + i] * ga[0] + br.Rt[1 * 3 + i] * ga[1] +
-                                                 br.Rt[2 * 3 + i] * ga[2]);
-                                Rp[i] = br.Rt[0 * 3 + i] * pl[0] + br.Rt[1 * 3 + i] * pl[1] + br.Rt[2 * 3 + i] * pl[2];
-                            }
-                            Real G[9];
-#pragma unroll
-                            for (int rr = 0; rr < 3; ++rr)
-#pragma unroll
-                                for (int cc = 0; cc < 3; ++cc) G[rr * 3 + cc] = -kk * (Rp[rr] * ga[cc] + ray.d[rr] * gb[cc]);
-                            quat_rotation_backward<Real>(br.q, G, v + 9);
-                        }
-                    } else if (!(fabs(h.a) < 1e-12)) {
-                        // The reference's formulation (geometry.cpp:70-105).
-                        const Real g_t = dd * ray.dz;
-                        Real gvs[3], gds[3], gvl[3], gdl[3];
-                        const Real ba2 = h.b / (h.a * h.a);
-#pragma unroll
-                        for (int i = 0; i < 3; ++i) {
-                            gvs[i] = g_t * (-h.ds[i] / h.a);
-                            gds[i] = g_t * (ba2 * h.ds[i] - br.vs[i] / h.a);
-                            v[13 + i] = -((gvs[i] * br.vs[i] + gds[i] * h.ds[i]) * sigma / br.axes[i]);
-                            gvl[i] = gvs[i] / br.axes[i];
-                            gdl[i] = gds[i] / br.axes[i];
-                        }
-                        Real vv[3];
-#pragma unroll
-                        for (int i = 0; i < 3; ++i) {
-                            v[6 + i] = -(br.Rt[0 * 3 + i] * gvl[0] + br.Rt[1 * 3 + i] * gvl[1] + br.Rt[2 * 3 + i] * gvl[2]);
-                            vv[i] = br.Rt[0 * 3 + i] * br.vl[0] + br.Rt[1 * 3 + i] * br.vl[1] + br.Rt[2 * 3 + i] * br.vl[2];
-                        }
-                        Real G[9];
-#pragma unroll
-                        for (int rr = 0; rr < 3; ++rr)
-#pragma unroll
-                            for (int cc = 0; cc < 3; ++cc) G[rr * 3 + cc] = vv[rr] * gvl[cc] + ray.d[rr] * gdl[cc];
-                        quat_rotation_backward<Real>(br.q, G, v + 9);
-                    }
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 3; ++i) v[6 + i] = dd * Real(a.cam.Rw2c[6 + i]);
-                }
-            }
-        }
-        // Geometric gradients: segmented sums, one atomic per value per Gaussian.
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const Real s = seg_sum<Real>(v[i], same);
-            if (head && s != Real(0)) {
-                Real* dst;
-                if (i == 0) dst = a.g_opac + g;
-                else if (i < 3) dst = a.acc_dmean + size_t(g) * 2 + (i - 1);
-                else if (i < 6) dst = a.acc_dconic + size_t(g) * 3 + (i - 3);
-                else if (i < 9) dst = a.g_pos + size_t(g) * 3 + (i - 6);
-                else if (i < 13) dst = a.g_rot + size_t(g) * 4 + (i - 9);
-                else dst = a.g_scale + size_t(g) * 3 + (i - 13);
-                atomicAdd(dst, s);
-            }
-        }
-        // Seed-linear gradients (dcolor, dk, dsem += w s_p), channel-parallel.
-        // Clamped channel indices keep every shared read inside the row (C may be 0).
-        const int c0 = lane < sp ? lane : 0, c1 = lane + 32 < sp ? lane + 32 : 0;
-        Real acc0 = Real(0), acc1 = Real(0);
-        for (int e = 0; e < n; ++e) {
-            const uint32_t me = ws->q_meta[e];
-            const Real we = ws->q_w[e];
-            const Real* seedL = warp_seed + int(me & 0xffu) * sp;
-            acc0 += we * seedL[c0];
-            acc1 += we * seedL[c1];
-            for (int ch = lane + 64; ch < S; ch += 32) {  // C > 60: direct atomics
-                const Real sv = we * seedL[ch];
-                if (sv != Real(0)) atomicAdd(a.g_sem + size_t(ws->gid[(me >> 8) & 0xffu]) * C + (ch - 4), sv);
-            }
-            const bool last = e == n - 1 || ((ws->q_meta[e + 1] >> 8) & 0xffu) != ((me >> 8) & 0xffu);
-            if (last) {
-                const uint32_t ge = ws->gid[(me >> 8) & 0xffu];
-                if (lane < S && acc0 != Real(0)) {
-                    Real* dst = lane < 3 ? a.acc_dcolor + size_t(ge) * 3 + lane
-                                         : (lane == 3 ? a.g_k + ge : a.g_sem + size_t(ge) * C + (lane - 4));
-                    atomicAdd(dst, acc0);
-                }
-                if (lane + 32 < S && acc1 != Real(0)) atomicAdd(a.g_sem + size_t(ge) * C + (lane + 28), acc1);
-                acc0 = acc1 = Real(0);
-            }
-        }
-        __syncwarp();
-    };
-
-    // ------------------------------------------------------- main loop
     for (int c = (wmax - 1) >> 5; c >= 0; --c) {
         const int pos = c * 32 + lane;
         bool hit = false;
@@ -315,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
             const unsigned mask = __ballot_sync(0xffffffffu, ae.pass);
             if (mask == 0) continue;
             const uint32_t g = ws->gid[slot];
-            // Stage F_j = [rgb, k, sem] for the dot products.
+            // Stage F_j = [rgb, k, sem].
             if (lane < 4) {
                 const BlendRec<Real>& br = a.brec[g];
                 warp_F[lane] = lane < 3 ? br.rgb[lane] : br.k;
@@ -333,37 +317,67 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
                 const Real dalpha = (FS - accA) * T - (T_final / (Real(1) - ae.alpha)) * bg_dot;
                 lastFS = FS;
                 last_alpha = ae.alpha;
-                const int q = qn + __popc(mask & ((1u << lane) - 1u));
-                ws->q_meta[q] = uint32_t(lane) | (uint32_t(slot) << 8) | (ae.clamped ? (1u << 16) : 0u);
-                ws->q_w[q] = w;
-                ws->q_da[q] = dalpha;
-                ws->q_al[q] = ae.alpha;
-                ws->q_gs[q] = ae.gauss;
+                const int e = qn + __popc(mask & ((1u << lane) - 1u));
+                const AlphaRec<Real>& ar = ws->rec[slot];
+                Q.meta[e] = uint32_t(lane) | (ae.clamped ? (1u << 8) : 0u);
+                Q.gid[e] = g;
+                Q.w[e] = w;
+                Q.da[e] = dalpha;
+                Q.al[e] = ae.alpha;
+                Q.gs[e] = ae.gauss;
+                Q.cx[e] = ar.cx;
+                Q.cy[e] = ar.cy;
+                Q.ca[e] = ar.ca;
+                Q.cb[e] = ar.cb;
+                Q.cc[e] = ar.cc;
             }
-            qn += __popc(mask);
             __syncwarp();
+            // Seed-linear gradients of this event, channel-parallel.
+            {
+                const int npairs = __popc(mask);
+                Real acc0 = Real(0), acc1 = Real(0);
+                for (int e = qn; e < qn + npairs; ++e) {
+                    const Real we = Q.w[e];
+                    const Real* seedL = warp_seed + int(Q.meta[e] & 0xffu) * sp;
+                    acc0 += we * seedL[c0];
+                    acc1 += we * seedL[c1];
+                }
+                if (lane < S && acc0 != Real(0)) {
+                    Real* dst = lane < 3 ? a.acc_dcolor + size_t(g) * 3 + lane
+                                         : (lane == 3 ? a.g_k + g : a.g_sem + size_t(g) * C + (lane - 4));
+                    atomicAdd(dst, acc0);
+                }
+                if (lane + 32 < S && acc1 != Real(0)) atomicAdd(a.g_sem + size_t(g) * C + (lane + 28), acc1);
+                for (int ch = lane + 64; ch < S; ch += 32) {  // C > 60
+                    Real s = Real(0);
+                    for (int e = qn; e < qn + npairs; ++e) s += Q.w[e] * warp_seed[int(Q.meta[e] & 0xffu) * sp + ch];
+                    if (s != Real(0)) atomicAdd(a.g_sem + size_t(g) * C + (ch - 4), s);
+                }
+                qn += npairs;
+            }
             if (qn >= 32) {
-                flush(32);
+                flush_pairs<Real>(a, Q, ws->dD, 32, bx, by);
                 const int rest = qn - 32;
-                if (lane < rest) {
-                    const uint32_t m2 = ws->q_meta[32 + lane];
-                    const Real w2 = ws->q_w[32 + lane], d2 = ws->q_da[32 + lane];
-                    const Real a2 = ws->q_al[32 + lane], g2 = ws->q_gs[32 + lane];
-                    ws->q_meta[lane] = m2;  // reads >= 32, writes < 32: no overlap
-                    ws->q_w[lane] = w2;
-                    ws->q_da[lane] = d2;
-                    ws->q_al[lane] = a2;
-                    ws->q_gs[lane] = g2;
+                if (lane < rest) {  // reads >= 32, writes < 32: no overlap
+                    const int s2 = 32 + lane;
+                    Q.meta[lane] = Q.meta[s2];
+                    Q.gid[lane] = Q.gid[s2];
+                    Q.w[lane] = Q.w[s2];
+                    Q.da[lane] = Q.da[s2];
+                    Q.al[lane] = Q.al[s2];
+                    Q.gs[lane] = Q.gs[s2];
+                    Q.cx[lane] = Q.cx[s2];
+                    Q.cy[lane] = Q.cy[s2];
+                    Q.ca[lane] = Q.ca[s2];
+                    Q.cb[lane] = Q.cb[s2];
+                    Q.cc[lane] = Q.cc[s2];
                 }
                 qn = rest;
                 __syncwarp();
             }
         }
-        if (qn > 0) {  // chunk records are about to be replaced
-            flush(qn);
-            qn = 0;
-        }
     }
+    if (qn > 0) flush_pairs<Real>(a, Q, ws->dD, qn, bx, by);
 }
 
 template <typename Real>
