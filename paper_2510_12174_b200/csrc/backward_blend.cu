@@ -287,6 +287,12 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
             ws->rec[lane] = r;
             ws->gid[lane] = g;
             hit = !(r.bx1 < rx0 || r.bx0 > rx1 || r.by1 < ry0 || r.by0 > ry1);
+            if (hit) {  // the event staging below reads these: pull them into L1 now
+                const char* sem = reinterpret_cast<const char*>(a.semantics + size_t(g) * C);
+                for (int off = 0; off < int(sizeof(Real)) * C; off += 128)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(sem + off));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(a.brec + g) + 48));
+            }
         }
         unsigned bits = __ballot_sync(0xffffffffu, hit);
         __syncwarp();

@@ -1,23 +1,23 @@
 // K6: per-tile forward multimodal blend.  Replaces the tile loop of rasterize
 // (core/src/rasterizer.cpp:112-187).
 //
-// One CTA per 16x16 tile, one thread per pixel; warps own 8x4 pixel blocks.
-// The tile's Gaussian list is streamed through shared memory in batches of
-// kBatch 48-byte alpha records (coalesced loads, one record per thread).
-// Each warp then culls the batch against its 8x4 block with the records'
-// conservative alpha-support boxes (8 ballots -> a 256-bit mask) and walks only
-// the surviving entries, front to back, exactly as the reference walks the
-// list: alpha test, skip below 1/255, ray-ellipsoid midpoint depth (fallback:
-// centre depth), blend colour/depth/k, T *= 1-alpha, break after blending once
-// T < early_stop_T.  A skipped entry would have failed the alpha test, so the
-// result is the reference's.
+// One CTA per 16x16 tile, one thread per pixel; warps own 8x4 pixel blocks and
+// run INDEPENDENTLY (no block barrier): each warp streams the tile list front
+// to back in 32-entry chunks, culls each chunk against its block with the
+// conservative alpha-support boxes (one ballot), and walks the surviving
+// entries exactly as the reference walks the list: alpha test, skip below
+// 1/255, blend, T *= 1-alpha, break after blending once T < early_stop_T.  A
+// culled entry would have failed the alpha test, so results are the
+// reference's.
 //
-// Semantics (C logits per pixel) accumulate in shared memory rows
-// s_O[warp*32+lane][C] (warp-local order).  When a warp blends Gaussian j at
-// one or more pixels (ballot), its lanes switch to a channel-parallel update:
-// lane ch holds sem_j[ch] and sem_j[ch+32] (one coalesced load each) and adds
-// w_L * sem_j[ch] into the row of every blending lane L.  Per pixel the
-// additions still happen in list order, like the reference's sem_accum.
+// Phase A (per (warp, Gaussian) event, sequential per pixel): alpha, w = alpha T,
+//   colour / k accumulation, T update, contributor count and terminus; the
+//   semantic logits accumulate channel-parallel into shared rows
+//   s_O[lane][C] (lane ch adds w_L * sem_j[ch] for each blending lane L, in
+//   list order per pixel).  Each blended pair is enqueued (pixel, Gaussian, w).
+// Phase B (flush, 32 pairs per warp vector): the ray-ellipsoid midpoint depth
+//   (fallback: centre depth) of every queued pair with all lanes busy, and
+//   w * depth added to the owning pixel's depth sum.
 #include "blend_common.cuh"
 #include "kernels.h"
 
@@ -25,16 +25,51 @@ namespace msplat_cuda {
 
 namespace {
 
-constexpr int kBatch = 256;
 constexpr int kThreads = 256;
-constexpr int kMaskWords = kBatch / 32;
+constexpr int kQueue = 64;
 
 __host__ __device__ inline int sem_pitch(int C) { return C | 1; }  // odd pitch: conflict-free rows
 
 template <typename Real>
+struct FwdWarpSmem {
+    AlphaRec<Real> rec[32];
+    uint32_t gid[32];
+    uint32_t q_lane[kQueue];
+    uint32_t q_gid[kQueue];
+    Real q_w[kQueue];
+    Real q_wd[kQueue];
+};
+
+template <typename Real>
 size_t forward_smem_bytes(int C) {
-    return sizeof(AlphaRec<Real>) * kBatch + sizeof(uint32_t) * kBatch + sizeof(Real) * 8 * 32 +
-           sizeof(Real) * kTilePixels * size_t(C > 0 ? sem_pitch(C) : 0);
+    return 8 * (sizeof(FwdWarpSmem<Real>) + sizeof(Real) * 32 * size_t(C > 0 ? sem_pitch(C) : 0)) + 64;
+}
+
+// Phase B on the first n queue entries (n <= 32).  `own` has bit e set when
+// queue entry e belongs to this lane's pixel.
+template <typename Real>
+__device__ __noinline__ void flush_depth(const ForwardArgs<Real>& a, FwdWarpSmem<Real>* ws, int n, int bx, int by,
+                                         Real& dep, unsigned own) {
+    const int lane = threadIdx.x & 31;
+    if (lane < n) {
+        const int L = int(ws->q_lane[lane]);
+        const uint32_t g = ws->q_gid[lane];
+        const BlendRec<Real>& br = a.brec[g];
+        const int xL = bx + (L & 7), yL = by + (L >> 3);
+        const PixelRay<Real> ray = make_ray<Real>(a.cam, xL, yL);
+        const HitEval<Real> h = intersect<Real>(br, ray, a.cam, a.raw, g);
+        const Real d = !h.hit ? br.zc
+                              : (h.depth_fp64 >= Real(0) ? h.depth_fp64 : midpoint_depth<Real>(a.cam, ray, h.t_mid));
+        if (!isfinite(d)) raise_error(a.err, kErrNonFiniteBlend, (long long)yL * a.W + xL, g);
+        ws->q_wd[lane] = ws->q_w[lane] * d;
+    }
+    __syncwarp();
+    while (own) {  // this pixel's entries, in queue (= list) order
+        const int e = __ffs(own) - 1;
+        own &= own - 1;
+        dep += ws->q_wd[e];
+    }
+    __syncwarp();
 }
 
 }  // namespace
@@ -42,123 +77,137 @@ size_t forward_smem_bytes(int C) {
 template <typename Real>
 __global__ void __launch_bounds__(kThreads, 2) forward_kernel(const ForwardArgs<Real> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    AlphaRec<Real>* s_rec = reinterpret_cast<AlphaRec<Real>*>(smem_raw);
-    uint32_t* s_gid = reinterpret_cast<uint32_t*>(s_rec + kBatch);
-    Real* s_w = reinterpret_cast<Real*>(s_gid + kBatch);  // [8][32]
-    Real* s_O = s_w + 8 * 32;                              // [256][pitch], row = warp*32 + lane
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int C = a.C, pitch = sem_pitch(C);
+    FwdWarpSmem<Real>* ws = reinterpret_cast<FwdWarpSmem<Real>*>(smem_raw) + warp;
+    Real* const warp_O = reinterpret_cast<Real*>(reinterpret_cast<FwdWarpSmem<Real>*>(smem_raw) + 8) +
+                         size_t(warp) * 32 * pitch;
+    Real* const my_O = warp_O + size_t(lane) * pitch;
+    for (int ch = 0; ch < C; ++ch) my_O[ch] = Real(0);
 
     const int tile = blockIdx.x;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int x = tx * kTile + tile_pixel_x(warp, lane);
-    const int y = ty * kTile + tile_pixel_y(warp, lane);
+    const int bx = tx * kTile + (warp & 1) * 8, by = ty * kTile + (warp >> 1) * 4;
+    const int x = bx + (lane & 7), y = by + (lane >> 3);
     const bool inside = x < a.W && y < a.H;
-    const int C = a.C, pitch = sem_pitch(C);
-    Real* const warp_O = s_O + size_t(warp * 32) * pitch;
-    Real* const my_O = warp_O + size_t(lane) * pitch;
-    Real* const warp_w = s_w + warp * 32;
-    for (int ch = 0; ch < C; ++ch) my_O[ch] = Real(0);
-
-    // The warp's pixel-centre rectangle, for culling.
-    const Real rx0 = Real(tx * kTile + (warp & 1) * 8) + Real(0.5), rx1 = rx0 + Real(7);
-    const Real ry0 = Real(ty * kTile + (warp >> 1) * 4) + Real(0.5), ry1 = ry0 + Real(3);
-
-    const PixelRay<Real> ray = make_ray<Real>(a.cam, x, y);
+    const Real pxf = Real(x) + Real(0.5), pyf = Real(y) + Real(0.5);
+    const Real rx0 = Real(bx) + Real(0.5), rx1 = rx0 + Real(7);
+    const Real ry0 = Real(by) + Real(0.5), ry1 = ry0 + Real(3);
     const uint2 range = a.tile_range[tile];
+    const int len = int(range.y - range.x);
 
     Real T = Real(1), col0 = 0, col1 = 0, col2 = 0, dep = 0, kk = 0;
     int count = 0, last = 0;
     bool done = !inside;
     const Real early = Real(a.rp.early_stop_T);
+    const bool c0 = lane < C, c1 = lane + 32 < C;
+    int qn = 0;
+    unsigned long long own = 0;  // queue entries owned by this pixel
 
-    for (uint32_t b0 = range.x; b0 < range.y; b0 += kBatch) {
-        const int nb = int(min(uint32_t(kBatch), range.y - b0));
-        __syncthreads();
-        if (int(threadIdx.x) < nb) {
-            const uint32_t g = a.inst_gauss[b0 + threadIdx.x];
-            s_gid[threadIdx.x] = g;
-            s_rec[threadIdx.x] = a.arec[g];
+    for (int c = 0; c * 32 < len; ++c) {
+        if (__all_sync(0xffffffffu, done)) break;
+        const int pos = c * 32 + lane;
+        bool hit = false;
+        if (pos < len) {
+            const uint32_t g = a.inst_gauss[range.x + pos];
+            const AlphaRec<Real> r = a.arec[g];
+            ws->rec[lane] = r;
+            ws->gid[lane] = g;
+            hit = !(r.bx1 < rx0 || r.bx0 > rx1 || r.by1 < ry0 || r.by0 > ry1);
+            if (hit) asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(a.brec + g)));
         }
-        __syncthreads();
-        if (!__all_sync(0xffffffffu, done)) {
-            uint32_t wm[kMaskWords];
-#pragma unroll
-            for (int r = 0; r < kMaskWords; ++r) {
-                const int i = r * 32 + lane;
-                bool hit = false;
-                if (i < nb) {
-                    const AlphaRec<Real>& g = s_rec[i];
-                    hit = !(g.bx1 < rx0 || g.bx0 > rx1 || g.by1 < ry0 || g.by0 > ry1);
+        unsigned bits = __ballot_sync(0xffffffffu, hit);
+        __syncwarp();
+        while (bits) {
+            const int slot = __ffs(bits) - 1;
+            bits &= bits - 1;
+            AlphaEval<Real> ae;
+            ae.pass = false;
+            if (!done) ae = eval_alpha<Real>(ws->rec[slot], pxf, pyf);
+            const unsigned mask = __ballot_sync(0xffffffffu, ae.pass);
+            if (mask == 0) continue;
+            const uint32_t g = ws->gid[slot];
+            if (ae.pass) {
+                if (!isfinite(ae.alpha)) {
+                    raise_error(a.err, kErrNonFiniteBlend, (long long)y * a.W + x, g);
+                    done = true;
                 }
-                wm[r] = __ballot_sync(0xffffffffu, hit);
+                const BlendRec<Real>& br = a.brec[g];
+                const Real w = ae.alpha * T;
+                col0 += w * br.rgb[0];
+                col1 += w * br.rgb[1];
+                col2 += w * br.rgb[2];
+                kk += w * br.k;
+                if (a.weight_sums) atomicAdd(a.weight_sums + g, w);
+                const int e = qn + __popc(mask & ((1u << lane) - 1u));
+                own |= 1ull << e;
+                ws->q_lane[e] = uint32_t(lane);
+                ws->q_gid[e] = g;
+                ws->q_w[e] = w;
+                T *= (Real(1) - ae.alpha);
+                ++count;
+                last = c * 32 + slot + 1;
+                if (a.rp.early_termination && T < early) done = true;
             }
-#pragma unroll
-            for (int r = 0; r < kMaskWords; ++r) {
-                unsigned bits = wm[r];
-                while (bits) {
-                    const int j = r * 32 + __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    AlphaEval<Real> ae;
-                    ae.pass = false;
-                    if (!done) ae = eval_alpha<Real>(s_rec[j], ray.px, ray.py);
-                    const unsigned mask = __ballot_sync(0xffffffffu, ae.pass);
-                    if (mask == 0) continue;
-                    const uint32_t g = s_gid[j];
-                    if (ae.pass) {
-                        const BlendRec<Real>& br = a.brec[g];
-                        const HitEval<Real> h = intersect<Real>(br, ray, a.cam, a.raw, g);
-                        const Real d = !h.hit ? br.zc
-                                              : (h.depth_fp64 >= Real(0) ? h.depth_fp64
-                                                                         : midpoint_depth<Real>(a.cam, ray, h.t_mid));
-                        if (!isfinite(ae.alpha) || !isfinite(d)) {
-                            raise_error(a.err, kErrNonFiniteBlend, (long long)y * a.W + x, g);
-                            done = true;
-                        }
-                        const Real w = ae.alpha * T;
-                        col0 += w * br.rgb[0];
-                        col1 += w * br.rgb[1];
-                        col2 += w * br.rgb[2];
-                        dep += w * d;
-                        kk += w * br.k;
-                        if (a.weight_sums) atomicAdd(a.weight_sums + g, w);
-                        warp_w[lane] = w;
-                        T *= (Real(1) - ae.alpha);
-                        ++count;
-                        last = int(b0 - range.x) + j + 1;
-                        if (a.rp.early_termination && T < early) done = true;
+            __syncwarp();
+            const int npairs = __popc(mask);
+            if (C > 0) {  // semantic logits, channel-parallel, list order per pixel
+                const Real* semg = a.semantics + size_t(g) * C;
+                const Real sv0 = c0 ? semg[lane] : Real(0);
+                const Real sv1 = c1 ? semg[lane + 32] : Real(0);
+                // The event's rows are distinct pixels: batch the loads before the
+                // stores so the shared-memory round trips overlap.
+                const int cc0 = c0 ? lane : 0, cc1 = c1 ? lane + 32 : 0;
+                int e = qn;
+                for (; e + 4 <= qn + npairs; e += 4) {
+                    Real* r0 = warp_O + int(ws->q_lane[e]) * pitch;
+                    Real* r1 = warp_O + int(ws->q_lane[e + 1]) * pitch;
+                    Real* r2 = warp_O + int(ws->q_lane[e + 2]) * pitch;
+                    Real* r3 = warp_O + int(ws->q_lane[e + 3]) * pitch;
+                    const Real w0 = ws->q_w[e], w1 = ws->q_w[e + 1], w2 = ws->q_w[e + 2], w3 = ws->q_w[e + 3];
+                    const Real a0 = r0[cc0], a1 = r1[cc0], a2 = r2[cc0], a3 = r3[cc0];
+                    const Real b0 = r0[cc1], b1 = r1[cc1], b2 = r2[cc1], b3 = r3[cc1];
+                    if (c0) {
+                        r0[lane] = a0 + w0 * sv0;
+                        r1[lane] = a1 + w1 * sv0;
+                        r2[lane] = a2 + w2 * sv0;
+                        r3[lane] = a3 + w3 * sv0;
                     }
-                    if (C > 0) {
-                        __syncwarp();
-                        const Real* semg = a.semantics + size_t(g) * C;
-                        const bool c0 = lane < C, c1 = lane + 32 < C;
-                        const Real sv0 = c0 ? semg[lane] : Real(0);
-                        const Real sv1 = c1 ? semg[lane + 32] : Real(0);
-                        unsigned m = mask;
-                        while (m) {
-                            const int L = __ffs(m) - 1;
-                            m &= m - 1;
-                            const Real wL = warp_w[L];
-                            Real* row = warp_O + L * pitch;
-                            if (c0) row[lane] += wL * sv0;
-                            if (c1) row[lane + 32] += wL * sv1;
-                        }
-                        for (int ch = lane + 64; ch < C; ch += 32) {  // C > 64
-                            const Real sv = semg[ch];
-                            unsigned m2 = mask;
-                            while (m2) {
-                                const int L = __ffs(m2) - 1;
-                                m2 &= m2 - 1;
-                                warp_O[L * pitch + ch] += warp_w[L] * sv;
-                            }
-                        }
-                        __syncwarp();
+                    if (c1) {
+                        r0[lane + 32] = b0 + w0 * sv1;
+                        r1[lane + 32] = b1 + w1 * sv1;
+                        r2[lane + 32] = b2 + w2 * sv1;
+                        r3[lane + 32] = b3 + w3 * sv1;
                     }
                 }
+                for (; e < qn + npairs; ++e) {
+                    const Real wL = ws->q_w[e];
+                    Real* row = warp_O + int(ws->q_lane[e]) * pitch;
+                    if (c0) row[lane] += wL * sv0;
+                    if (c1) row[lane + 32] += wL * sv1;
+                }
+                for (int ch = lane + 64; ch < C; ch += 32) {  // C > 64
+                    const Real sv = semg[ch];
+                    for (int e = qn; e < qn + npairs; ++e) warp_O[int(ws->q_lane[e]) * pitch + ch] += ws->q_w[e] * sv;
+                }
+                __syncwarp();
+            }
+            qn += npairs;
+            if (qn >= 32) {
+                flush_depth<Real>(a, ws, 32, bx, by, dep, unsigned(own));
+                own >>= 32;
+                const int rest = qn - 32;
+                if (lane < rest) {  // reads >= 32, writes < 32
+                    ws->q_lane[lane] = ws->q_lane[32 + lane];
+                    ws->q_gid[lane] = ws->q_gid[32 + lane];
+                    ws->q_w[lane] = ws->q_w[32 + lane];
+                }
+                qn = rest;
+                __syncwarp();
             }
         }
-        if (__syncthreads_and(done)) break;
     }
-    __syncwarp();
+    if (qn > 0) flush_depth<Real>(a, ws, qn, bx, by, dep, unsigned(own));
     if (!inside) return;
     col0 += T * Real(a.rp.bg[0]);
     col1 += T * Real(a.rp.bg[1]);
