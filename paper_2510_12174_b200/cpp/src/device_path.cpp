@@ -1,0 +1,450 @@
+// msplat C++ drop-in: the render path on the B200.
+//
+// rasterize / rasterize_backward / estimate_normals / normals_backward /
+// chain_activations / bin_and_sort keep the reference signatures
+// (msplat/rasterizer.hpp:52-83, normals.hpp:33-43, scene.hpp:74) and run
+// through the C ABI of include/msplat_b200.h.  This file only marshals: AoS
+// Eigen doubles <-> SoA device buffers, HWC host grids <-> planar device grids,
+// and msplat_status -> the reference's exception types and messages.
+//
+// Precision: MSPLAT_F64 unless MSPLAT_PRECISION=32 is set in the environment.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "msplat/normals.hpp"
+#include "msplat/rasterizer.hpp"
+#include "msplat/scene.hpp"
+#include "msplat_b200.h"
+
+namespace msplat {
+
+namespace {
+
+void rethrow(msplat_status st) {
+    if (st == MSPLAT_OK) return;
+    const std::string m = msplat_last_error();
+    if (st == MSPLAT_ERR_INVALID_ARGUMENT) throw std::invalid_argument(m);
+    if (st == MSPLAT_ERR_LOGIC) throw std::logic_error(m);
+    throw std::runtime_error(m);
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+bool use_fp32() {
+    const char* p = std::getenv("MSPLAT_PRECISION");
+    return p && std::string(p) == "32";
+}
+
+msplat_context* context() {
+    thread_local std::unique_ptr<msplat_context, void (*)(msplat_context*)> ctx(nullptr, msplat_context_destroy);
+    if (!ctx) {
+        const char* d = std::getenv("MSPLAT_DEVICE");
+        msplat_context* c = nullptr;
+        rethrow(msplat_context_create(d ? std::atoi(d) : 0, nullptr, &c));
+        ctx.reset(c);
+    }
+    return ctx.get();
+}
+
+// Device buffer holding host doubles converted to the kernel precision.
+struct DBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    bool f32 = false;
+    DBuf() = default;
+    DBuf(size_t count, bool fp32) : n(count), f32(fp32) {
+        cuda_check(cudaMalloc(&p, std::max<size_t>(count, 1) * (fp32 ? 4 : 8)), "cudaMalloc");
+        cuda_check(cudaMemset(p, 0, std::max<size_t>(count, 1) * (fp32 ? 4 : 8)), "cudaMemset");
+    }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    void upload(const std::vector<double>& h) {
+        if (h.empty()) return;
+        if (f32) {
+            std::vector<float> t(h.begin(), h.end());
+            cuda_check(cudaMemcpy(p, t.data(), t.size() * 4, cudaMemcpyHostToDevice), "upload");
+        } else {
+            cuda_check(cudaMemcpy(p, h.data(), h.size() * 8, cudaMemcpyHostToDevice), "upload");
+        }
+    }
+    std::vector<double> download() const {
+        std::vector<double> h(n);
+        if (!n) return h;
+        if (f32) {
+            std::vector<float> t(n);
+            cuda_check(cudaMemcpy(t.data(), p, n * 4, cudaMemcpyDeviceToHost), "download");
+            h.assign(t.begin(), t.end());
+        } else {
+            cuda_check(cudaMemcpy(h.data(), p, n * 8, cudaMemcpyDeviceToHost), "download");
+        }
+        return h;
+    }
+};
+
+// Scene -> SoA device buffers (scene.hpp layout; sh rows per colour channel).
+struct DeviceScene {
+    bool f32;
+    int64_t n;
+    int C, deg, K;
+    DBuf means, quats, log_scales, opac, k, sh, sem;
+    DeviceScene(const Scene& s, bool fp32)
+        : f32(fp32), n(int64_t(s.size())), C(s.num_classes), deg(s.sh_degree), K(s.sh_coeff_count()),
+          means(3 * n, fp32), quats(4 * n, fp32), log_scales(3 * n, fp32), opac(n, fp32), k(n, fp32),
+          sh(size_t(3 * K) * n, fp32), sem(size_t(C) * n, fp32) {
+        std::vector<double> m(3 * n), q(4 * n), ls(3 * n), o(n), kk(n), shv(size_t(3 * K) * n), se(size_t(C) * n);
+        for (int64_t i = 0; i < n; ++i) {
+            const GaussianPrimitive& g = s.gaussians[size_t(i)];
+            for (int j = 0; j < 3; ++j) {
+                m[3 * i + j] = g.position[j];
+                ls[3 * i + j] = g.log_scale[j];
+            }
+            for (int j = 0; j < 4; ++j) q[4 * i + j] = g.rotation[j];
+            o[i] = g.opacity_logit;
+            kk[i] = g.gradient_factor;
+            for (int c = 0; c < 3; ++c)
+                for (int j = 0; j < K; ++j) shv[(i * 3 + c) * K + j] = g.sh(c, j);
+            for (int c = 0; c < C; ++c) se[i * C + c] = g.semantic_logits[c];
+        }
+        means.upload(m);
+        quats.upload(q);
+        log_scales.upload(ls);
+        opac.upload(o);
+        k.upload(kk);
+        sh.upload(shv);
+        sem.upload(se);
+    }
+    msplat_scene abi() const {
+        return msplat_scene{n, C, deg, f32 ? MSPLAT_F32 : MSPLAT_F64, means.p, quats.p, log_scales.p, opac.p,
+                            k.p, sh.p, C ? sem.p : nullptr};
+    }
+};
+
+msplat_camera to_abi(const CameraView& v) {
+    msplat_camera c{};
+    c.fx = v.fx;
+    c.fy = v.fy;
+    c.cx = v.cx;
+    c.cy = v.cy;
+    c.width = v.width;
+    c.height = v.height;
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) c.R_c2w[i * 3 + j] = v.R_cam_to_world(i, j);
+        c.t_c2w[i] = v.t_cam_to_world[i];
+    }
+    return c;
+}
+
+msplat_render_config to_abi(const RenderConfig& r) {
+    return msplat_render_config{r.sigma_scale, {r.background.x(), r.background.y(), r.background.z()},
+                                r.early_stop_transmittance, r.early_termination ? 1 : 0, r.threads};
+}
+
+msplat_normal_config to_abi(const NormalConfig& n) {
+    return msplat_normal_config{n.step1, n.step2, n.fuse_lambda, n.mask_threshold};
+}
+
+// HWC grid <-> planar [C][H][W] host vectors.
+std::vector<double> to_planar(const GridF& g) {
+    const int W = g.width(), H = g.height(), C = g.channels();
+    std::vector<double> out(size_t(W) * H * C);
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x)
+            for (int c = 0; c < C; ++c) out[(size_t(c) * H + y) * W + x] = g.at(x, y, c);
+    return out;
+}
+
+GridF from_planar(const std::vector<double>& v, int W, int H, int C) {
+    GridF g(W, H, C, 0.0);
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x)
+            for (int c = 0; c < C; ++c) g.at(x, y, c) = v[(size_t(c) * H + y) * W + x];
+    return g;
+}
+
+}  // namespace
+
+struct DeviceReplay {
+    msplat_replay* handle = nullptr;
+    bool f32 = false;
+    explicit DeviceReplay(bool fp32) : f32(fp32) {
+        rethrow(msplat_replay_create(context(), &handle));
+        rethrow(msplat_replay_set_capture(handle, 3));
+    }
+    ~DeviceReplay() { msplat_replay_destroy(handle); }
+};
+
+PixelGradients PixelGradients::zero(int width, int height, int num_classes) {
+    PixelGradients pg;
+    pg.dcolor = GridF(width, height, 3, 0.0);
+    pg.ddepth = GridF(width, height, 1, 0.0);
+    pg.dsemantics = GridF(width, height, num_classes, 0.0);
+    pg.dkmap = GridF(width, height, 1, 0.0);
+    return pg;
+}
+
+// bin_and_sort -- core/src/rasterizer.cpp:14-45, on the device radix sort.
+TileBins bin_and_sort(const std::vector<std::optional<Splat2D>>& splats, int width, int height) {
+    const int64_t n = int64_t(splats.size());
+    std::vector<uint8_t> vis(n);
+    std::vector<double> center(2 * n), radius(n), depth(n);
+    for (int64_t i = 0; i < n; ++i) {
+        vis[i] = splats[i].has_value();
+        if (!vis[i]) continue;
+        center[2 * i] = splats[i]->center.x();
+        center[2 * i + 1] = splats[i]->center.y();
+        radius[i] = splats[i]->radius;
+        depth[i] = splats[i]->sort_depth;
+    }
+    TileBins out;
+    out.tiles_x = (width + TileBins::kTileSize - 1) / TileBins::kTileSize;
+    out.tiles_y = (height + TileBins::kTileSize - 1) / TileBins::kTileSize;
+    const size_t tiles = size_t(out.tiles_x) * out.tiles_y;
+    std::vector<int64_t> off(tiles + 1);
+    std::vector<int32_t> vals(std::max<int64_t>(n, 1) * 4);
+    int64_t count = 0;
+    for (;;) {
+        rethrow(msplat_bin_and_sort_host(context(), n, vis.data(), center.data(), radius.data(), depth.data(), width,
+                                         height, off.data(), vals.data(), int64_t(vals.size()), &count));
+        if (count <= int64_t(vals.size())) break;
+        vals.resize(size_t(count));
+    }
+    out.bins.resize(tiles);
+    for (size_t t = 0; t < tiles; ++t) out.bins[t].assign(vals.begin() + off[t], vals.begin() + off[t + 1]);
+    return out;
+}
+
+// rasterize -- core/src/rasterizer.cpp:87-205
+MultimodalFrame rasterize(const Scene& scene, const CameraView& view, const RenderConfig& cfg, ReplayState* replay) {
+    scene.validate();
+    const bool f32 = use_fp32();
+    const int W = view.width, H = view.height, C = scene.num_classes;
+    const size_t HW = size_t(W) * H;
+    DeviceScene ds(scene, f32);
+    DBuf color(3 * HW, f32), depth(HW, f32), sem(size_t(C) * HW, f32), kmap(HW, f32), T(HW, f32), normals(3 * HW, f32);
+    int32_t* contrib = nullptr;
+    cuda_check(cudaMalloc(&contrib, std::max<size_t>(HW, 1) * 4), "cudaMalloc");
+    std::unique_ptr<int32_t, decltype(&cudaFree)> contrib_guard(contrib, cudaFree);
+    msplat_frame fr{color.p, depth.p, C ? sem.p : nullptr, kmap.p, T.p, nullptr, contrib};
+    auto dev = replay ? std::make_shared<DeviceReplay>(f32) : nullptr;
+    const msplat_scene s = ds.abi();
+    const msplat_camera c = to_abi(view);
+    const msplat_render_config rc = to_abi(cfg);
+    rethrow(msplat_rasterize(context(), &s, &c, &rc, &fr, dev ? dev->handle : nullptr));
+
+    MultimodalFrame f;
+    f.width = W;
+    f.height = H;
+    f.num_classes = C;
+    f.color = from_planar(color.download(), W, H, 3);
+    f.depth = from_planar(depth.download(), W, H, 1);
+    f.semantics = C ? from_planar(sem.download(), W, H, C) : GridF(W, H, 0, 0.0);
+    f.kmap = from_planar(kmap.download(), W, H, 1);
+    f.transmittance = from_planar(T.download(), W, H, 1);
+    f.normals = GridF(W, H, 3, 0.0);  // filled by estimate_normals, as in the reference
+    f.contributors = Grid<int>(W, H, 1, 0);
+    cuda_check(cudaMemcpy(f.contributors.data(), contrib, HW * 4, cudaMemcpyDeviceToHost), "download");
+
+    if (replay) {
+        const size_t n = scene.size();
+        replay->device = dev;
+        replay->activated = activate_scene(scene);  // borrows from `scene`, like the reference
+        std::vector<uint8_t> vis(n), cl(3 * n);
+        std::vector<double> center(2 * n), conic(3 * n), sdepth(n), radius(n), rgb(3 * n);
+        rethrow(msplat_replay_splats(dev->handle, vis.data(), center.data(), conic.data(), sdepth.data(),
+                                     radius.data(), rgb.data(), cl.data()));
+        replay->splats.assign(n, std::nullopt);
+        replay->colors.assign(n, ShColor{});
+        for (size_t i = 0; i < n; ++i) {
+            if (!vis[i]) continue;
+            Splat2D sp;
+            sp.center = Vec2(center[2 * i], center[2 * i + 1]);
+            sp.conic << conic[3 * i], conic[3 * i + 1], conic[3 * i + 1], conic[3 * i + 2];
+            const Scalar det = conic[3 * i] * conic[3 * i + 2] - conic[3 * i + 1] * conic[3 * i + 1];
+            sp.cov << conic[3 * i + 2] / det, -conic[3 * i + 1] / det, -conic[3 * i + 1] / det, conic[3 * i] / det;
+            sp.sort_depth = sdepth[i];
+            sp.radius = radius[i];
+            replay->splats[i] = sp;
+            for (int ch = 0; ch < 3; ++ch) {
+                replay->colors[i].rgb[ch] = rgb[3 * i + ch];
+                replay->colors[i].clamped[ch] = cl[3 * i + ch] != 0;
+            }
+        }
+        msplat_counters cn{};
+        rethrow(msplat_replay_counters(dev->handle, &cn));
+        std::vector<int64_t> off(size_t(cn.tiles) + 1);
+        std::vector<int32_t> vals(size_t(std::max<int64_t>(cn.instances, 1)));
+        rethrow(msplat_replay_bins(dev->handle, off.data(), vals.data(), int64_t(vals.size())));
+        replay->bins.tiles_x = (W + TileBins::kTileSize - 1) / TileBins::kTileSize;
+        replay->bins.tiles_y = (H + TileBins::kTileSize - 1) / TileBins::kTileSize;
+        replay->bins.bins.assign(size_t(cn.tiles), {});
+        for (size_t t = 0; t < size_t(cn.tiles); ++t)
+            replay->bins.bins[t].assign(vals.begin() + off[t], vals.begin() + off[t + 1]);
+        replay->terminus = Grid<int>(W, H, 1, 0);
+        rethrow(msplat_replay_terminus(dev->handle, replay->terminus.data()));
+        replay->weight_sums.assign(n, 0.0);
+        if (n) rethrow(msplat_replay_weight_sums(dev->handle, replay->weight_sums.data()));
+        replay->num_gaussians = n;
+        replay->sh_degree = scene.sh_degree;
+        replay->num_classes = scene.num_classes;
+        replay->cfg = cfg;
+    }
+    return f;
+}
+
+namespace {
+
+void grads_from_device(GradientBuffer& g, const Scene& scene, DBuf& dpos, DBuf& drot, DBuf& dsc, DBuf& dop, DBuf& dk,
+                       DBuf& dsh, DBuf& dsem) {
+    g.resize_zero(scene);
+    const int K = scene.sh_coeff_count(), C = scene.num_classes;
+    const auto p = dpos.download(), r = drot.download(), s = dsc.download(), o = dop.download(), k = dk.download(),
+               h = dsh.download(), e = dsem.download();
+    for (size_t i = 0; i < scene.size(); ++i) {
+        g.dposition[i] = Vec3(p[3 * i], p[3 * i + 1], p[3 * i + 2]);
+        g.drotation[i] = Vec4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+        g.dscale[i] = Vec3(s[3 * i], s[3 * i + 1], s[3 * i + 2]);
+        g.dopacity[i] = o[i];
+        g.dk[i] = k[i];
+        for (int c = 0; c < 3; ++c)
+            for (int j = 0; j < K; ++j) g.dsh[i](c, j) = h[(i * 3 + c) * K + j];
+        for (int c = 0; c < C; ++c) g.dsemantics[i][c] = e[i * C + c];
+    }
+}
+
+}  // namespace
+
+// rasterize_backward -- core/src/rasterizer_backward.cpp:127-264 (check_replay :35-53)
+GradientBuffer rasterize_backward(const Scene& scene, const CameraView& view, const MultimodalFrame& frame,
+                                  const ReplayState& replay, const PixelGradients& pix) {
+    if (replay.num_gaussians != scene.size() || replay.sh_degree != scene.sh_degree ||
+        replay.num_classes != scene.num_classes || !replay.device)
+        throw std::runtime_error("rasterize_backward: replay state does not match the scene");
+    for (size_t i = 0; i < scene.size(); ++i)
+        if ((replay.activated[i].position.array() != scene.gaussians[i].position.array()).any() ||
+            replay.activated[i].k != scene.gaussians[i].gradient_factor)
+            throw std::runtime_error("rasterize_backward: scene modified since forward (primitive " +
+                                     std::to_string(i) + ")");
+    if (frame.width != view.width || frame.height != view.height)
+        throw std::runtime_error("rasterize_backward: frame/view size mismatch");
+    const bool ok = pix.dcolor.width() == frame.width && pix.dcolor.height() == frame.height &&
+                    pix.dcolor.channels() == 3 && pix.ddepth.same_shape(frame.depth) &&
+                    pix.dsemantics.same_shape(frame.semantics) && pix.dkmap.same_shape(frame.kmap);
+    if (!ok) throw std::runtime_error("rasterize_backward: pixel-gradient shape mismatch");
+
+    const bool f32 = replay.device->f32;
+    const int W = frame.width, H = frame.height, C = scene.num_classes;
+    const size_t HW = size_t(W) * H, n = scene.size();
+    DeviceScene ds(scene, f32);
+    DBuf T(HW, f32), dC(3 * HW, f32), dD(HW, f32), dO(size_t(C) * HW, f32), dK(HW, f32);
+    T.upload(to_planar(frame.transmittance));
+    dC.upload(to_planar(pix.dcolor));
+    dD.upload(to_planar(pix.ddepth));
+    if (C) dO.upload(to_planar(pix.dsemantics));
+    dK.upload(to_planar(pix.dkmap));
+    const int K = scene.sh_coeff_count();
+    DBuf gpos(3 * n, f32), grot(4 * n, f32), gsc(3 * n, f32), gop(n, f32), gk(n, f32), gsh(size_t(3 * K) * n, f32),
+        gsem(size_t(C) * n, f32);
+    msplat_frame fr{nullptr, nullptr, nullptr, nullptr, T.p, nullptr, nullptr};
+    msplat_pixel_grads pg{dC.p, dD.p, C ? dO.p : nullptr, dK.p, nullptr};
+    msplat_grads g{gpos.p, grot.p, gsc.p, gop.p, gk.p, gsh.p, C ? gsem.p : nullptr};
+    const msplat_scene s = ds.abi();
+    const msplat_camera c = to_abi(view);
+    rethrow(msplat_rasterize_backward(context(), &s, &c, &fr, replay.device->handle, &pg, &g));
+    GradientBuffer out;
+    grads_from_device(out, scene, gpos, grot, gsc, gop, gk, gsh, gsem);
+    return out;
+}
+
+// chain_activations -- core/src/scene.cpp:108-129, on the device.
+void chain_activations(GradientBuffer& buf, const Scene& scene) {
+    if (buf.size() != scene.size()) throw std::invalid_argument("chain_activations: buffer/scene size mismatch");
+    if (buf.raw_space) throw std::logic_error("chain_activations: buffer already in raw-parameter space");
+    const bool f32 = use_fp32();
+    const size_t n = scene.size();
+    DeviceScene ds(scene, f32);
+    DBuf grot(4 * n, f32), gsc(3 * n, f32), gop(n, f32);
+    std::vector<double> r(4 * n), sc(3 * n), op(n);
+    for (size_t i = 0; i < n; ++i) {
+        for (int j = 0; j < 4; ++j) r[4 * i + j] = buf.drotation[i][j];
+        for (int j = 0; j < 3; ++j) sc[3 * i + j] = buf.dscale[i][j];
+        op[i] = buf.dopacity[i];
+    }
+    grot.upload(r);
+    gsc.upload(sc);
+    gop.upload(op);
+    msplat_grads g{nullptr, grot.p, gsc.p, gop.p, nullptr, nullptr, nullptr};
+    const msplat_scene s = ds.abi();
+    rethrow(msplat_chain_activations(context(), &s, &g));
+    rethrow(msplat_context_check(context()));
+    r = grot.download();
+    sc = gsc.download();
+    op = gop.download();
+    for (size_t i = 0; i < n; ++i) {
+        buf.drotation[i] = Vec4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+        buf.dscale[i] = Vec3(sc[3 * i], sc[3 * i + 1], sc[3 * i + 2]);
+        buf.dopacity[i] = op[i];
+    }
+    buf.raw_space = true;
+}
+
+// estimate_normals -- core/src/normals.cpp:28-101, on the device.
+NormalState estimate_normals(const GridF& depth, const GridF& transmittance, const CameraView& view,
+                             const NormalConfig& cfg, GridF& normals) {
+    if (cfg.step1 >= cfg.step2) throw std::invalid_argument("estimate_normals: step1 must be smaller than step2");
+    if (cfg.fuse_lambda < 0 || cfg.fuse_lambda > 1)
+        throw std::invalid_argument("estimate_normals: fuse weight must be in [0,1]");
+    NormalState st;
+    st.p_world = backproject(depth, view);  // also validates the depth shape
+    const int W = view.width, H = view.height;
+    const size_t HW = size_t(W) * H;
+    const bool f32 = use_fp32();
+    DBuf d(HW, f32), t(HW, f32), nrm(3 * HW, f32);
+    d.upload(depth.storage());
+    t.upload(transmittance.storage());
+    const msplat_camera c = to_abi(view);
+    const msplat_normal_config nc = to_abi(cfg);
+    rethrow(msplat_estimate_normals(context(), f32 ? MSPLAT_F32 : MSPLAT_F64, d.p, t.p, &c, &nc, nrm.p));
+    rethrow(msplat_context_check(context()));
+    normals = from_planar(nrm.download(), W, H, 3);
+    st.width = W;
+    st.height = H;
+    st.cfg = cfg;
+    st.valid = Grid<std::uint8_t>(W, H, 1, 0);
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x)
+            st.valid.at(x, y) = normals.at(x, y, 0) != 0 || normals.at(x, y, 1) != 0 || normals.at(x, y, 2) != 0;
+    st.depth = depth;
+    st.transmittance = transmittance;
+    return st;
+}
+
+// normals_backward -- core/src/normals.cpp:103-152, gather form on the device.
+GridF normals_backward(const GridF& dL_dnormals, const NormalState& state, const CameraView& view) {
+    const int W = state.width, H = state.height;
+    if (dL_dnormals.width() != W || dL_dnormals.height() != H || dL_dnormals.channels() != 3)
+        throw std::invalid_argument("normals_backward: gradient shape mismatch");
+    const size_t HW = size_t(W) * H;
+    const bool f32 = use_fp32();
+    DBuf g(3 * HW, f32), d(HW, f32), t(HW, f32), dD(HW, f32);
+    g.upload(to_planar(dL_dnormals));
+    d.upload(state.depth.storage());
+    t.upload(state.transmittance.storage());
+    const msplat_camera c = to_abi(view);
+    const msplat_normal_config nc = to_abi(state.cfg);
+    rethrow(msplat_normals_backward(context(), f32 ? MSPLAT_F32 : MSPLAT_F64, g.p, d.p, t.p, &c, &nc, 1.0, dD.p));
+    rethrow(msplat_context_check(context()));
+    return from_planar(dD.download(), W, H, 1);
+}
+
+}  // namespace msplat
