@@ -160,6 +160,12 @@ MSPLAT_API void msplat_context_destroy(msplat_context* ctx);
 MSPLAT_API msplat_status msplat_context_set_stream(msplat_context* ctx, void* cuda_stream);
 /* Synchronizing: waits for the stream and reports a latched device error. */
 MSPLAT_API msplat_status msplat_context_check(msplat_context* ctx);
+/* Deterministic backward (TrainConfig::deterministic, msplat/trainer.hpp:48-63;
+ * tests/test_rasterizer.cpp:386-419): K9 writes per-(instance, warp) partial
+ * slots instead of float atomics and a fixed-order reduction sums them, so
+ * gradients are bitwise reproducible run to run.  Costs ~8 (20+C) reals per
+ * instance of scratch and a host sync per backward (not graph-capturable). */
+MSPLAT_API msplat_status msplat_context_set_deterministic(msplat_context* ctx, int enable);
 
 MSPLAT_API msplat_status msplat_replay_create(msplat_context* ctx, msplat_replay** out);
 MSPLAT_API void msplat_replay_destroy(msplat_replay* replay);

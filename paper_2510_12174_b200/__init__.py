@@ -10,7 +10,7 @@ from .rasterizer import (  # noqa: F401
     CameraView, GradientBuffer, LogicError, MultimodalFrame, NormalConfig, OptimizerState,
     PixelGradients, RenderConfig, ReplayState, Scene, TileBins, TrainConfig, adam_step, bin_and_sort,
     chain_activations, estimate_normals, fwd_bwd, make_camera, make_lookat_camera, normals_backward,
-    param_layout, prune, rasterize, rasterize_backward,
+    param_layout, prune, rasterize, rasterize_backward, set_deterministic, set_stage_timing, stage_timings,
 )
 
 __version__ = "0.1.0"

@@ -111,6 +111,7 @@ def _sig(lib):
         ("msplat_bin_and_sort_host", ct.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, ct.c_int, ct.c_int,
                                                 P(_i64), P(ct.c_int32), _i64, P(_i64)]),
         ("msplat_context_set_timing", ct.c_int, [_vp, ct.c_int]),
+        ("msplat_context_set_deterministic", ct.c_int, [_vp, ct.c_int]),
         ("msplat_context_timings", ct.c_int, [_vp, P(ct.c_double), P(_i64)]),
         ("msplat_kernel_launches", _i64, []),
     ]

@@ -49,6 +49,9 @@ msplat_context* context() {
         const char* d = std::getenv("MSPLAT_DEVICE");
         msplat_context* c = nullptr;
         rethrow(msplat_context_create(d ? std::atoi(d) : 0, nullptr, &c));
+        // The reference's accumulation is reproducible at a fixed thread count
+        // (tests/test_rasterizer.cpp:386-419): fixed-order reduction, no atomics.
+        rethrow(msplat_context_set_deterministic(c, 1));
         ctx.reset(c);
     }
     return ctx.get();

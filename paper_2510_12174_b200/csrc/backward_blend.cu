@@ -25,6 +25,7 @@
 //   contiguous) and one atomic per value per Gaussian.
 #include "blend_common.cuh"
 #include "kernels.h"
+#include "radix_sort.cuh"
 
 namespace msplat_cuda {
 
@@ -45,6 +46,7 @@ template <typename Real>
 struct PairQueue {
     uint32_t meta[kQueue];  // pixel lane | clamped << 8
     uint32_t gid[kQueue];
+    uint32_t inst[kQueue];  // position in the tile-sorted list (deterministic mode)
     Real w[kQueue], da[kQueue], al[kQueue], gs[kQueue];
     Real cx[kQueue], cy[kQueue], ca[kQueue], cb[kQueue], cc[kQueue];
 };
@@ -101,6 +103,7 @@ __device__ __noinline__ void flush_pairs(const BackwardArgs<Real>& a, const Pair
     const bool act = lane < n;
     const uint32_t meta = act ? q.meta[lane] : 0u;
     const uint32_t g = act ? q.gid[lane] : 0xffffffffu - lane;  // padding lanes: unique keys
+    const uint32_t inst = act ? q.inst[lane] : 0u;
     bool same[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
@@ -200,10 +203,17 @@ __device__ __noinline__ void flush_pairs(const BackwardArgs<Real>& a, const Pair
             }
         }
     }
+    // Deterministic mode: this (instance, warp) owns a private slot; plain
+    // read-modify-write in program order, reduced later in a fixed order.
+    Real* const slot = a.partial ? a.partial + (size_t(inst) * 8 + (threadIdx.x >> 5)) * a.V : nullptr;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
         const Real s = seg_sum<Real>(v[i], same);
         if (head && s != Real(0)) {
+            if (slot) {
+                slot[i] += s;
+                continue;
+            }
             Real* dst;
             if (i == 0) dst = a.g_opac + g;
             else if (i < 3) dst = a.acc_dmean + size_t(g) * 2 + (i - 1);
@@ -327,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
                 const AlphaRec<Real>& ar = ws->rec[slot];
                 Q.meta[e] = uint32_t(lane) | (ae.clamped ? (1u << 8) : 0u);
                 Q.gid[e] = g;
+                Q.inst[e] = list0 + uint32_t(c * 32 + slot);
                 Q.w[e] = w;
                 Q.da[e] = dalpha;
                 Q.al[e] = ae.alpha;
@@ -348,13 +359,22 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
                     acc0 += we * seedL[c0];
                     acc1 += we * seedL[c1];
                 }
-                if (lane < S && acc0 != Real(0)) {
+                if (a.partial) {  // fields 16 + ch: dcolor, dk, dsem
+                    Real* const ps = a.partial + (size_t(list0 + c * 32 + slot) * 8 + warp) * a.V + 16;
+                    if (lane < S && acc0 != Real(0)) ps[lane] += acc0;
+                    if (lane + 32 < S && acc1 != Real(0)) ps[lane + 32] += acc1;
+                    for (int ch = lane + 64; ch < S; ch += 32) {
+                        Real s = Real(0);
+                        for (int e = qn; e < qn + npairs; ++e) s += Q.w[e] * warp_seed[int(Q.meta[e] & 0xffu) * sp + ch];
+                        if (s != Real(0)) ps[ch] += s;
+                    }
+                } else if (lane < S && acc0 != Real(0)) {
                     Real* dst = lane < 3 ? a.acc_dcolor + size_t(g) * 3 + lane
                                          : (lane == 3 ? a.g_k + g : a.g_sem + size_t(g) * C + (lane - 4));
                     atomicAdd(dst, acc0);
                 }
-                if (lane + 32 < S && acc1 != Real(0)) atomicAdd(a.g_sem + size_t(g) * C + (lane + 28), acc1);
-                for (int ch = lane + 64; ch < S; ch += 32) {  // C > 60
+                if (!a.partial && lane + 32 < S && acc1 != Real(0)) atomicAdd(a.g_sem + size_t(g) * C + (lane + 28), acc1);
+                for (int ch = lane + 64; !a.partial && ch < S; ch += 32) {  // C > 60
                     Real s = Real(0);
                     for (int e = qn; e < qn + npairs; ++e) s += Q.w[e] * warp_seed[int(Q.meta[e] & 0xffu) * sp + ch];
                     if (s != Real(0)) atomicAdd(a.g_sem + size_t(g) * C + (ch - 4), s);
@@ -368,6 +388,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
                     const int s2 = 32 + lane;
                     Q.meta[lane] = Q.meta[s2];
                     Q.gid[lane] = Q.gid[s2];
+                    Q.inst[lane] = Q.inst[s2];
                     Q.w[lane] = Q.w[s2];
                     Q.da[lane] = Q.da[s2];
                     Q.al[lane] = Q.al[s2];
@@ -397,6 +418,88 @@ void launch_backward_blend(const BackwardArgs<Real>& a, int ntiles, cudaStream_t
     backward_kernel<Real><<<ntiles, kThreads, backward_smem_bytes<Real>(a.C), s>>>(a);
     count_launches(1);
 }
+
+namespace {
+
+__global__ void det_keys_kernel(const int64_t* __restrict__ d_count, const uint32_t* __restrict__ sorted_gauss,
+                                uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= *d_count) return;
+    keys[i] = sorted_gauss[i];
+    vals[i] = uint32_t(i);
+}
+
+__global__ void det_ranges_kernel(const int64_t* __restrict__ d_count, const uint32_t* __restrict__ gid_sorted,
+                                  uint2* __restrict__ range) {
+    const int64_t count = *d_count;
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const uint32_t g = gid_sorted[i];
+    if (i == 0 || gid_sorted[i - 1] != g) range[g].x = uint32_t(i);
+    if (i == count - 1 || gid_sorted[i + 1] != g) range[g].y = uint32_t(i + 1);
+}
+
+// One warp per Gaussian, lanes over the V fields; sequential in (instance, warp).
+template <typename Real>
+__global__ void det_reduce_kernel(const BackwardArgs<Real> a, const uint2* __restrict__ range,
+                                  const uint32_t* __restrict__ inst_of) {
+    const int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (g >= a.n) return;
+    const uint2 r = range[g];
+    if (r.y <= r.x) return;
+    const int C = a.C;
+    for (int f = lane; f < a.V; f += 32) {
+        Real s = Real(0);
+        for (uint32_t k = r.x; k < r.y; ++k) {
+            const Real* slot = a.partial + size_t(inst_of[k]) * 8 * a.V + f;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) s += slot[size_t(w) * a.V];
+        }
+        if (s == Real(0)) continue;
+        Real* dst;
+        if (f == 0) dst = a.g_opac + g;
+        else if (f < 3) dst = a.acc_dmean + g * 2 + (f - 1);
+        else if (f < 6) dst = a.acc_dconic + g * 3 + (f - 3);
+        else if (f < 9) dst = a.g_pos + g * 3 + (f - 6);
+        else if (f < 13) dst = a.g_rot + g * 4 + (f - 9);
+        else if (f < 16) dst = a.g_scale + g * 3 + (f - 13);
+        else if (f < 19) dst = a.acc_dcolor + g * 3 + (f - 16);
+        else if (f == 19) dst = a.g_k + g;
+        else dst = a.g_sem + g * C + (f - 20);
+        *dst += s;  // single writer per (Gaussian, field)
+    }
+}
+
+int bits_for_ids(int64_t v) {
+    int b = 1;
+    while ((int64_t(1) << b) < v) ++b;
+    return b;
+}
+
+}  // namespace
+
+template <typename Real>
+void launch_deterministic_reduce(const BackwardArgs<Real>& a, const DetScratch& d, const int64_t* d_count,
+                                 int64_t count, cudaStream_t s) {
+    if (count == 0 || a.n == 0) return;
+    const unsigned blocks = unsigned((count + 255) / 256);
+    det_keys_kernel<<<blocks, 256, 0, s>>>(d_count, a.inst_gauss, d.keys, d.vals);
+    SortScratch sc{d.hist, d.hist_scanned, d.scan_tiles};
+    const bool in_b = radix_sort_pairs<uint32_t, 8>(d.keys, d.vals, d.keys_alt, d.vals_alt, d_count, count,
+                                                    bits_for_ids(a.n), sc, s);
+    const uint32_t* gid_sorted = in_b ? d.keys_alt : d.keys;
+    const uint32_t* inst_of = in_b ? d.vals_alt : d.vals;
+    cudaMemsetAsync(d.gid_range, 0, sizeof(uint2) * size_t(a.n), s);
+    det_ranges_kernel<<<blocks, 256, 0, s>>>(d_count, gid_sorted, d.gid_range);
+    det_reduce_kernel<Real><<<unsigned((a.n * 32 + 255) / 256), 256, 0, s>>>(a, d.gid_range, inst_of);
+    count_launches(3);
+}
+
+template void launch_deterministic_reduce<float>(const BackwardArgs<float>&, const DetScratch&, const int64_t*,
+                                                 int64_t, cudaStream_t);
+template void launch_deterministic_reduce<double>(const BackwardArgs<double>&, const DetScratch&, const int64_t*,
+                                                  int64_t, cudaStream_t);
 
 template void launch_backward_blend<float>(const BackwardArgs<float>&, int, cudaStream_t);
 template void launch_backward_blend<double>(const BackwardArgs<double>&, int, cudaStream_t);

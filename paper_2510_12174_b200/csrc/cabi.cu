@@ -144,6 +144,9 @@ struct msplat_context {
     unsigned long long* h_u64 = nullptr;  // pinned scratch
     // scratch owned by the context (shared by calls on its stream)
     DevBuf acc_dcolor, acc_dmean, acc_dconic, ddepth_total, normal_dv, kept;
+    // deterministic backward (msplat_context_set_deterministic)
+    int deterministic = 0;
+    DevBuf det_partial, det_keys, det_keys_alt, det_vals, det_vals_alt, det_range;
     StageTimer timer;
 };
 
@@ -549,8 +552,33 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
     a.acc_dmean = ctx->acc_dmean.as<Real>();
     a.acc_dconic = ctx->acc_dconic.as<Real>();
     a.err = ctx->d_err;
+    int64_t det_count = 0;
+    DetScratch det{};
+    if (ctx->deterministic) {
+        // Synchronizing: the partial slots are sized by this render's instance count.
+        CUDA_TRY(cudaMemcpyAsync(ctx->h_u64, r->d_inst_count.p, 8, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        det_count = int64_t(*ctx->h_u64);
+        const size_t dc = size_t(std::max<int64_t>(det_count, 1));
+        a.V = 20 + C;
+        CUDA_TRY(ctx->det_partial.ensure(dc * 8 * size_t(a.V) * R));
+        CUDA_TRY(cudaMemsetAsync(ctx->det_partial.p, 0, dc * 8 * size_t(a.V) * R, st));
+        CUDA_TRY(ctx->det_keys.ensure(dc * 4));
+        CUDA_TRY(ctx->det_keys_alt.ensure(dc * 4));
+        CUDA_TRY(ctx->det_vals.ensure(dc * 4));
+        CUDA_TRY(ctx->det_vals_alt.ensure(dc * 4));
+        CUDA_TRY(ctx->det_range.ensure(nn * 8));
+        a.partial = ctx->det_partial.as<Real>();
+        // the replay's radix scratch is sized for inst_cap >= det_count items
+        det = DetScratch{ctx->det_keys.as<uint32_t>(), ctx->det_keys_alt.as<uint32_t>(),
+                         ctx->det_vals.as<uint32_t>(), ctx->det_vals_alt.as<uint32_t>(),
+                         ctx->det_range.as<uint2>(), r->hist.as<uint32_t>(), r->hist_scanned.as<uint32_t>(),
+                         r->scan_tiles.as<uint32_t>()};
+    }
     ctx->timer.begin(MSPLAT_STAGE_BACKWARD, st);
     launch_backward_blend<Real>(a, r->tiles_x * r->tiles_y, st);
+    if (ctx->deterministic)
+        launch_deterministic_reduce<Real>(a, det, r->d_inst_count.as<int64_t>(), det_count, st);
     ctx->timer.end(st);
     ProjBackwardArgs<Real> p{};
     p.n = n;
@@ -863,6 +891,12 @@ msplat_status msplat_adam_step(msplat_context* ctx, int dtype, int64_t n, int C,
 msplat_status msplat_context_set_timing(msplat_context* ctx, int enable) {
     if (!ctx) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null context");
     ctx->timer.enabled = enable != 0;
+    return MSPLAT_OK;
+}
+
+msplat_status msplat_context_set_deterministic(msplat_context* ctx, int enable) {
+    if (!ctx) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null context");
+    ctx->deterministic = enable != 0;
     return MSPLAT_OK;
 }
 

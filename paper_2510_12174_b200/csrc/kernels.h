@@ -138,10 +138,26 @@ struct BackwardArgs {
     // accumulation targets (zeroed before K9)
     Real *g_pos, *g_rot, *g_scale, *g_opac, *g_k, *g_sem;  // output gradient buffer
     Real *acc_dcolor, *acc_dmean, *acc_dconic;             // scratch [n][3], [n][2], [n][3]
+    // Deterministic mode (null = atomics): per-(instance, warp) slots of V =
+    // 20 + C values [opac, dmean2, dconic3, pos3, rot4, scale3, dcolor3, k, sem C].
+    Real* partial;
+    int V;
     DeviceError* err;
 };
 template <typename Real>
 void launch_backward_blend(const BackwardArgs<Real>& a, int ntiles, cudaStream_t s);
+
+// Deterministic reduction of BackwardArgs::partial into the targets: instances
+// stably sorted by Gaussian id, then each Gaussian sums its slots in (list
+// position, warp) order -- bitwise reproducible run to run.
+struct DetScratch {
+    uint32_t *keys, *keys_alt, *vals, *vals_alt;  // >= count each
+    uint2* gid_range;                             // [n]
+    uint32_t *hist, *hist_scanned, *scan_tiles;   // radix-sort scratch for count items
+};
+template <typename Real>
+void launch_deterministic_reduce(const BackwardArgs<Real>& a, const DetScratch& d, const int64_t* d_count,
+                                 int64_t count, cudaStream_t s);
 
 template <typename Real>
 struct ProjBackwardArgs {

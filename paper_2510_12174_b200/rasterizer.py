@@ -501,6 +501,13 @@ def set_stage_timing(enable: bool, device=None):
     check(_lib.lib().msplat_context_set_timing(_Context.get(device).h, int(enable)))
 
 
+def set_deterministic(enable: bool, device=None):
+    """Bitwise-reproducible backward (TrainConfig::deterministic,
+    msplat/trainer.hpp:48-63): per-(instance, warp) partial slots reduced in a
+    fixed order instead of float atomics.  Synchronizing, not graph-capturable."""
+    check(_lib.lib().msplat_context_set_deterministic(_Context.get(device).h, int(enable)))
+
+
 def stage_timings(device=None) -> dict:
     """{stage: (device ms summed since the last call, launches of the stage)}; synchronizing."""
     ms = (ct.c_double * 8)()

@@ -65,9 +65,12 @@ def test_dropin_fp64_matches_reference_test_results():
 def test_dropin_fp32_reference_tests():
     lines, summary = _run({"MSPLAT_PRECISION": "32"})
     fails = sorted(l for l in lines if l.startswith("[FAIL]"))
-    # The reference's tolerances are written for doubles; record which cases
-    # FP32 cannot meet (1e-10..1e-12 bounds) and require the rest.
+    # The reference's tolerances are written for doubles; these cases assert
+    # bounds below FP32 resolution (1e-9 .. 1e-14) and are allowed to fail; every
+    # other case must pass.
     allowed = set(REF_FAILS) | {
+        "[FAIL] backward trivial cases for k and semantics",                  # eps 1e-12 / 1e-9
+        "[FAIL] projected quaternion gradient is tangent to the unit sphere",  # |g.q| < 1e-14
         "[FAIL] two-contributor blend matches the closed form",
         "[FAIL] per-pixel blending weights sum to 1 - T_final",
         "[FAIL] gradient-factor map is linear in k",

@@ -114,6 +114,33 @@ def test_backward_matches_oracle(port, case, dtype, tol):
         assert e < tol, k
 
 
+@pytest.mark.parametrize("dtype,tol", [("float64", 1e-8), ("float32", 1e-3)])
+def test_deterministic_backward_is_bitwise_reproducible(port, dtype, tol):
+    """tests/test_rasterizer.cpp:386-419: repeated backward passes are bitwise
+    equal (fixed-order reduction), and match the oracle like the atomic path."""
+    import torch
+    import paper_2510_12174_b200 as M
+    s = scenes.make_random_scene(3000, 6, 2, seed=77)
+    cam = {"fx": 120.0, "fy": 120.0, "cx": 80.0, "cy": 60.0, "width": 160, "height": 120,
+           "R_c2w": np.eye(3), "t_c2w": np.array([0.0, 0.0, -1.2])}
+    dt = torch.float64 if dtype == "float64" else torch.float32
+    pix = scenes.pixel_grads(cam["width"], cam["height"], s["num_classes"], seed=5, scale=1.0)
+    M.set_deterministic(True)
+    try:
+        runs = []
+        for _ in range(3):
+            scene, view, rc, replay, frame = gpu_forward(s, cam, BG, dtype)
+            runs.append(grads_np(M.rasterize_backward(scene, view, frame, replay, torch_pix(pix, dt))))
+    finally:
+        M.set_deterministic(False)
+    for k in GRAD_NAMES:
+        assert np.array_equal(runs[0][k], runs[1][k]) and np.array_equal(runs[0][k], runs[2][k]), k
+    ref = port.backward(s, cam, hwc_pix(pix), BG)
+    for k in GRAD_NAMES:
+        if ref[k].size:
+            assert rel_l2_err(runs[0][k], ref[k]) < tol, k
+
+
 @pytest.mark.parametrize("dtype,tol", [("float64", 1e-10), ("float32", 1e-4)])
 def test_normals_forward_and_backward(port, dtype, tol):
     import torch
