@@ -11,7 +11,8 @@ import ctypes as ct
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmsplat_b200.so")
+# MSPLAT_LIB overrides the path (A/B timing of two in-tree builds).
+LIB_PATH = os.environ.get("MSPLAT_LIB") or os.path.join(HERE, "libmsplat_b200.so")
 
 MSPLAT_OK = 0
 MSPLAT_ERR_INVALID_ARGUMENT = 1

@@ -96,14 +96,14 @@ __device__ __forceinline__ Real seg_sum(Real v, const bool* same) {
 
 // Phase B on the first n queue entries (n <= 32): per-pair geometric
 // gradients, segmented by Gaussian, one atomic per value per Gaussian.
-template <typename Real>
+template <typename Real, bool DET>
 __device__ __noinline__ void flush_pairs(const BackwardArgs<Real>& a, const PairQueue<Real>& q, const Real* dDw,
                                          int n, int bx, int by) {
     const int lane = threadIdx.x & 31;
     const bool act = lane < n;
     const uint32_t meta = act ? q.meta[lane] : 0u;
     const uint32_t g = act ? q.gid[lane] : 0xffffffffu - lane;  // padding lanes: unique keys
-    const uint32_t inst = act ? q.inst[lane] : 0u;
+    const uint32_t inst = DET && act ? q.inst[lane] : 0u;
     bool same[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
@@ -205,12 +205,12 @@ __device__ __noinline__ void flush_pairs(const BackwardArgs<Real>& a, const Pair
     }
     // Deterministic mode: this (instance, warp) owns a private slot; plain
     // read-modify-write in program order, reduced later in a fixed order.
-    Real* const slot = a.partial ? a.partial + (size_t(inst) * 8 + (threadIdx.x >> 5)) * a.V : nullptr;
+    Real* const slot = DET ? a.partial + (size_t(inst) * 8 + (threadIdx.x >> 5)) * a.V : nullptr;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
         const Real s = seg_sum<Real>(v[i], same);
         if (head && s != Real(0)) {
-            if (slot) {
+            if constexpr (DET) {
                 slot[i] += s;
                 continue;
             }
@@ -229,7 +229,7 @@ __device__ __noinline__ void flush_pairs(const BackwardArgs<Real>& a, const Pair
 
 }  // namespace
 
-template <typename Real>
+template <typename Real, bool DET>
 __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArgs<Real> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int C = a.C, sp = seed_pitch(C), S = C + 4;
@@ -326,18 +326,21 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
             }
             __syncwarp();
             if (ae.pass) {
-                T = T / (Real(1) - ae.alpha);
+                // One reciprocal for the T restore and the background term (FP32);
+                // FP64 keeps the reference's divisions.
+                const Real inv = sizeof(Real) == 4 ? Real(1) / (Real(1) - ae.alpha) : Real(0);
+                T = sizeof(Real) == 4 ? T * inv : T / (Real(1) - ae.alpha);
                 const Real w = ae.alpha * T;
                 const Real FS = dot_rows<Real>(warp_F, my_seed, sp);
                 accA = last_alpha * lastFS + (Real(1) - last_alpha) * accA;
-                const Real dalpha = (FS - accA) * T - (T_final / (Real(1) - ae.alpha)) * bg_dot;
+                const Real dalpha = (FS - accA) * T - (sizeof(Real) == 4 ? T_final * inv : T_final / (Real(1) - ae.alpha)) * bg_dot;
                 lastFS = FS;
                 last_alpha = ae.alpha;
                 const int e = qn + __popc(mask & ((1u << lane) - 1u));
                 const AlphaRec<Real>& ar = ws->rec[slot];
                 Q.meta[e] = uint32_t(lane) | (ae.clamped ? (1u << 8) : 0u);
                 Q.gid[e] = g;
-                Q.inst[e] = list0 + uint32_t(c * 32 + slot);
+                if constexpr (DET) Q.inst[e] = list0 + uint32_t(c * 32 + slot);
                 Q.w[e] = w;
                 Q.da[e] = dalpha;
                 Q.al[e] = ae.alpha;
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
                     acc0 += we * seedL[c0];
                     acc1 += we * seedL[c1];
                 }
-                if (a.partial) {  // fields 16 + ch: dcolor, dk, dsem
+                if constexpr (DET) {  // fields 16 + ch: dcolor, dk, dsem
                     Real* const ps = a.partial + (size_t(list0 + c * 32 + slot) * 8 + warp) * a.V + 16;
                     if (lane < S && acc0 != Real(0)) ps[lane] += acc0;
                     if (lane + 32 < S && acc1 != Real(0)) ps[lane + 32] += acc1;
@@ -373,8 +376,8 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
                                          : (lane == 3 ? a.g_k + g : a.g_sem + size_t(g) * C + (lane - 4));
                     atomicAdd(dst, acc0);
                 }
-                if (!a.partial && lane + 32 < S && acc1 != Real(0)) atomicAdd(a.g_sem + size_t(g) * C + (lane + 28), acc1);
-                for (int ch = lane + 64; !a.partial && ch < S; ch += 32) {  // C > 60
+                if (!DET && lane + 32 < S && acc1 != Real(0)) atomicAdd(a.g_sem + size_t(g) * C + (lane + 28), acc1);
+                for (int ch = lane + 64; !DET && ch < S; ch += 32) {  // C > 60
                     Real s = Real(0);
                     for (int e = qn; e < qn + npairs; ++e) s += Q.w[e] * warp_seed[int(Q.meta[e] & 0xffu) * sp + ch];
                     if (s != Real(0)) atomicAdd(a.g_sem + size_t(g) * C + (ch - 4), s);
@@ -382,13 +385,13 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
                 qn += npairs;
             }
             if (qn >= 32) {
-                flush_pairs<Real>(a, Q, ws->dD, 32, bx, by);
+                flush_pairs<Real, DET>(a, Q, ws->dD, 32, bx, by);
                 const int rest = qn - 32;
                 if (lane < rest) {  // reads >= 32, writes < 32: no overlap
                     const int s2 = 32 + lane;
                     Q.meta[lane] = Q.meta[s2];
                     Q.gid[lane] = Q.gid[s2];
-                    Q.inst[lane] = Q.inst[s2];
+                    if constexpr (DET) Q.inst[lane] = Q.inst[s2];
                     Q.w[lane] = Q.w[s2];
                     Q.da[lane] = Q.da[s2];
                     Q.al[lane] = Q.al[s2];
@@ -404,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
             }
         }
     }
-    if (qn > 0) flush_pairs<Real>(a, Q, ws->dD, qn, bx, by);
+    if (qn > 0) flush_pairs<Real, DET>(a, Q, ws->dD, qn, bx, by);
 }
 
 template <typename Real>
@@ -412,10 +415,14 @@ void launch_backward_blend(const BackwardArgs<Real>& a, int ntiles, cudaStream_t
     if (ntiles == 0) return;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(backward_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(backward_kernel<Real, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(backward_kernel<Real, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         configured = true;
     }
-    backward_kernel<Real><<<ntiles, kThreads, backward_smem_bytes<Real>(a.C), s>>>(a);
+    if (a.partial)
+        backward_kernel<Real, true><<<ntiles, kThreads, backward_smem_bytes<Real>(a.C), s>>>(a);
+    else
+        backward_kernel<Real, false><<<ntiles, kThreads, backward_smem_bytes<Real>(a.C), s>>>(a);
     count_launches(1);
 }
 

@@ -51,13 +51,12 @@ for r in csv.reader(io.StringIO(src)):
         hdr = r
         ie, st = hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
         continue
-    if r[0] != "":
-        cur = (fname, r[0], r[1].strip()[:80])
-        continue
-    if cur and hdr and len(r) > ie and r[2].startswith("0x"):
+    if r[0] != "" and hdr and len(r) > ie and cur_f:
+        # line rows carry the per-line aggregates; the SASS rows below repeat them
         try:
-            funcs[cur_f][cur][0] += float(r[ie] or 0)
-            funcs[cur_f][cur][1] += float(r[st] or 0)
+            key = (fname, r[0], r[1].strip()[:80])
+            funcs[cur_f][key][0] += float(r[ie] if r[ie] not in ("-", "") else 0)
+            funcs[cur_f][key][1] += float(r[st] if r[st] not in ("-", "") else 0)
         except ValueError:
             pass
 lines = [f"# {title}", ""]
