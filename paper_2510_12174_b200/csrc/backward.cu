@@ -29,6 +29,12 @@ __global__ void __launch_bounds__(256) projection_backward_kernel(const ProjBack
     Real gr[4] = {a.g_rot[4 * i], a.g_rot[4 * i + 1], a.g_rot[4 * i + 2], a.g_rot[4 * i + 3]};
     Real gs[3] = {a.g_scale[3 * i], a.g_scale[3 * i + 1], a.g_scale[3 * i + 2]};
     Real go = a.g_opac[i];
+    // K9's per-pair sums (acc16 row): opacity, position, rotation, scale
+    const Real* A16 = a.acc16 + size_t(i) * 16;
+    go += A16[0];
+    for (int k = 0; k < 3; ++k) gp[k] += A16[6 + k];
+    for (int k = 0; k < 4; ++k) gr[k] += A16[9 + k];
+    for (int k = 0; k < 3; ++k) gs[k] += A16[13 + k];
 
     if (a.visible[i]) {
         Real R[9];
@@ -69,8 +75,7 @@ __global__ void __launch_bounds__(256) projection_backward_kernel(const ProjBack
         const Real det = cov[0] * cov[3] - cov[2] * cov[1];
         const Real con[4] = {cov[3] / det, -cov[1] / det, -cov[1] / det, cov[0] / det};
         // dcov2d = -conic Gc conic (rasterizer_backward.cpp:66-69)
-        const Real Gc[4] = {a.acc_dconic[3 * i], a.acc_dconic[3 * i + 1], a.acc_dconic[3 * i + 1],
-                            a.acc_dconic[3 * i + 2]};
+        const Real Gc[4] = {A16[3], A16[4], A16[4], A16[5]};
         Real t1[4], dcov[4];
         for (int r = 0; r < 2; ++r)
             for (int k = 0; k < 2; ++k) t1[r * 2 + k] = -(con[r * 2] * Gc[k] + con[r * 2 + 1] * Gc[2 + k]);
@@ -97,7 +102,7 @@ __global__ void __launch_bounds__(256) projection_backward_kernel(const ProjBack
         dp[0] = dJ[2] * (-fx / z2);
         dp[1] = dJ[5] * (-fy / z2);
         dp[2] = dJ[0] * (-fx / z2) + dJ[4] * (-fy / z2) + dJ[2] * (2 * fx * x / z3) + dJ[5] * (2 * fy * y / z3);
-        const Real dm0 = a.acc_dmean[2 * i], dm1 = a.acc_dmean[2 * i + 1];
+        const Real dm0 = A16[1], dm1 = A16[2];
         dp[0] += dm0 * fx / z;
         dp[1] += dm1 * fy / z;
         dp[2] += -dm0 * fx * x / z2 - dm1 * fy * y / z2;

@@ -42,12 +42,21 @@ __host__ __device__ inline int seed_pitch(int C) {
     return p;
 }
 
+// Blend weight + the pixel's seed-row offset, read together (one 64-bit LDS
+// for FP32) by the seed-linear loop.
+template <typename Real>
+struct __align__(2 * sizeof(Real)) WeightRow {
+    Real w;
+    uint32_t soff;
+};
+
 template <typename Real>
 struct PairQueue {
     uint32_t meta[kQueue];  // pixel lane | clamped << 8
     uint32_t gid[kQueue];
     uint32_t inst[kQueue];  // position in the tile-sorted list (deterministic mode)
-    Real w[kQueue], da[kQueue], al[kQueue], gs[kQueue];
+    WeightRow<Real> ws[kQueue];
+    Real da[kQueue], al[kQueue], gs[kQueue];
     Real cx[kQueue], cy[kQueue], ca[kQueue], cb[kQueue], cc[kQueue];
 };
 
@@ -69,13 +78,19 @@ template <typename Real>
 __device__ __forceinline__ Real dot_rows(const Real* a, const Real* b, int n) {
     Real s = Real(0);
     if constexpr (sizeof(Real) == 4) {
+        // four independent FMA chains (latency, not throughput, bound)
         const float4* a4 = reinterpret_cast<const float4*>(a);
         const float4* b4 = reinterpret_cast<const float4*>(b);
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll 4
         for (int i = 0; i < n / 4; ++i) {
             const float4 x = a4[i], y = b4[i];
-            s += x.x * y.x + x.y * y.y + x.z * y.z + x.w * y.w;
+            s0 = fmaf(x.x, y.x, s0);
+            s1 = fmaf(x.y, y.y, s1);
+            s2 = fmaf(x.z, y.z, s2);
+            s3 = fmaf(x.w, y.w, s3);
         }
+        s = (s0 + s1) + (s2 + s3);
     } else {
         for (int i = 0; i < n; ++i) s += a[i] * b[i];
     }
@@ -118,7 +133,7 @@ __device__ __noinline__ void flush_pairs(const BackwardArgs<Real>& a, const Pair
     if (act) {
         const int L = int(meta & 0xffu);
         const bool clamped = (meta >> 8) & 1u;
-        const Real w = q.w[lane], dalpha = q.da[lane], alpha = q.al[lane], gauss = q.gs[lane];
+        const Real w = q.ws[lane].w, dalpha = q.da[lane], alpha = q.al[lane], gauss = q.gs[lane];
         const int xL = bx + (L & 7), yL = by + (L >> 3);
         const Real dx = Real(xL) + Real(0.5) - q.cx[lane], dy = Real(yL) + Real(0.5) - q.cy[lane];
         if (!clamped) {  // rasterizer_backward.cpp:234-244
@@ -207,21 +222,27 @@ __device__ __noinline__ void flush_pairs(const BackwardArgs<Real>& a, const Pair
     // read-modify-write in program order, reduced later in a fixed order.
     Real* const slot = DET ? a.partial + (size_t(inst) * 8 + (threadIdx.x >> 5)) * a.V : nullptr;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        const Real s = seg_sum<Real>(v[i], same);
-        if (head && s != Real(0)) {
-            if constexpr (DET) {
-                slot[i] += s;
-                continue;
+    for (int i = 0; i < 16; ++i) v[i] = seg_sum<Real>(v[i], same);
+    if (head) {
+        if constexpr (DET) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                if (v[i] != Real(0)) slot[i] += v[i];
+        } else {
+            Real* const row = a.acc16 + size_t(g) * 16;
+            if constexpr (sizeof(Real) == 4) {
+                // four 16-byte vector reductions into the Gaussian's 64-byte row
+#pragma unroll
+                for (int i = 0; i < 16; i += 4)
+                    if (v[i] != 0.f || v[i + 1] != 0.f || v[i + 2] != 0.f || v[i + 3] != 0.f)
+                        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + i), "f"(v[i]),
+                                     "f"(v[i + 1]), "f"(v[i + 2]), "f"(v[i + 3])
+                                     : "memory");
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (v[i] != Real(0)) atomicAdd(row + i, v[i]);
             }
-            Real* dst;
-            if (i == 0) dst = a.g_opac + g;
-            else if (i < 3) dst = a.acc_dmean + size_t(g) * 2 + (i - 1);
-            else if (i < 6) dst = a.acc_dconic + size_t(g) * 3 + (i - 3);
-            else if (i < 9) dst = a.g_pos + size_t(g) * 3 + (i - 6);
-            else if (i < 13) dst = a.g_rot + size_t(g) * 4 + (i - 9);
-            else dst = a.g_scale + size_t(g) * 3 + (i - 13);
-            atomicAdd(dst, s);
         }
     }
     __syncwarp();
@@ -286,6 +307,11 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
     const uint32_t list0 = a.tile_range[tile].x;
     // Clamped channel indices keep every shared read inside a seed row (C may be 0).
     const int c0 = lane < sp ? lane : 0, c1 = lane + 32 < sp ? lane + 32 : 0;
+    // Destination of the F channel this lane accumulates (F = [rgb, k, sem]):
+    // base + gid * stride, hoisted out of the event loop.
+    Real* const dst0 = lane < 3 ? a.acc_dcolor + lane : (lane == 3 ? a.g_k : a.g_sem + (lane - 4));
+    const int stride0 = lane < 3 ? 3 : (lane == 3 ? 1 : C);
+    Real* const dst1 = a.g_sem + (lane + 28);  // channel lane + 32
     int qn = 0;
 
     for (int c = (wmax - 1) >> 5; c >= 0; --c) {
@@ -322,7 +348,9 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
             }
             {
                 const Real* semg = a.semantics + size_t(g) * C;
-                for (int ch = lane; ch < C; ch += 32) warp_F[4 + ch] = semg[ch];
+                if (lane < C) warp_F[4 + lane] = semg[lane];
+                if (lane + 32 < C) warp_F[36 + lane] = semg[lane + 32];
+                for (int ch = lane + 64; ch < C; ch += 32) warp_F[4 + ch] = semg[ch];  // C > 64
             }
             __syncwarp();
             if (ae.pass) {
@@ -341,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
                 Q.meta[e] = uint32_t(lane) | (ae.clamped ? (1u << 8) : 0u);
                 Q.gid[e] = g;
                 if constexpr (DET) Q.inst[e] = list0 + uint32_t(c * 32 + slot);
-                Q.w[e] = w;
+                Q.ws[e] = WeightRow<Real>{w, uint32_t(lane * sp)};
                 Q.da[e] = dalpha;
                 Q.al[e] = ae.alpha;
                 Q.gs[e] = ae.gauss;
@@ -356,11 +384,11 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
             {
                 const int npairs = __popc(mask);
                 Real acc0 = Real(0), acc1 = Real(0);
+#pragma unroll 2
                 for (int e = qn; e < qn + npairs; ++e) {
-                    const Real we = Q.w[e];
-                    const Real* seedL = warp_seed + int(Q.meta[e] & 0xffu) * sp;
-                    acc0 += we * seedL[c0];
-                    acc1 += we * seedL[c1];
+                    const WeightRow<Real> wr = Q.ws[e];
+                    acc0 += wr.w * warp_seed[wr.soff + c0];
+                    acc1 += wr.w * warp_seed[wr.soff + c1];
                 }
                 if constexpr (DET) {  // fields 16 + ch: dcolor, dk, dsem
                     Real* const ps = a.partial + (size_t(list0 + c * 32 + slot) * 8 + warp) * a.V + 16;
@@ -368,18 +396,16 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
                     if (lane + 32 < S && acc1 != Real(0)) ps[lane + 32] += acc1;
                     for (int ch = lane + 64; ch < S; ch += 32) {
                         Real s = Real(0);
-                        for (int e = qn; e < qn + npairs; ++e) s += Q.w[e] * warp_seed[int(Q.meta[e] & 0xffu) * sp + ch];
+                        for (int e = qn; e < qn + npairs; ++e) s += Q.ws[e].w * warp_seed[Q.ws[e].soff + ch];
                         if (s != Real(0)) ps[ch] += s;
                     }
                 } else if (lane < S && acc0 != Real(0)) {
-                    Real* dst = lane < 3 ? a.acc_dcolor + size_t(g) * 3 + lane
-                                         : (lane == 3 ? a.g_k + g : a.g_sem + size_t(g) * C + (lane - 4));
-                    atomicAdd(dst, acc0);
+                    atomicAdd(dst0 + size_t(g) * stride0, acc0);
                 }
-                if (!DET && lane + 32 < S && acc1 != Real(0)) atomicAdd(a.g_sem + size_t(g) * C + (lane + 28), acc1);
+                if (!DET && lane + 32 < S && acc1 != Real(0)) atomicAdd(dst1 + size_t(g) * C, acc1);
                 for (int ch = lane + 64; !DET && ch < S; ch += 32) {  // C > 60
                     Real s = Real(0);
-                    for (int e = qn; e < qn + npairs; ++e) s += Q.w[e] * warp_seed[int(Q.meta[e] & 0xffu) * sp + ch];
+                    for (int e = qn; e < qn + npairs; ++e) s += Q.ws[e].w * warp_seed[Q.ws[e].soff + ch];
                     if (s != Real(0)) atomicAdd(a.g_sem + size_t(g) * C + (ch - 4), s);
                 }
                 qn += npairs;
@@ -392,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArg
                     Q.meta[lane] = Q.meta[s2];
                     Q.gid[lane] = Q.gid[s2];
                     if constexpr (DET) Q.inst[lane] = Q.inst[s2];
-                    Q.w[lane] = Q.w[s2];
+                    Q.ws[lane] = Q.ws[s2];
                     Q.da[lane] = Q.da[s2];
                     Q.al[lane] = Q.al[s2];
                     Q.gs[lane] = Q.gs[s2];
@@ -465,12 +491,7 @@ __global__ void det_reduce_kernel(const BackwardArgs<Real> a, const uint2* __res
         }
         if (s == Real(0)) continue;
         Real* dst;
-        if (f == 0) dst = a.g_opac + g;
-        else if (f < 3) dst = a.acc_dmean + g * 2 + (f - 1);
-        else if (f < 6) dst = a.acc_dconic + g * 3 + (f - 3);
-        else if (f < 9) dst = a.g_pos + g * 3 + (f - 6);
-        else if (f < 13) dst = a.g_rot + g * 4 + (f - 9);
-        else if (f < 16) dst = a.g_scale + g * 3 + (f - 13);
+        if (f < 16) dst = a.acc16 + g * 16 + f;
         else if (f < 19) dst = a.acc_dcolor + g * 3 + (f - 16);
         else if (f == 19) dst = a.g_k + g;
         else dst = a.g_sem + g * C + (f - 20);

@@ -143,7 +143,7 @@ struct msplat_context {
     DeviceError* h_err = nullptr;  // pinned
     unsigned long long* h_u64 = nullptr;  // pinned scratch
     // scratch owned by the context (shared by calls on its stream)
-    DevBuf acc_dcolor, acc_dmean, acc_dconic, ddepth_total, normal_dv, kept;
+    DevBuf acc_dcolor, acc16, ddepth_total, normal_dv, kept;
     // deterministic backward (msplat_context_set_deterministic)
     int deterministic = 0;
     DevBuf det_partial, det_keys, det_keys_alt, det_vals, det_vals_alt, det_range;
@@ -504,12 +504,10 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
     const int C = s->num_classes, K = int(sh_coeffs(s->sh_degree));
     const size_t nn = size_t(std::max<int64_t>(n, 1));
     CUDA_TRY(ctx->acc_dcolor.ensure(nn * 3 * R));
-    CUDA_TRY(ctx->acc_dmean.ensure(nn * 2 * R));
-    CUDA_TRY(ctx->acc_dconic.ensure(nn * 3 * R));
+    CUDA_TRY(ctx->acc16.ensure(nn * 16 * R));
     cudaStream_t st = ctx->stream;
     CUDA_TRY(cudaMemsetAsync(ctx->acc_dcolor.p, 0, nn * 3 * R, st));
-    CUDA_TRY(cudaMemsetAsync(ctx->acc_dmean.p, 0, nn * 2 * R, st));
-    CUDA_TRY(cudaMemsetAsync(ctx->acc_dconic.p, 0, nn * 3 * R, st));
+    CUDA_TRY(cudaMemsetAsync(ctx->acc16.p, 0, nn * 16 * R, st));
     if (!accumulate && n > 0) {
         CUDA_TRY(cudaMemsetAsync(g->dposition, 0, size_t(n) * 3 * R, st));
         CUDA_TRY(cudaMemsetAsync(g->drotation, 0, size_t(n) * 4 * R, st));
@@ -549,8 +547,7 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
     a.g_k = static_cast<Real*>(g->dk);
     a.g_sem = static_cast<Real*>(g->dsemantics);
     a.acc_dcolor = ctx->acc_dcolor.as<Real>();
-    a.acc_dmean = ctx->acc_dmean.as<Real>();
-    a.acc_dconic = ctx->acc_dconic.as<Real>();
+    a.acc16 = ctx->acc16.as<Real>();
     a.err = ctx->d_err;
     int64_t det_count = 0;
     DetScratch det{};
@@ -594,8 +591,7 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
     p.visible = r->visible.as<uint8_t>();
     p.clamped_bits = r->clamped.as<uint8_t>();
     p.acc_dcolor = a.acc_dcolor;
-    p.acc_dmean = a.acc_dmean;
-    p.acc_dconic = a.acc_dconic;
+    p.acc16 = a.acc16;
     p.g_pos = a.g_pos;
     p.g_rot = a.g_rot;
     p.g_scale = a.g_scale;
@@ -649,7 +645,7 @@ msplat_status msplat_context_create(int device, void* cuda_stream, msplat_contex
 void msplat_context_destroy(msplat_context* ctx) {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->stream);
-    for (DevBuf* b : {&ctx->acc_dcolor, &ctx->acc_dmean, &ctx->acc_dconic, &ctx->ddepth_total, &ctx->normal_dv,
+    for (DevBuf* b : {&ctx->acc_dcolor, &ctx->acc16, &ctx->ddepth_total, &ctx->normal_dv,
                       &ctx->kept})
         b->release();
     cudaFree(ctx->d_err);

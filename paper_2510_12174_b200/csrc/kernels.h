@@ -137,7 +137,11 @@ struct BackwardArgs {
     const Real *dcolor, *ddepth, *dsem, *dkmap;  // planar pixel grads
     // accumulation targets (zeroed before K9)
     Real *g_pos, *g_rot, *g_scale, *g_opac, *g_k, *g_sem;  // output gradient buffer
-    Real *acc_dcolor, *acc_dmean, *acc_dconic;             // scratch [n][3], [n][2], [n][3]
+    Real* acc_dcolor;  // scratch [n][3]
+    // scratch [n][16]: the per-pair geometric sums of K9 in one 64-byte row,
+    // [opacity, dmean2, dconic3, dposition3, drotation4, dscale3]; K10 folds
+    // it into the gradient buffer.
+    Real* acc16;
     // Deterministic mode (null = atomics): per-(instance, warp) slots of V =
     // 20 + C values [opac, dmean2, dconic3, pos3, rot4, scale3, dcolor3, k, sem C].
     Real* partial;
@@ -167,7 +171,7 @@ struct ProjBackwardArgs {
     const Real *means, *quats, *log_scales, *opacity_logits, *sh;
     const uint8_t* visible;
     const uint8_t* clamped_bits;
-    const Real *acc_dcolor, *acc_dmean, *acc_dconic;
+    const Real *acc_dcolor, *acc16;
     Real *g_pos, *g_rot, *g_scale, *g_opac, *g_sh, *g_k, *g_sem;
     int chain;  // fuse chain_activations (scene.cpp:108-129); only for single-view buffers
     DeviceError* err;
