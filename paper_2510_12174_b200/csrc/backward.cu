@@ -10,7 +10,7 @@ namespace msplat_cuda {
 
 // ------------------------------------------------------------------ K10
 template <typename Real>
-__global__ void __launch_bounds__(256) projection_backward_kernel(const ProjBackwardArgs<Real> a) {
+__global__ void __launch_bounds__(256) projection_backward_kernel(const __grid_constant__ ProjBackwardArgs<Real> a) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= a.n) return;
     const Cam& c = a.cam;

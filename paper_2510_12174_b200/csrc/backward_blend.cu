@@ -251,7 +251,7 @@ __device__ __noinline__ void flush_pairs(const BackwardArgs<Real>& a, const Pair
 }  // namespace
 
 template <typename Real, bool DET>
-__global__ void __launch_bounds__(kThreads, 2) backward_kernel(const BackwardArgs<Real> a) {
+__global__ void __launch_bounds__(kThreads, 2) backward_kernel(const __grid_constant__ BackwardArgs<Real> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int C = a.C, sp = seed_pitch(C), S = C + 4;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -474,7 +474,7 @@ __global__ void det_ranges_kernel(const int64_t* __restrict__ d_count, const uin
 
 // One warp per Gaussian, lanes over the V fields; sequential in (instance, warp).
 template <typename Real>
-__global__ void det_reduce_kernel(const BackwardArgs<Real> a, const uint2* __restrict__ range,
+__global__ void det_reduce_kernel(const __grid_constant__ BackwardArgs<Real> a, const uint2* __restrict__ range,
                                   const uint32_t* __restrict__ inst_of) {
     const int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;

@@ -75,7 +75,7 @@ __device__ __noinline__ void flush_depth(const ForwardArgs<Real>& a, FwdWarpSmem
 }  // namespace
 
 template <typename Real>
-__global__ void __launch_bounds__(kThreads, 2) forward_kernel(const ForwardArgs<Real> a) {
+__global__ void __launch_bounds__(kThreads, 2) forward_kernel(const __grid_constant__ ForwardArgs<Real> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int C = a.C, pitch = sem_pitch(C);

@@ -93,7 +93,7 @@ __device__ bool centre_state(const NormalCtx<Real>& nc, int x, int y, Stencil<Re
 }
 
 template <typename Real>
-__global__ void normals_forward_kernel(const NormalArgs<Real> a) {
+__global__ void normals_forward_kernel(const __grid_constant__ NormalArgs<Real> a) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
     if (x >= a.W || y >= a.H) return;
     const NormalCtx<Real> nc{&a};
@@ -112,7 +112,7 @@ __global__ void normals_forward_kernel(const NormalArgs<Real> a) {
 }
 
 template <typename Real>
-__global__ void normals_adjoint_kernel(const NormalArgs<Real> a) {
+__global__ void normals_adjoint_kernel(const __grid_constant__ NormalArgs<Real> a) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
     if (x >= a.W || y >= a.H) return;
     const size_t HW = size_t(a.W) * a.H, p = size_t(y) * a.W + x;
@@ -146,7 +146,7 @@ __global__ void normals_adjoint_kernel(const NormalArgs<Real> a) {
 }
 
 template <typename Real>
-__global__ void normals_gather_kernel(const NormalArgs<Real> a) {
+__global__ void normals_gather_kernel(const __grid_constant__ NormalArgs<Real> a) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
     if (x >= a.W || y >= a.H) return;
     const size_t HW = size_t(a.W) * a.H;

@@ -86,7 +86,7 @@ __device__ __forceinline__ bool finite_params(const PreprocessArgs<Real>& a, int
 }  // namespace
 
 template <typename Real>
-__global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs<Real> a) {
+__global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__ PreprocessArgs<Real> a) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= a.n) return;
     const Cam& c = a.cam;
