@@ -112,7 +112,7 @@ __device__ __forceinline__ Real seg_sum(Real v, const bool* same) {
 // Phase B on the first n queue entries (n <= 32): per-pair geometric
 // gradients, segmented by Gaussian, one atomic per value per Gaussian.
 template <typename Real, bool DET>
-__device__ __noinline__ void flush_pairs(const BackwardArgs<Real>& a, const PairQueue<Real>& q, const Real* dDw,
+__device__ __forceinline__ void flush_pairs(const BackwardArgs<Real>& a, const PairQueue<Real>& q, const Real* dDw,
                                          int n, int bx, int by) {
     const int lane = threadIdx.x & 31;
     const bool act = lane < n;

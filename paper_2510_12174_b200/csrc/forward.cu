@@ -48,7 +48,7 @@ size_t forward_smem_bytes(int C) {
 // Phase B on the first n queue entries (n <= 32).  `own` has bit e set when
 // queue entry e belongs to this lane's pixel.
 template <typename Real>
-__device__ __noinline__ void flush_depth(const ForwardArgs<Real>& a, FwdWarpSmem<Real>* ws, int n, int bx, int by,
+__device__ __forceinline__ void flush_depth(const ForwardArgs<Real>& a, FwdWarpSmem<Real>* ws, int n, int bx, int by,
                                          Real& dep, unsigned own) {
     const int lane = threadIdx.x & 31;
     if (lane < n) {

@@ -1,5 +1,5 @@
-"""Per-source-line stall breakdown of an ncu report (--import-source on).
-Usage: python tools/ncu_lines.py <rep> [top]"""
+"""Per-source-line stall breakdown of an ncu report (--import-source on), per kernel.
+Usage: python tools/ncu_lines.py <rep> [top] [kernel-substring]"""
 import csv
 import io
 import subprocess
@@ -7,27 +7,26 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+want = sys.argv[3] if len(sys.argv) > 3 else ""
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 hdr = None
-fname = ""
-rows = []
+fname = func = ""
+per = {}
 for r in csv.reader(io.StringIO(src)):
     if not r:
         continue
     if r[0] == "File Path":
         fname = r[1].split("/")[-1]
         continue
+    if r[0] == "Function Name":
+        func = r[1].split("(")[0]
+        continue
     if r[0] == "Line No":
         hdr = r
         continue
-    if hdr and r[0] not in ("", "Function Name"):
-        rows.append((fname, r))
-reasons = ["stall_long_sb", "stall_short_sb", "stall_lg", "stall_mio", "stall_wait", "stall_math", "stall_branch_resolving",
-           "stall_selected", "stall_not_selected", "stall_membar", "stall_drain", "stall_no_inst", "stall_dispatch"]
-idx = {k: hdr.index(k) for k in reasons}
-tot_i = hdr.index("Warp Stall Sampling (All Samples)")
-ins_i = hdr.index("Instructions Executed")
+    if hdr and r[0] != "":
+        per.setdefault(func, []).append((fname, r))
 
 
 def f(x):
@@ -37,12 +36,18 @@ def f(x):
         return 0.0
 
 
-T = sum(f(r[tot_i]) for _, r in rows) or 1
-agg = {}
-for k in reasons:
-    agg[k] = sum(f(r[idx[k]]) for _, r in rows) / T * 100
-print("overall:", ", ".join(f"{k[6:]} {v:.1f}%" for k, v in sorted(agg.items(), key=lambda kv: -kv[1]) if v > 0.5))
-for fn, r in sorted(rows, key=lambda x: -f(x[1][tot_i]))[:top]:
-    parts = sorted(((f(r[idx[k]]), k[6:]) for k in reasons), reverse=True)[:3]
-    print(f"{f(r[tot_i]) / T * 100:5.1f}% {fn}:{r[0]:>4} inst={int(f(r[ins_i])):>10} "
-          + " ".join(f"{n}={v / max(f(r[tot_i]), 1) * 100:.0f}%" for v, n in parts if v > 0) + f" | {r[1].strip()[:70]}")
+reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
+idx = {k: hdr.index(k) for k in reasons}
+tot_i = hdr.index("Warp Stall Sampling (All Samples)")
+ins_i = hdr.index("Instructions Executed")
+for func, rows in per.items():
+    if want not in func:
+        continue
+    T = sum(f(r[tot_i]) for _, r in rows) or 1
+    agg = {k: sum(f(r[idx[k]]) for _, r in rows) / T * 100 for k in reasons}
+    print(f"== {func}  (samples {int(T)})")
+    print("overall:", ", ".join(f"{k[6:]} {v:.1f}%" for k, v in sorted(agg.items(), key=lambda kv: -kv[1]) if v > 0.5))
+    for fn, r in sorted(rows, key=lambda x: -f(x[1][tot_i]))[:top]:
+        parts = sorted(((f(r[idx[k]]), k[6:]) for k in reasons), reverse=True)[:3]
+        print(f"{f(r[tot_i]) / T * 100:5.1f}% {fn}:{r[0]:>4} inst={int(f(r[ins_i])):>10} "
+              + " ".join(f"{n}={v / max(f(r[tot_i]), 1) * 100:.0f}%" for v, n in parts if v > 0) + f" | {r[1].strip()[:70]}")
