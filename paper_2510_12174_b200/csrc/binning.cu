@@ -41,32 +41,57 @@ __global__ void finalize_count_kernel(const uint32_t* __restrict__ total32, int6
     }
 }
 
-// One warp per depth-sorted Gaussian: lanes stride over its tile rect, so a
-// huge near-plane splat covering thousands of tiles does not serialise one
-// thread (2.9k such splats produced 94% of instances).
-__global__ void emit_instances_kernel(int64_t n, const uint32_t* __restrict__ order_sorted,
-                                      const uint2* __restrict__ tile_rect,
-                                      const uint32_t* __restrict__ count_sorted,
-                                      const uint32_t* __restrict__ offset_sorted, int tiles_x,
-                                      const int64_t* __restrict__ d_count,
-                                      uint32_t* __restrict__ inst_tile,
-                                      uint32_t* __restrict__ inst_gauss) {
-    const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+// One thread per depth-sorted Gaussian emits its (usually 1-4) instances; the
+// rare Gaussian covering more than 32 tiles (a near-plane splat: SURVEY.md
+// App. C saw 2.9k of them produce 94% of instances) is emitted by its whole
+// warp instead, so no thread serialises a huge rect.  Consecutive threads own
+// consecutive output ranges (the scan is in depth order): coalesced writes.
+__global__ void __launch_bounds__(256) emit_instances_kernel(int64_t n, const uint32_t* __restrict__ order_sorted,
+                                                             const uint2* __restrict__ tile_rect,
+                                                             const uint32_t* __restrict__ count_sorted,
+                                                             const uint32_t* __restrict__ offset_sorted, int tiles_x,
+                                                             const int64_t* __restrict__ d_count,
+                                                             uint32_t* __restrict__ inst_tile,
+                                                             uint32_t* __restrict__ inst_gauss) {
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    if (r >= n) return;
-    const uint32_t cnt = count_sorted[r];
-    if (cnt == 0) return;
-    if (*d_count == 0) return;  // overflow: nothing is emitted
-    const uint32_t g = order_sorted[r];
-    const uint2 rect = tile_rect[g];
-    const int tx0 = int(rect.x & 0xffffu), tx1 = int(rect.x >> 16);
-    const int ty0 = int(rect.y & 0xffffu);
-    const int w = tx1 - tx0 + 1;
-    const uint32_t off = offset_sorted[r];
-    for (uint32_t j = lane; j < cnt; j += 32) {
-        const int ty = ty0 + int(j) / w, tx = tx0 + int(j) % w;
-        inst_tile[off + j] = uint32_t(ty * tiles_x + tx);
-        inst_gauss[off + j] = g;
+    const bool overflow = *d_count == 0;  // nothing is emitted; the host grows the buffers
+    uint32_t cnt = 0, g = 0, off = 0;
+    uint2 rect = make_uint2(0, 0);
+    if (r < n && !overflow) {
+        cnt = count_sorted[r];
+        if (cnt) {
+            g = order_sorted[r];
+            rect = tile_rect[g];
+            off = offset_sorted[r];
+        }
+    }
+    const bool big = cnt > 32u;
+    if (cnt && !big) {
+        const int tx0 = int(rect.x & 0xffffu), tx1 = int(rect.x >> 16), ty0 = int(rect.y & 0xffffu);
+        int tx = tx0, ty = ty0;
+        for (uint32_t j = 0; j < cnt; ++j) {
+            inst_tile[off + j] = uint32_t(ty * tiles_x + tx);
+            inst_gauss[off + j] = g;
+            if (++tx > tx1) {
+                tx = tx0;
+                ++ty;
+            }
+        }
+    }
+    unsigned bigs = __ballot_sync(0xffffffffu, big);
+    while (bigs) {
+        const int src = __ffs(bigs) - 1;
+        bigs &= bigs - 1;
+        const uint32_t bc = __shfl_sync(0xffffffffu, cnt, src), bg = __shfl_sync(0xffffffffu, g, src);
+        const uint32_t bo = __shfl_sync(0xffffffffu, off, src);
+        const uint32_t rx = __shfl_sync(0xffffffffu, rect.x, src), ry = __shfl_sync(0xffffffffu, rect.y, src);
+        const int tx0 = int(rx & 0xffffu), tx1 = int(rx >> 16), ty0 = int(ry & 0xffffu);
+        const int w = tx1 - tx0 + 1;
+        for (uint32_t j = lane; j < bc; j += 32) {
+            inst_tile[bo + j] = uint32_t((ty0 + int(j) / w) * tiles_x + tx0 + int(j) % w);
+            inst_gauss[bo + j] = bg;
+        }
     }
 }
 
@@ -119,7 +144,7 @@ void run_binning(BinningBuffers& b, cudaStream_t s) {
     finalize_count_kernel<<<1, 1, 0, s>>>(b.d_inst_total32, b.inst_cap, b.d_inst_count, b.err);
     count_launches(1);
     if (n > 0)
-        emit_instances_kernel<<<unsigned((n * 32 + 255) / 256), 256, 0, s>>>(
+        emit_instances_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(
             n, order_sorted, b.tile_rect, b.count_sorted, b.offset_sorted, b.tiles_x,
             b.d_inst_count, b.inst_tile, b.inst_gauss);
         count_launches(1);

@@ -5,6 +5,9 @@
 //              learning rate is a function of the element's segment.
 //   prune mask (core/src/trainer.cpp:135-147): keep = !(|k-1| > T)
 //              (or !(|k-1| < T) with prune_keep_small).
+#include <algorithm>
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -18,20 +21,56 @@ struct AdamSegments {
 };
 
 template <typename Real>
-__global__ void adam_kernel(int64_t total, AdamSegments seg, Real* __restrict__ p, const Real* __restrict__ g,
-                            Real* __restrict__ m, Real* __restrict__ v, double bc1, double bc2) {
-    const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (e >= total) return;
+__device__ __forceinline__ Real adam_one(Real p, Real gr, Real& m, Real& v, Real lr, double bc1, double bc2) {
+    m = Real(0.9) * m + (Real(1) - Real(0.9)) * gr;
+    v = Real(0.999) * v + (Real(1) - Real(0.999)) * gr * gr;
+    if constexpr (sizeof(Real) == 8)  // the reference's operation order (trainer.cpp:120-127)
+        return p - lr * (m / bc1) / (sqrt(v / bc2) + 1e-15);
+    else  // FP32: reciprocals of the bias corrections, one IEEE divide
+        return p - lr * (m * float(1.0 / bc1)) / (sqrtf(v * float(1.0 / bc2)) + 1e-15f);
+}
+
+__device__ __forceinline__ int adam_segment(const AdamSegments& seg, int64_t e) {
     int s = 0;
 #pragma unroll
     for (int k = 1; k < 7; ++k) s += e >= seg.start[k];
-    const Real lr = Real(seg.lr[s]);
-    const Real gr = g[e];
-    const Real mm = Real(0.9) * m[e] + (Real(1) - Real(0.9)) * gr;
-    const Real vv = Real(0.999) * v[e] + (Real(1) - Real(0.999)) * gr * gr;
-    m[e] = mm;
-    v[e] = vv;
-    p[e] -= lr * (mm / Real(bc1)) / (sqrt(vv / Real(bc2)) + Real(1e-15));
+    return s;
+}
+
+// Grid-stride, 16-byte vectors (4 floats / 2 doubles per access): the update
+// is a pure stream over p, g, m, v (28 B per FP32 element).
+template <typename Real>
+__global__ void __launch_bounds__(256) adam_kernel(int64_t total, AdamSegments seg, Real* __restrict__ p,
+                                                   const Real* __restrict__ g, Real* __restrict__ m,
+                                                   Real* __restrict__ v, double bc1, double bc2, bool aligned) {
+    constexpr int VEC = 16 / sizeof(Real);
+    using V = typename std::conditional<sizeof(Real) == 4, float4, double2>::type;
+    const int64_t nvec = aligned ? total / VEC : 0;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec; i += stride) {
+        V pv = reinterpret_cast<const V*>(p)[i];
+        const V gv = reinterpret_cast<const V*>(g)[i];
+        V mv = reinterpret_cast<const V*>(m)[i];
+        V vv = reinterpret_cast<const V*>(v)[i];
+        Real* pp = reinterpret_cast<Real*>(&pv);
+        const Real* gg = reinterpret_cast<const Real*>(&gv);
+        Real* mm = reinterpret_cast<Real*>(&mv);
+        Real* ww = reinterpret_cast<Real*>(&vv);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+            const Real lr = Real(seg.lr[adam_segment(seg, i * VEC + j)]);
+            pp[j] = adam_one<Real>(pp[j], gg[j], mm[j], ww[j], lr, bc1, bc2);
+        }
+        reinterpret_cast<V*>(p)[i] = pv;
+        reinterpret_cast<V*>(m)[i] = mv;
+        reinterpret_cast<V*>(v)[i] = vv;
+    }
+    for (int64_t e = nvec * VEC + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+        Real mm = m[e], ww = v[e];
+        p[e] = adam_one<Real>(p[e], g[e], mm, ww, Real(seg.lr[adam_segment(seg, e)]), bc1, bc2);
+        m[e] = mm;
+        v[e] = ww;
+    }
 }
 
 template <typename Real>
@@ -58,7 +97,11 @@ void launch_adam(int64_t total, const int64_t* seg_starts, const double* lr, Rea
     AdamSegments seg;
     for (int i = 0; i < 8; ++i) seg.start[i] = seg_starts[i];
     for (int i = 0; i < 7; ++i) seg.lr[i] = lr[i];
-    adam_kernel<Real><<<unsigned((total + 255) / 256), 256, 0, s>>>(total, seg, params, grads, m, v, bc1, bc2);
+    const bool aligned = ((reinterpret_cast<uintptr_t>(params) | reinterpret_cast<uintptr_t>(grads) |
+                           reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 15u) == 0;
+    const int64_t work = aligned ? (total + 15) / 16 * 4 : total;
+    const unsigned blocks = unsigned(std::min<int64_t>((work + 255) / 256, 148 * 16));
+    adam_kernel<Real><<<blocks, 256, 0, s>>>(total, seg, params, grads, m, v, bc1, bc2, aligned);
     count_launches(1);
 }
 

@@ -295,6 +295,13 @@ def test_adam_and_prune_match_oracle(port):
     M.adam_step(scene, g, st, tc)
     for f in ("means", "quats", "log_scales", "opacity_logits", "sh", "semantics", "k"):
         assert np.allclose(getattr(scene, f).cpu().numpy(), p_ref[f], rtol=1e-13, atol=1e-15), f
+    # FP32: same step within single-precision rounding
+    scene32 = M.Scene.from_numpy(s, dtype=torch.float32)
+    g32 = M.GradientBuffer(*(torch.as_tensor(gd[k], device="cuda", dtype=torch.float32) for k in GRAD_NAMES),
+                           raw_space=True)
+    M.adam_step(scene32, g32, M.OptimizerState.init(scene32), tc)
+    for f in ("means", "quats", "log_scales", "opacity_logits", "sh", "semantics", "k"):
+        assert np.allclose(getattr(scene32, f).cpu().numpy(), p_ref[f], rtol=2e-6, atol=1e-6), f
     k = rng.uniform(0, 2, 5000)
     for keep_small in (False, True):
         sc = M.Scene.from_numpy(dict(scenes.make_random_scene(5000, 1, 0, seed=3), k=k), dtype=torch.float64)
