@@ -64,7 +64,7 @@ struct Vec3T {
 // Per-visible-Gaussian records written by K1 and gathered per tile by K6/K9.
 // Alpha-test record (everything a visited pair needs), 12 Reals.
 template <typename Real>
-struct AlphaRec {
+struct __align__(16) AlphaRec {  // 48 B (FP32): three 16-byte stores / loads
     Real cx, cy;      // splat centre (pixels)
     Real ca, cb, cc;  // conic (xx, xy, yy)
     Real opacity;     // activated alpha (logistic of the logit)
@@ -79,7 +79,7 @@ struct AlphaRec {
 // Blend record (everything a blended pair needs beyond the alpha test).
 // Rt is R^T of the activated rotation, row-major; inv_axes = 1/(sigma*s).
 template <typename Real>
-struct BlendRec {
+struct __align__(16) BlendRec {  // 128 B (FP32): eight 16-byte stores
     Real Rt[9];
     Real axes[3];     // sigma * s (double path divides like the reference)
     Real inv_axes[3]; // 1 / (sigma * s)

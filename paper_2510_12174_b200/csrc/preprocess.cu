@@ -18,6 +18,8 @@
 
 namespace msplat_cuda {
 
+constexpr int kPreThreads = 256;
+
 namespace {
 
 __device__ __forceinline__ double dot3(const double* a, const double* b) {
@@ -78,16 +80,38 @@ __device__ __forceinline__ bool finite_params(const PreprocessArgs<Real>& a, int
         ok &= isfinite(double(a.means[3 * i + j])) && isfinite(double(a.log_scales[3 * i + j]));
     for (int j = 0; j < 4; ++j) ok &= isfinite(double(a.quats[4 * i + j]));
     ok &= isfinite(double(a.opacity_logits[i])) && isfinite(double(a.k[i]));
-    for (int j = 0; j < 3 * a.K; ++j) ok &= isfinite(double(a.sh[i * 3 * a.K + j]));
-    for (int j = 0; j < a.C; ++j) ok &= isfinite(double(a.semantics[i * a.C + j]));
     return ok;
 }
 
 }  // namespace
 
 template <typename Real>
-__global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__ PreprocessArgs<Real> a) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kPreThreads) preprocess_kernel(const __grid_constant__ PreprocessArgs<Real> a) {
+    // The block's SH rows (3K values per Gaussian, contiguous) are staged in
+    // shared memory by one coalesced copy, and the semantic rows are scanned for
+    // non-finite values the same way; per-thread strided row reads would thrash
+    // L1.  Row pitch 3K is odd for K = 1, 9: conflict-free FP32 row reads.
+    extern __shared__ __align__(16) unsigned char pre_smem[];
+    Real* const sh_s = reinterpret_cast<Real*>(pre_smem);
+    uint8_t* const bad_s = reinterpret_cast<uint8_t*>(sh_s + size_t(kPreThreads) * 3 * a.K);
+    const int64_t base = int64_t(blockIdx.x) * kPreThreads;
+    const int cnt = int(a.n - base < kPreThreads ? a.n - base : kPreThreads);
+    {
+        const int rs = 3 * a.K;
+        bad_s[threadIdx.x] = 0;
+        __syncthreads();
+        const Real* src = a.sh + base * rs;
+        for (int e = threadIdx.x; e < cnt * rs; e += kPreThreads) {
+            const Real v = src[e];
+            sh_s[e] = v;
+            if (!isfinite(double(v))) bad_s[e / rs] = 1;
+        }
+        const Real* sem = a.semantics + base * a.C;
+        for (int e = threadIdx.x; e < cnt * a.C; e += kPreThreads)
+            if (!isfinite(double(sem[e]))) bad_s[e / a.C] = 1;
+        __syncthreads();
+    }
+    const int64_t i = base + threadIdx.x;
     if (i >= a.n) return;
     const Cam& c = a.cam;
 
@@ -96,7 +120,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__
     a.tile_count[i] = 0;
     a.visible[i] = 0;
 
-    if (!finite_params(a, i)) {  // Scene::validate / activate (scene.cpp:36-38, 43-45)
+    if (bad_s[threadIdx.x] || !finite_params(a, i)) {  // Scene::validate / activate (scene.cpp:36-38, 43-45)
         raise_error(a.err, kErrNonFiniteParam, 0, i);
         return;
     }
@@ -171,14 +195,20 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__
     cov[0] += kCovFloor;
     cov[3] += kCovFloor;
     const double det = cov[0] * cov[3] - cov[2] * cov[1];
-    if (det <= 0) return;
+    const bool proj_ok = det > 0;
+    {  // one atomic per warp for the visible count (a same-address atomic per
+       // Gaussian serialises in L2)
+        const unsigned act = __activemask();
+        const unsigned vis = __ballot_sync(act, proj_ok);
+        if (proj_ok && (threadIdx.x & 31) == __ffs(vis) - 1) atomicAdd(a.visible_count, (unsigned long long)__popc(vis));
+    }
+    if (!proj_ok) return;
     const double ca = cov[3] / det, cb = -cov[1] / det, cc = cov[0] / det;
     const double mid = 0.5 * (cov[0] + cov[3]);
     const double m2 = mid * mid - det;
     const double lambda_max = mid + sqrt(0.1 < m2 ? m2 : 0.1);
     const double radius = 3.0 * sqrt(lambda_max);
     a.visible[i] = 1;
-    atomicAdd(a.visible_count, 1ull);
 
     // ---- pixel rect -> tile rect (rasterizer.cpp:32-39)
     int x0 = floor_to_int(cxp - radius), x1 = floor_to_int(cxp + radius);
@@ -207,7 +237,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__
         double b[16];
         sh_basis(a.deg, dx, dy, dz, b);
         for (int ch = 0; ch < 3; ++ch) {
-            const Real* shc = a.sh + (i * 3 + ch) * a.K;
+            const Real* shc = sh_s + (size_t(threadIdx.x) * 3 + ch) * a.K;
             double t = double(shc[0]) * b[0];
             for (int j = 1; j < a.K; ++j) t += double(shc[j]) * b[j];
             const double raw = t + 0.5;
@@ -292,9 +322,14 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const __grid_constant__
 template <typename Real>
 void launch_preprocess(const PreprocessArgs<Real>& a, cudaStream_t s) {
     if (a.n == 0) return;
-    const int threads = 256;
-    const int64_t blocks = (a.n + threads - 1) / threads;
-    preprocess_kernel<Real><<<unsigned(blocks), threads, 0, s>>>(a);
+    const int64_t blocks = (a.n + kPreThreads - 1) / kPreThreads;
+    const size_t smem = sizeof(Real) * size_t(kPreThreads) * 3 * a.K + kPreThreads;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(preprocess_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = true;
+    }
+    preprocess_kernel<Real><<<unsigned(blocks), kPreThreads, smem, s>>>(a);
     count_launches(1);
 }
 
