@@ -189,16 +189,16 @@ __global__ void __launch_bounds__(256) projection_backward_kernel(const __grid_c
     for (int k = 0; k < 3; ++k) {
         a.g_pos[3 * i + k] = gp[k];
         a.g_scale[3 * i + k] = gs[k];
-        ok &= isfinite(double(gp[k])) && isfinite(double(gs[k]));
+        ok &= isfinite(gp[k]) && isfinite(gs[k]);
     }
     for (int j = 0; j < 4; ++j) {
         a.g_rot[4 * i + j] = gr[j];
-        ok &= isfinite(double(gr[j]));
+        ok &= isfinite(gr[j]);
     }
     a.g_opac[i] = go;
-    ok &= isfinite(double(go)) && isfinite(double(a.g_k[i]));
-    for (int j = 0; j < 3 * a.K; ++j) ok &= isfinite(double(a.g_sh[i * 3 * a.K + j]));
-    for (int j = 0; j < a.C; ++j) ok &= isfinite(double(a.g_sem[i * a.C + j]));
+    ok &= isfinite(go) && isfinite(a.g_k[i]);
+    for (int j = 0; j < 3 * a.K; ++j) ok &= isfinite(a.g_sh[i * 3 * a.K + j]);
+    for (int j = 0; j < a.C; ++j) ok &= isfinite(a.g_sem[i * a.C + j]);
     if (!ok) raise_error(a.err, kErrNonFiniteGrad, 0, i);
 }
 

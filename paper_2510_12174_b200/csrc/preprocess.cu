@@ -49,27 +49,28 @@ __device__ __forceinline__ void quat_to_rotation(const double* q, double* R) {
     R[6] = 2 * (x * z - w * y); R[7] = 2 * (y * z + w * x); R[8] = 1 - 2 * (x * x + y * y);
 }
 
-__device__ __forceinline__ void sh_basis(int deg, double x, double y, double z, double* b) {
-    const double C0 = 0.28209479177387814, C1 = 0.4886025119029199;
+template <typename T>
+__device__ __forceinline__ void sh_basis(int deg, T x, T y, T z, T* b) {
+    const T C0 = T(0.28209479177387814), C1 = T(0.4886025119029199);
     b[0] = C0;
     if (deg >= 1) { b[1] = -C1 * y; b[2] = C1 * z; b[3] = -C1 * x; }
     if (deg >= 2) {
-        const double xx = x * x, yy = y * y, zz = z * z;
-        b[4] = 1.0925484305920792 * x * y;
-        b[5] = -1.0925484305920792 * y * z;
-        b[6] = 0.31539156525252005 * (2 * zz - xx - yy);
-        b[7] = -1.0925484305920792 * x * z;
-        b[8] = 0.5462742152960396 * (xx - yy);
+        const T xx = x * x, yy = y * y, zz = z * z;
+        b[4] = T(1.0925484305920792) * x * y;
+        b[5] = -T(1.0925484305920792) * y * z;
+        b[6] = T(0.31539156525252005) * (T(2) * zz - xx - yy);
+        b[7] = -T(1.0925484305920792) * x * z;
+        b[8] = T(0.5462742152960396) * (xx - yy);
     }
     if (deg >= 3) {
-        const double xx = x * x, yy = y * y, zz = z * z;
-        b[9] = -0.5900435899266435 * y * (3 * xx - yy);
-        b[10] = 2.890611442640554 * x * y * z;
-        b[11] = -0.4570457994644658 * y * (4 * zz - xx - yy);
-        b[12] = 0.3731763325901154 * z * (2 * zz - 3 * xx - 3 * yy);
-        b[13] = -0.4570457994644658 * x * (4 * zz - xx - yy);
-        b[14] = 1.445305721320277 * z * (xx - yy);
-        b[15] = -0.5900435899266435 * x * (xx - 3 * yy);
+        const T xx = x * x, yy = y * y, zz = z * z;
+        b[9] = -T(0.5900435899266435) * y * (T(3) * xx - yy);
+        b[10] = T(2.890611442640554) * x * y * z;
+        b[11] = -T(0.4570457994644658) * y * (T(4) * zz - xx - yy);
+        b[12] = T(0.3731763325901154) * z * (T(2) * zz - 3 * xx - T(3) * yy);
+        b[13] = -T(0.4570457994644658) * x * (T(4) * zz - xx - yy);
+        b[14] = T(1.445305721320277) * z * (xx - yy);
+        b[15] = -T(0.5900435899266435) * x * (xx - T(3) * yy);
     }
 }
 
@@ -77,9 +78,9 @@ template <typename Real>
 __device__ __forceinline__ bool finite_params(const PreprocessArgs<Real>& a, int64_t i) {
     bool ok = true;
     for (int j = 0; j < 3; ++j)
-        ok &= isfinite(double(a.means[3 * i + j])) && isfinite(double(a.log_scales[3 * i + j]));
-    for (int j = 0; j < 4; ++j) ok &= isfinite(double(a.quats[4 * i + j]));
-    ok &= isfinite(double(a.opacity_logits[i])) && isfinite(double(a.k[i]));
+        ok &= isfinite(a.means[3 * i + j]) && isfinite(a.log_scales[3 * i + j]);
+    for (int j = 0; j < 4; ++j) ok &= isfinite(a.quats[4 * i + j]);
+    ok &= isfinite(a.opacity_logits[i]) && isfinite(a.k[i]);
     return ok;
 }
 
@@ -100,15 +101,23 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(const __grid_co
         const int rs = 3 * a.K;
         bad_s[threadIdx.x] = 0;
         __syncthreads();
+        // (element -> row index by a running quotient: no integer division per element)
         const Real* src = a.sh + base * rs;
-        for (int e = threadIdx.x; e < cnt * rs; e += kPreThreads) {
+        for (int e = threadIdx.x, row = threadIdx.x / rs, rem = threadIdx.x % rs; e < cnt * rs;
+             e += kPreThreads, rem += kPreThreads % rs, row += kPreThreads / rs) {
+            if (rem >= rs) { rem -= rs; ++row; }
             const Real v = src[e];
             sh_s[e] = v;
-            if (!isfinite(double(v))) bad_s[e / rs] = 1;
+            if (!isfinite(v)) bad_s[row] = 1;
         }
-        const Real* sem = a.semantics + base * a.C;
-        for (int e = threadIdx.x; e < cnt * a.C; e += kPreThreads)
-            if (!isfinite(double(sem[e]))) bad_s[e / a.C] = 1;
+        if (a.C > 0) {
+            const Real* sem = a.semantics + base * a.C;
+            for (int e = threadIdx.x, row = threadIdx.x / a.C, rem = threadIdx.x % a.C; e < cnt * a.C;
+                 e += kPreThreads, rem += kPreThreads % a.C, row += kPreThreads / a.C) {
+                if (rem >= a.C) { rem -= a.C; ++row; }
+                if (!isfinite(sem[e])) bad_s[row] = 1;
+            }
+        }
         __syncthreads();
     }
     const int64_t i = base + threadIdx.x;
@@ -142,7 +151,8 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(const __grid_co
     const double mu[3] = {double(a.means[3 * i]), double(a.means[3 * i + 1]), double(a.means[3 * i + 2])};
     const double s[3] = {exp(double(a.log_scales[3 * i])), exp(double(a.log_scales[3 * i + 1])),
                          exp(double(a.log_scales[3 * i + 2]))};
-    const double opacity = 1.0 / (1.0 + exp(-double(a.opacity_logits[i])));
+    // opacity / log threshold only feed Real-precision records
+    const Real opacity = Real(1) / (Real(1) + exp(-a.opacity_logits[i]));
 
     // ---- project_gaussian (geometry.cpp:107-136)
     double pc[3];
@@ -227,22 +237,24 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(const __grid_co
     }
 
     // ---- view-dependent colour (rasterizer.cpp:66-71, sh.cpp:75-84)
-    double rgb[3];
+    // In the kernel precision: the colour only feeds Real records (FP64 keeps
+    // the reference's double evaluation).
+    Real rgb[3];
     uint8_t clamped[3];
     {
         const double tg[3] = {mu[0] - c.tc2w[0], mu[1] - c.tc2w[1], mu[2] - c.tc2w[2]};
         const double nrm = sqrt(dot3(tg, tg));
         double dx = 0, dy = 0, dz = 1;
         if (nrm > 1e-12) { dx = tg[0] / nrm; dy = tg[1] / nrm; dz = tg[2] / nrm; }
-        double b[16];
-        sh_basis(a.deg, dx, dy, dz, b);
+        Real b[16];
+        sh_basis<Real>(a.deg, Real(dx), Real(dy), Real(dz), b);
         for (int ch = 0; ch < 3; ++ch) {
             const Real* shc = sh_s + (size_t(threadIdx.x) * 3 + ch) * a.K;
-            double t = double(shc[0]) * b[0];
-            for (int j = 1; j < a.K; ++j) t += double(shc[j]) * b[j];
-            const double raw = t + 0.5;
-            clamped[ch] = raw < 0;
-            rgb[ch] = clamped[ch] ? 0.0 : raw;
+            Real t = shc[0] * b[0];
+            for (int j = 1; j < a.K; ++j) t += shc[j] * b[j];
+            const Real raw = t + Real(0.5);
+            clamped[ch] = raw < Real(0);
+            rgb[ch] = clamped[ch] ? Real(0) : raw;
         }
     }
 
@@ -269,13 +281,13 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(const __grid_co
     ar.cb = Real(cb);
     ar.cc = Real(cc);
     ar.opacity = Real(opacity);
-    const double log_thr = log(1.0 / (255.0 * opacity));
-    ar.log_thr = Real(log_thr);
+    const Real log_thr = log(Real(1) / (Real(255) * opacity));
+    ar.log_thr = log_thr;
     ar.pad = Real(0);
     {
         // d^T conic d <= r2 with r2 = -2 (log_thr - 1e-3); the tight box of that
         // ellipse has half-widths sqrt(r2 cov_xx), sqrt(r2 cov_yy) (cov = conic^-1).
-        const double r2 = -2.0 * (log_thr - 1e-3);
+        const double r2 = -2.0 * (double(log_thr) - 1e-3);
         if (r2 > 0) {
             const double hx = sqrt(r2 * cov[0]) * 1.001 + 1e-3, hy = sqrt(r2 * cov[3]) * 1.001 + 1e-3;
             ar.bx0 = Real(cxp - hx);
