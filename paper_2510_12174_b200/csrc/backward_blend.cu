@@ -64,6 +64,8 @@ template <typename Real>
 struct WarpSmem {
     AlphaRec<Real> rec[32];
     uint32_t gid[32];
+    uint32_t emask[32];  // blend-event batch: forward lane mask (active lanes only)
+    uint32_t pos[32];    //   and list position
     Real dD[32];
     PairQueue<Real> q;
 };
@@ -71,7 +73,7 @@ struct WarpSmem {
 template <typename Real>
 size_t backward_smem_bytes(int C) {
     const int sp = seed_pitch(C);
-    return 8 * (sizeof(WarpSmem<Real>) + sizeof(Real) * size_t(32 + 1) * sp) + 64;
+    return 8 * (sizeof(WarpSmem<Real>) + sizeof(Real) * size_t(32 + 2) * sp) + 64;
 }
 
 template <typename Real>
@@ -257,9 +259,9 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const __grid_cons
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem<Real>* ws = reinterpret_cast<WarpSmem<Real>*>(smem_raw) + warp;
     Real* const warp_seed = reinterpret_cast<Real*>(reinterpret_cast<WarpSmem<Real>*>(smem_raw) + 8) +
-                            size_t(warp) * (32 + 1) * sp;
+                            size_t(warp) * (32 + 2) * sp;
     Real* const my_seed = warp_seed + size_t(lane) * sp;
-    Real* const warp_F = warp_seed + size_t(32) * sp;  // staged F_j
+    Real* const F_rows = warp_seed + size_t(32) * sp;  // staged F_j, double-buffered
     PairQueue<Real>& Q = ws->q;
 
     const int tile = blockIdx.x;
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const __grid_cons
     Real T_final = Real(1), dD = Real(0);
     bool any = false;
     for (int ch = 0; ch < sp; ++ch) my_seed[ch] = Real(0);
-    for (int i = lane; i < sp; i += 32) warp_F[i] = Real(0);
+    for (int i = lane; i < 2 * sp; i += 32) F_rows[i] = Real(0);
     if (inside) {
         term = a.terminus[p];
         T_final = a.T_final[p];
@@ -302,9 +304,8 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const __grid_cons
     const Real pxf = Real(x) + Real(0.5), pyf = Real(y) + Real(0.5);
     const Real bg_dot = Real(a.rp.bg[0]) * my_seed[0] + Real(a.rp.bg[1]) * my_seed[1] + Real(a.rp.bg[2]) * my_seed[2];
     Real T = T_final, accA = 0, lastFS = 0, last_alpha = 0;
-    const Real rx0 = Real(bx) + Real(0.5), rx1 = rx0 + Real(7);
-    const Real ry0 = Real(by) + Real(0.5), ry1 = ry0 + Real(3);
-    const uint32_t list0 = a.tile_range[tile].x;
+    const uint2 range = a.tile_range[tile];
+    const uint32_t list0 = range.x;
     // Clamped channel indices keep every shared read inside a seed row (C may be 0).
     const int c0 = lane < sp ? lane : 0, c1 = lane + 32 < sp ? lane + 32 : 0;
     // Destination of the F channel this lane accumulates (F = [rgb, k, sem]):
@@ -312,46 +313,46 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const __grid_cons
     Real* const dst0 = lane < 3 ? a.acc_dcolor + lane : (lane == 3 ? a.g_k : a.g_sem + (lane - 4));
     const int stride0 = lane < 3 ? 3 : (lane == 3 ? 1 : C);
     Real* const dst1 = a.g_sem + (lane + 28);  // channel lane + 32
-    int qn = 0;
+    int qn = 0, fb = 0;
+    // The forward's blend-event log for this warp: exactly the (Gaussian, lane
+    // mask) events in which some pixel of the block blended, front to back.
+    // Replayed back to front in batches of 32 whose ids and alpha records are
+    // fetched in parallel; no culling or alpha test of non-blending pairs.
+    const unsigned act_mask = __ballot_sync(0xffffffffu, term > 0);
+    const uint32_t nev = a.ev_count[size_t(tile) * 8 + warp];
+    const uint2* const evl = a.ev_list + size_t(8) * list0 + size_t(warp) * (range.y - list0);
 
-    for (int c = (wmax - 1) >> 5; c >= 0; --c) {
-        const int pos = c * 32 + lane;
-        bool hit = false;
-        if (pos < wmax) {
-            const uint32_t g = a.inst_gauss[list0 + pos];
-            const AlphaRec<Real> r = a.arec[g];
-            ws->rec[lane] = r;
-            ws->gid[lane] = g;
-            hit = !(r.bx1 < rx0 || r.bx0 > rx1 || r.by1 < ry0 || r.by0 > ry1);
-            if (hit) {  // the event staging below reads these: pull them into L1 now
-                const char* sem = reinterpret_cast<const char*>(a.semantics + size_t(g) * C);
-                for (int off = 0; off < int(sizeof(Real)) * C; off += 128)
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(sem + off));
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(a.brec + g) + 48));
+    for (int cb = int(nev) - 1; cb >= 0; cb -= 32) {
+        __syncwarp();  // the previous batch's records are no longer read
+        {
+            const int e = cb - lane;
+            if (e >= 0) {
+                const uint2 ev = evl[e];
+                const uint32_t g = a.inst_gauss[list0 + ev.x];
+                ws->rec[lane] = a.arec[g];
+                ws->gid[lane] = g;
+                ws->emask[lane] = ev.y & act_mask;
+                ws->pos[lane] = ev.x;
             }
         }
-        unsigned bits = __ballot_sync(0xffffffffu, hit);
         __syncwarp();
-        while (bits) {
-            const int slot = 31 - __clz(bits);
-            bits &= ~(1u << slot);
+        const int nb = cb + 1 < 32 ? cb + 1 : 32;
+        stage_F_async<Real>(F_rows + fb * sp, a.brec, a.semantics, C, ws->gid[0], lane);
+        for (int slot = 0; slot < nb; ++slot) {
+            const Real* const warp_F = F_rows + fb * sp;
+            fb ^= 1;
+            // the next event's row streams in while this one is processed
+            if (slot + 1 < nb) stage_F_async<Real>(F_rows + fb * sp, a.brec, a.semantics, C, ws->gid[slot + 1], lane);
+            else stage_F_commit_empty();
+            const unsigned fmask = ws->emask[slot];
+            if (fmask == 0) continue;
             AlphaEval<Real> ae;
             ae.pass = false;
-            if (c * 32 + slot < term) ae = eval_alpha<Real>(ws->rec[slot], pxf, pyf);
+            if ((fmask >> lane) & 1u) ae = eval_alpha<Real>(ws->rec[slot], pxf, pyf);
             const unsigned mask = __ballot_sync(0xffffffffu, ae.pass);
             if (mask == 0) continue;
+            stage_F_wait_prev();
             const uint32_t g = ws->gid[slot];
-            // Stage F_j = [rgb, k, sem].
-            if (lane < 4) {
-                const BlendRec<Real>& br = a.brec[g];
-                warp_F[lane] = lane < 3 ? br.rgb[lane] : br.k;
-            }
-            {
-                const Real* semg = a.semantics + size_t(g) * C;
-                if (lane < C) warp_F[4 + lane] = semg[lane];
-                if (lane + 32 < C) warp_F[36 + lane] = semg[lane + 32];
-                for (int ch = lane + 64; ch < C; ch += 32) warp_F[4 + ch] = semg[ch];  // C > 64
-            }
             __syncwarp();
             if (ae.pass) {
                 // One reciprocal for the T restore and the background term (FP32);
@@ -368,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const __grid_cons
                 const AlphaRec<Real>& ar = ws->rec[slot];
                 Q.meta[e] = uint32_t(lane) | (ae.clamped ? (1u << 8) : 0u);
                 Q.gid[e] = g;
-                if constexpr (DET) Q.inst[e] = list0 + uint32_t(c * 32 + slot);
+                if constexpr (DET) Q.inst[e] = list0 + ws->pos[slot];
                 Q.ws[e] = WeightRow<Real>{w, uint32_t(lane * sp)};
                 Q.da[e] = dalpha;
                 Q.al[e] = ae.alpha;
@@ -391,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const __grid_cons
                     acc1 += wr.w * warp_seed[wr.soff + c1];
                 }
                 if constexpr (DET) {  // fields 16 + ch: dcolor, dk, dsem
-                    Real* const ps = a.partial + (size_t(list0 + c * 32 + slot) * 8 + warp) * a.V + 16;
+                    Real* const ps = a.partial + (size_t(list0 + ws->pos[slot]) * 8 + warp) * a.V + 16;
                     if (lane < S && acc0 != Real(0)) ps[lane] += acc0;
                     if (lane + 32 < S && acc1 != Real(0)) ps[lane + 32] += acc1;
                     for (int ch = lane + 64; ch < S; ch += 32) {

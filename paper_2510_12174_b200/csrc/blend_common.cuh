@@ -274,6 +274,33 @@ __device__ __forceinline__ void quat_rotation_backward(const Real* q, const Real
 }
 
 // Tile-local pixel coordinates: warps cover 8x4 pixel blocks, 2 across x 4 down.
+// Asynchronous staging of F_j = [rgb, k, sem] (the per-Gaussian row the
+// backward reads every event) into a shared row with cp.async: issued one event
+// ahead into the other half of a double buffer, it costs no registers and the
+// L2 latency overlaps the current event.  Channels >= C + 4 of the row are
+// never written (callers zero them once).
+template <typename Real>
+__device__ __forceinline__ void stage_F_async(Real* row, const BlendRec<Real>* brec, const Real* semantics, int C,
+                                              uint32_t g, int lane) {
+    const int S = C + 4;
+    for (int ch = lane; ch < S; ch += 32) {
+        const Real* src = ch < 3 ? &brec[g].rgb[ch] : (ch == 3 ? &brec[g].k : semantics + size_t(g) * C + (ch - 4));
+        const unsigned dst = unsigned(__cvta_generic_to_shared(row + ch));
+        if constexpr (sizeof(Real) == 4)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+        else
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void stage_F_commit_empty() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// Waits until at most the lookahead row is in flight, then makes the completed
+// rows warp-visible.
+__device__ __forceinline__ void stage_F_wait_prev() {
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+}
+
 __device__ __forceinline__ int tile_pixel_x(int warp, int lane) { return (warp & 1) * 8 + (lane & 7); }
 __device__ __forceinline__ int tile_pixel_y(int warp, int lane) { return (warp >> 1) * 4 + (lane >> 3); }
 __device__ __forceinline__ int tile_pixel_index(int warp, int lane) {

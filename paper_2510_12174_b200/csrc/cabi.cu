@@ -164,7 +164,7 @@ struct msplat_replay {
     DevBuf arec, brec, visible, clamped, depth_key, depth_key_alt, order, order_alt, tile_count, tile_rect,
         count_sorted, offset_sorted, inst_tile, inst_tile_alt, inst_gauss, inst_gauss_alt, tile_range,
         d_inst_count, d_inst_total32, hist, hist_scanned, scan_tiles, terminus, weight_sums, saved_means,
-        saved_k, cap_center, cap_conic, cap_depth, cap_radius, cap_rgb, visible_count;
+        saved_k, cap_center, cap_conic, cap_depth, cap_radius, cap_rgb, visible_count, ev_list, ev_count;
     uint32_t* sorted_gauss = nullptr;
 
     void release_all() {
@@ -172,7 +172,8 @@ struct msplat_replay {
                           &tile_count, &tile_rect, &count_sorted, &offset_sorted, &inst_tile, &inst_tile_alt,
                           &inst_gauss, &inst_gauss_alt, &tile_range, &d_inst_count, &d_inst_total32, &hist,
                           &hist_scanned, &scan_tiles, &terminus, &weight_sums, &saved_means, &saved_k,
-                          &cap_center, &cap_conic, &cap_depth, &cap_radius, &cap_rgb, &visible_count})
+                          &cap_center, &cap_conic, &cap_depth, &cap_radius, &cap_rgb, &visible_count, &ev_list,
+                          &ev_count})
             b->release();
     }
 };
@@ -303,6 +304,8 @@ msplat_status size_replay(msplat_replay* r, int dtype, int64_t n, int C, int deg
     const size_t ic = size_t(r->inst_cap);
     CUDA_TRY(r->inst_tile.ensure(ic * 4));
     CUDA_TRY(r->inst_tile_alt.ensure(ic * 4));
+    CUDA_TRY(r->ev_list.ensure(ic * 8 * sizeof(uint2)));  // 8 warps x (position, mask) per instance
+    CUDA_TRY(r->ev_count.ensure(size_t(tiles) * 8 * 4));
     CUDA_TRY(r->inst_gauss.ensure(ic * 4));
     CUDA_TRY(r->inst_gauss_alt.ensure(ic * 4));
     CUDA_TRY(r->tile_range.ensure(size_t(tiles) * 8));
@@ -462,6 +465,8 @@ msplat_status rasterize_impl(msplat_context* ctx, const msplat_scene* s, const m
     a.contributors = f->contributors;
     a.terminus = r->terminus.as<int32_t>();
     a.weight_sums = (r->capture & 2) ? r->weight_sums.as<Real>() : nullptr;
+    a.ev_list = r->ev_list.as<uint2>();
+    a.ev_count = r->ev_count.as<uint32_t>();
     a.err = ctx->d_err;
     ctx->timer.begin(MSPLAT_STAGE_FORWARD, ctx->stream);
     launch_forward<Real>(a, r->tiles_x * r->tiles_y, ctx->stream);
@@ -534,6 +539,8 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
     a.semantics = static_cast<const Real*>(s->semantics);
     a.raw = RawParams<Real>{static_cast<const Real*>(s->means), static_cast<const Real*>(s->quats),
                             static_cast<const Real*>(s->log_scales), r->rp.sigma_scale};
+    a.ev_list = r->ev_list.as<uint2>();
+    a.ev_count = r->ev_count.as<uint32_t>();
     a.T_final = static_cast<const Real*>(f->transmittance);
     a.terminus = r->terminus.as<int32_t>();
     a.dcolor = static_cast<const Real*>(pix->dcolor);

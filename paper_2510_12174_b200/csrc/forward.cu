@@ -103,6 +103,8 @@ __global__ void __launch_bounds__(kThreads, 2) forward_kernel(const __grid_const
     const bool c0 = lane < C, c1 = lane + 32 < C;
     int qn = 0;
     unsigned long long own = 0;  // queue entries owned by this pixel
+    uint2* const evl = a.ev_list ? a.ev_list + size_t(8) * range.x + size_t(warp) * len : nullptr;
+    uint32_t n_ev = 0;
 
     for (int c = 0; c * 32 < len; ++c) {
         if (__all_sync(0xffffffffu, done)) break;
@@ -126,6 +128,10 @@ __global__ void __launch_bounds__(kThreads, 2) forward_kernel(const __grid_const
             if (!done) ae = eval_alpha<Real>(ws->rec[slot], pxf, pyf);
             const unsigned mask = __ballot_sync(0xffffffffu, ae.pass);
             if (mask == 0) continue;
+            if (evl) {  // the backward replays exactly these events
+                if (lane == 0) evl[n_ev] = make_uint2(uint32_t(c * 32 + slot), mask);
+                ++n_ev;
+            }
             const uint32_t g = ws->gid[slot];
             if (ae.pass) {
                 if (!isfinite(ae.alpha)) {
@@ -208,6 +214,7 @@ __global__ void __launch_bounds__(kThreads, 2) forward_kernel(const __grid_const
         }
     }
     if (qn > 0) flush_depth<Real>(a, ws, qn, bx, by, dep, unsigned(own));
+    if (a.ev_count && lane == 0) a.ev_count[size_t(tile) * 8 + warp] = n_ev;
     if (!inside) return;
     col0 += T * Real(a.rp.bg[0]);
     col1 += T * Real(a.rp.bg[1]);

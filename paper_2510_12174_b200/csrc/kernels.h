@@ -94,6 +94,12 @@ struct ForwardArgs {
     int32_t* contributors;
     int32_t* terminus;
     Real* weight_sums;  // optional
+    // Blend-event log for the backward (optional): per (tile, warp) the events
+    // in which some lane blended, front to back, as (list position, lane mask),
+    // in the region [8 * range.x + warp * len, + len) of a buffer of 8 I
+    // entries; ev_count[tile * 8 + warp] = number of events.
+    uint2* ev_list;
+    uint32_t* ev_count;
     DeviceError* err;
 };
 template <typename Real>
@@ -132,6 +138,8 @@ struct BackwardArgs {
     const BlendRec<Real>* brec;
     const Real* semantics;
     RawParams<Real> raw;
+    const uint2* ev_list;     // the forward's blend-event log (ForwardArgs::ev_list)
+    const uint32_t* ev_count;
     const Real* T_final;
     const int32_t* terminus;
     const Real *dcolor, *ddepth, *dsem, *dkmap;  // planar pixel grads
