@@ -34,13 +34,11 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kQueue = 64;  // per-warp pair queue (flushed at >= 32)
 
-// Seed rows [dC0 dC1 dC2 dK dO...]: multiple of 4 (128-bit loads) with an odd
-// number of 16-byte units per row (conflict-free when each lane reads its row).
-__host__ __device__ inline int seed_pitch(int C) {
-    int p = ((C + 4 + 3) / 4) * 4;
-    if (((p / 4) & 1) == 0) p += 4;
-    return p;
-}
+// Seed rows [dC0 dC1 dC2 dK dO...]: the channel count rounded up to the mma K
+// step (8) plus 4 -- an odd number of 16-byte units per row, so both per-lane
+// row reads and the mma fragment loads (row = lane / 4) are conflict-free.
+__host__ __device__ inline int seed_k8(int C) { return ((C + 4 + 7) / 8) * 8; }
+__host__ __device__ inline int seed_pitch(int C) { return seed_k8(C) + 4; }
 
 // Blend weight + the pixel's seed-row offset, read together (one 64-bit LDS
 // for FP32) by the seed-linear loop.
@@ -52,6 +50,8 @@ struct __align__(2 * sizeof(Real)) WeightRow {
 
 template <typename Real>
 struct PairQueue {
+    static constexpr bool kConic = true;  // entries carry the splat centre / conic
+    __device__ Real weight(int i) const { return ws[i].w; }
     uint32_t meta[kQueue];  // pixel lane | clamped << 8
     uint32_t gid[kQueue];
     uint32_t inst[kQueue];  // position in the tile-sorted list (deterministic mode)
@@ -113,14 +113,15 @@ __device__ __forceinline__ Real seg_sum(Real v, const bool* same) {
 
 // Phase B on the first n queue entries (n <= 32): per-pair geometric
 // gradients, segmented by Gaussian, one atomic per value per Gaussian.
-template <typename Real, bool DET>
-__device__ __forceinline__ void flush_pairs(const BackwardArgs<Real>& a, const PairQueue<Real>& q, const Real* dDw,
-                                         int n, int bx, int by) {
+template <typename Real, bool DET, typename Queue>
+__device__ __forceinline__ void flush_pairs(const BackwardArgs<Real>& a, const Queue& q, const Real* dDw, int n, int bx,
+                                            int by) {
     const int lane = threadIdx.x & 31;
     const bool act = lane < n;
     const uint32_t meta = act ? q.meta[lane] : 0u;
     const uint32_t g = act ? q.gid[lane] : 0xffffffffu - lane;  // padding lanes: unique keys
-    const uint32_t inst = DET && act ? q.inst[lane] : 0u;
+    uint32_t inst = 0u;
+    if constexpr (DET) inst = act ? q.inst[lane] : 0u;
     bool same[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
@@ -135,11 +136,25 @@ __device__ __forceinline__ void flush_pairs(const BackwardArgs<Real>& a, const P
     if (act) {
         const int L = int(meta & 0xffu);
         const bool clamped = (meta >> 8) & 1u;
-        const Real w = q.ws[lane].w, dalpha = q.da[lane], alpha = q.al[lane], gauss = q.gs[lane];
+        const Real w = q.weight(lane), dalpha = q.da[lane], alpha = q.al[lane], gauss = q.gs[lane];
         const int xL = bx + (L & 7), yL = by + (L >> 3);
-        const Real dx = Real(xL) + Real(0.5) - q.cx[lane], dy = Real(yL) + Real(0.5) - q.cy[lane];
+        Real pcx, pcy, ca, cb, cc;
+        if constexpr (Queue::kConic) {
+            pcx = q.cx[lane];
+            pcy = q.cy[lane];
+            ca = q.ca[lane];
+            cb = q.cb[lane];
+            cc = q.cc[lane];
+        } else {  // compact queue: re-read the splat record (L2-resident)
+            const AlphaRec<Real> r = a.arec[g];
+            pcx = r.cx;
+            pcy = r.cy;
+            ca = r.ca;
+            cb = r.cb;
+            cc = r.cc;
+        }
+        const Real dx = Real(xL) + Real(0.5) - pcx, dy = Real(yL) + Real(0.5) - pcy;
         if (!clamped) {  // rasterizer_backward.cpp:234-244
-            const Real ca = q.ca[lane], cb = q.cb[lane], cc = q.cc[lane];
             v[0] = gauss * dalpha;
             const Real dpower = alpha * dalpha;
             v[1] = dpower * (ca * dx + cb * dy);
@@ -437,6 +452,295 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const __grid_cons
     if (qn > 0) flush_pairs<Real, DET>(a, Q, ws->dD, qn, bx, by);
 }
 
+// ---------------------------------------------------------------------------
+// K9 (FP32) on the tensor cores.  The two C-length contractions of the reverse
+// blend are GEMMs once a warp's blend events are taken kSub at a time from the
+// forward's event log:
+//   GEMM1  FS[px][e]  = sum_ch S[px][ch] F_e[ch]        (F_j . s_p for dalpha)
+//   GEMM2  dF[ch][e]  = sum_px S[px][ch] w_e[px]         (dcolor, dk, dsem)
+// with S the warp's 32 seed rows [dC, dK, dO] and F_e = [rgb, k, sem] of event
+// e.  Both run as mma.sync.m16n8k8 TF32 with a hi/lo split of every operand
+// (a_hi b_hi + a_hi b_lo + a_lo b_hi: FP32-level accuracy), the events on the
+// N = 8 side.  Between them the per-pixel recursion (T restore, w = alpha T,
+// dalpha with the suffix accumulator) runs sequentially per event exactly as
+// in backward_kernel, reading FS from shared memory and enqueueing pairs for
+// the same phase-B flush.
+namespace {
+
+constexpr int kSub = 8;         // events per sub-batch (mma N)
+constexpr int kTilePitch = 36;  // FS / W tiles [kSub][36]: conflict-free fragment stores and row reads
+
+struct PairQueueTC {
+    static constexpr bool kConic = false;  // centre / conic re-read from the splat record
+    __device__ float weight(int i) const { return w[i]; }
+    uint32_t meta[kQueue];
+    uint32_t gid[kQueue];
+    float w[kQueue], da[kQueue], al[kQueue], gs[kQueue];
+};
+
+struct WarpSmemTC {
+    AlphaRec<float> rec[kSub];
+    uint32_t gid[32];
+    uint32_t emask[32];
+    uint32_t pos[32];
+    float dD[32];
+    PairQueueTC q;
+};
+
+__host__ __device__ inline int tc_stage_floats(int C) {
+    const int sp = seed_pitch(C);
+    return kSub * sp > kSub * kTilePitch ? kSub * sp : kSub * kTilePitch;
+}
+__host__ __device__ inline int tc_warp_floats(int C) {
+    return 32 * seed_pitch(C) + tc_stage_floats(C) + kSub * kTilePitch;
+}
+size_t backward_tc_smem_bytes(int C) {
+    return 8 * (sizeof(WarpSmemTC) + sizeof(float) * size_t(tc_warp_floats(C))) + 64;
+}
+
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+    const float r = x - __uint_as_float(hi);
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+// d += A B with the 3-term split (A: 4 fp32 fragment values, B: 2).
+__device__ __forceinline__ void mma_3xtf32(float (&d)[4], const float (&a)[4], const float (&b)[2]) {
+    uint32_t ah[4], al[4], bh[2], bl[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) split_tf32(a[i], ah[i], al[i]);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) split_tf32(b[i], bh[i], bl[i]);
+    mma_tf32(d, al, bh);
+    mma_tf32(d, ah, bl);
+    mma_tf32(d, ah, bh);
+}
+
+}  // namespace
+
+// Stages F rows [rgb, k | sem] of n events into rows of pitch sp: one 16-byte
+// copy of (rgb, k) (BlendRec offset 80, 16-byte aligned) plus the semantic row
+// in 8-byte pieces when C is even (4-byte otherwise); lanes stride over all
+// pieces of all n rows, so one pass issues every copy.
+__device__ __forceinline__ void stage_rows_tc(float* Fb, int sp, const BlendRec<float>* brec, const float* semantics,
+                                              int C, const uint32_t* gid, int n, int lane) {
+    if ((C & 1) == 0) {
+        const int per = 1 + C / 2;  // pieces per row
+        for (int q = lane; q < n * per; q += 32) {
+            const int e = q / per, j = q - e * per;
+            const uint32_t g = gid[e];
+            if (j == 0) {
+                const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + e * sp));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(&brec[g].rgb[0]) : "memory");
+            } else {
+                const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + e * sp + 4 + 2 * (j - 1)));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst),
+                             "l"(semantics + size_t(g) * C + 2 * (j - 1))
+                             : "memory");
+            }
+        }
+    } else {
+        const int per = 1 + C;
+        for (int q = lane; q < n * per; q += 32) {
+            const int e = q / per, j = q - e * per;
+            const uint32_t g = gid[e];
+            if (j == 0) {
+                const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + e * sp));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(&brec[g].rgb[0]) : "memory");
+            } else {
+                const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + e * sp + 4 + (j - 1)));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst),
+                             "l"(semantics + size_t(g) * C + (j - 1))
+                             : "memory");
+            }
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_constant__ BackwardArgs<float> a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int C = a.C, sp = seed_pitch(C), S = C + 4, K8 = seed_k8(C);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g4 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
+    WarpSmemTC* ws = reinterpret_cast<WarpSmemTC*>(smem_raw) + warp;
+    float* const warp_seed =
+        reinterpret_cast<float*>(reinterpret_cast<WarpSmemTC*>(smem_raw) + 8) + size_t(warp) * tc_warp_floats(C);
+    float* const my_seed = warp_seed + size_t(lane) * sp;
+    float* const Fb = warp_seed + size_t(32) * sp;  // [kSub][sp] F rows; then FS [kSub][36] in place
+    float* const FSs = Fb;
+    float* const Wb = Fb + tc_stage_floats(C);      // [kSub][36] blend weights
+    PairQueueTC& Q = ws->q;
+
+    const int tile = blockIdx.x;
+    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    const int bx = tx * kTile + (warp & 1) * 8, by = ty * kTile + (warp >> 1) * 4;
+    const int x = bx + (lane & 7), y = by + (lane >> 3);
+    const bool inside = x < a.W && y < a.H;
+    const size_t HW = size_t(a.W) * a.H, p = size_t(y) * a.W + x;
+
+    int term = 0;
+    float T_final = 1.f, dD = 0.f;
+    bool any = false;
+    for (int ch = 0; ch < sp; ++ch) my_seed[ch] = 0.f;
+    for (int i = lane; i < tc_stage_floats(C) + kSub * kTilePitch; i += 32) Fb[i] = 0.f;
+    if (inside) {
+        term = a.terminus[p];
+        T_final = a.T_final[p];
+        dD = a.ddepth[p];
+        for (int ch = 0; ch < 3; ++ch) {
+            my_seed[ch] = a.dcolor[ch * HW + p];
+            any |= my_seed[ch] != 0.f;
+        }
+        my_seed[3] = a.dkmap[p];
+        any |= my_seed[3] != 0.f || dD != 0.f;
+        for (int ch = 0; ch < C; ++ch) {
+            my_seed[4 + ch] = a.dsem[size_t(ch) * HW + p];
+            any |= my_seed[4 + ch] != 0.f;
+        }
+    }
+    // rasterize_backward.cpp:156-171: nothing to do without blends or seeds.
+    if (!(inside && term > 0 && any)) term = 0;
+    ws->dD[lane] = dD;
+    const unsigned act_mask = __ballot_sync(0xffffffffu, term > 0);
+    if (act_mask == 0) return;
+    __syncwarp();
+
+    const float pxf = float(x) + 0.5f, pyf = float(y) + 0.5f;
+    const float bg_dot = float(a.rp.bg[0]) * my_seed[0] + float(a.rp.bg[1]) * my_seed[1] + float(a.rp.bg[2]) * my_seed[2];
+    float T = T_final, accA = 0.f, lastFS = 0.f, last_alpha = 0.f;
+    const uint2 range = a.tile_range[tile];
+    const uint32_t list0 = range.x;
+    const uint32_t nev = a.ev_count[size_t(tile) * 8 + warp];
+    const uint2* const evl = a.ev_list + size_t(8) * list0 + size_t(warp) * (range.y - list0);
+    const int mtiles2 = (S + 15) / 16;  // GEMM2 channel tiles
+    int qn = 0;
+
+    for (int cb = int(nev) - 1; cb >= 0; cb -= 32) {
+        __syncwarp();
+        {
+            const int e = cb - lane;
+            if (e >= 0) {
+                const uint2 ev = evl[e];
+                ws->gid[lane] = a.inst_gauss[list0 + ev.x];
+                ws->emask[lane] = ev.y & act_mask;
+                ws->pos[lane] = ev.x;
+            }
+        }
+        __syncwarp();
+        const int nb = cb + 1 < 32 ? cb + 1 : 32;
+        for (int s0 = 0; s0 < nb; s0 += kSub) {
+            const int ns = nb - s0 < kSub ? nb - s0 : kSub;
+            // (a) F rows (cp.async) and alpha records of the sub-batch.
+            stage_rows_tc(Fb, sp, a.brec, a.semantics, C, ws->gid + s0, ns, lane);
+            if (lane < ns) ws->rec[lane] = a.arec[ws->gid[s0 + lane]];
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
+            // (b) GEMM1: FS[px][e], px on M (two 16-row tiles), events on N.
+            float d1[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+            for (int k0 = 0; k0 < K8; k0 += 8) {
+                const float bf[2] = {Fb[g4 * sp + k0 + t4], Fb[g4 * sp + k0 + t4 + 4]};
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    const float* A0 = warp_seed + (mt * 16 + g4) * sp + k0 + t4;
+                    const float af[4] = {A0[0], A0[8 * sp], A0[4], A0[8 * sp + 4]};
+                    mma_3xtf32(d1[mt], af, bf);
+                }
+            }
+            __syncwarp();  // every lane is done with Fb: FS overwrites it
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    FSs[(2 * t4 + (i & 1)) * kTilePitch + mt * 16 + 8 * (i >> 1) + g4] = d1[mt][i];
+            __syncwarp();
+            // (c) the reference's sequential recursion, event by event.
+            for (int e = 0; e < ns; ++e) {
+                const unsigned fmask = ws->emask[s0 + e];
+                AlphaEval<float> ae;
+                ae.pass = false;
+                if ((fmask >> lane) & 1u) ae = eval_alpha<float>(ws->rec[e], pxf, pyf);
+                const unsigned mask = __ballot_sync(0xffffffffu, ae.pass);
+                float wv = 0.f;
+                if (ae.pass) {
+                    const float inv = 1.f / (1.f - ae.alpha);
+                    T = T * inv;
+                    const float w = ae.alpha * T;
+                    const float FS = FSs[e * kTilePitch + lane];
+                    accA = last_alpha * lastFS + (1.f - last_alpha) * accA;
+                    const float dalpha = (FS - accA) * T - T_final * inv * bg_dot;
+                    lastFS = FS;
+                    last_alpha = ae.alpha;
+                    const int qe = qn + __popc(mask & ((1u << lane) - 1u));
+                    Q.meta[qe] = uint32_t(lane) | (ae.clamped ? (1u << 8) : 0u);
+                    Q.gid[qe] = ws->gid[s0 + e];
+                    Q.w[qe] = w;
+                    Q.da[qe] = dalpha;
+                    Q.al[qe] = ae.alpha;
+                    Q.gs[qe] = ae.gauss;
+                    wv = w;
+                }
+                Wb[e * kTilePitch + lane] = wv;
+                qn += __popc(mask);
+                __syncwarp();
+                if (qn >= 32) {
+                    flush_pairs<float, false>(a, Q, ws->dD, 32, bx, by);
+                    const int rest = qn - 32;
+                    if (lane < rest) {  // reads >= 32, writes < 32
+                        const int s2 = 32 + lane;
+                        Q.meta[lane] = Q.meta[s2];
+                        Q.gid[lane] = Q.gid[s2];
+                        Q.w[lane] = Q.w[s2];
+                        Q.da[lane] = Q.da[s2];
+                        Q.al[lane] = Q.al[s2];
+                        Q.gs[lane] = Q.gs[s2];
+                    }
+                    qn = rest;
+                    __syncwarp();
+                }
+            }
+            for (int e = ns; e < kSub; ++e) Wb[e * kTilePitch + lane] = 0.f;
+            __syncwarp();
+            // (d) GEMM2: dF[ch][e] = sum_px S[px][ch] w_e[px], channels on M.
+            // this lane's two events (columns 2 t4, 2 t4 + 1): semantic channel ch
+            // lands at sem_base + ch; channels 0..3 (colour, k) are special.
+            const uint32_t ge0 = ws->gid[s0 + (2 * t4 < ns ? 2 * t4 : 0)];
+            const uint32_t ge1 = ws->gid[s0 + (2 * t4 + 1 < ns ? 2 * t4 + 1 : 0)];
+            float* const sem0 = a.g_sem + size_t(ge0) * C - 4;
+            float* const sem1 = a.g_sem + size_t(ge1) * C - 4;
+            for (int mt = 0; mt < mtiles2; ++mt) {
+                float d2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int k0 = 0; k0 < 32; k0 += 8) {
+                    const float bf[2] = {Wb[g4 * kTilePitch + k0 + t4], Wb[g4 * kTilePitch + k0 + t4 + 4]};
+                    const float* A0 = warp_seed + (k0 + t4) * sp + mt * 16 + g4;
+                    const float af[4] = {A0[0], A0[8], A0[4 * sp], A0[4 * sp + 8]};
+                    mma_3xtf32(d2, af, bf);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int ch = mt * 16 + g4 + 8 * (i >> 1), e = 2 * t4 + (i & 1);
+                    if (ch < S && e < ns && d2[i] != 0.f) {
+                        const uint32_t gg = (i & 1) ? ge1 : ge0;
+                        float* dst = ch >= 4 ? ((i & 1) ? sem1 : sem0) + ch
+                                             : (ch < 3 ? a.acc_dcolor + size_t(gg) * 3 + ch : a.g_k + gg);
+                        atomicAdd(dst, d2[i]);
+                    }
+                }
+            }
+        }
+    }
+    if (qn > 0) flush_pairs<float, false>(a, Q, ws->dD, qn, bx, by);
+}
+
 template <typename Real>
 void launch_backward_blend(const BackwardArgs<Real>& a, int ntiles, cudaStream_t s) {
     if (ntiles == 0) return;
@@ -446,10 +750,18 @@ void launch_backward_blend(const BackwardArgs<Real>& a, int ntiles, cudaStream_t
         cudaFuncSetAttribute(backward_kernel<Real, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         configured = true;
     }
-    if (a.partial)
+    if (a.partial) {
         backward_kernel<Real, true><<<ntiles, kThreads, backward_smem_bytes<Real>(a.C), s>>>(a);
-    else
+    } else if constexpr (sizeof(Real) == 4) {
+        static bool tc_configured = false;
+        if (!tc_configured) {
+            cudaFuncSetAttribute(backward_kernel_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            tc_configured = true;
+        }
+        backward_kernel_tc<<<ntiles, kThreads, backward_tc_smem_bytes(a.C), s>>>(a);
+    } else {
         backward_kernel<Real, false><<<ntiles, kThreads, backward_smem_bytes<Real>(a.C), s>>>(a);
+    }
     count_launches(1);
 }
 
