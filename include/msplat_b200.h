@@ -227,6 +227,42 @@ MSPLAT_API msplat_status msplat_fwd_bwd(msplat_context* ctx, const msplat_scene*
                              const msplat_pixel_grads* pix, msplat_grads* grads, int chain,
                              int accumulate, msplat_replay* replay);
 
+/* Ground truth of one frame (msplat/dataset.hpp FrameRecord), planar device
+ * buffers in the frame's dtype; NULL = modality absent. */
+typedef struct {
+    const void* rgb;       /* [3][H][W]                                  */
+    const void* depth;     /* [H][W]; pixels with depth > 0 supervised    */
+    const void* normal;    /* [3][H][W]; non-zero normals supervised      */
+    const uint8_t* labels; /* [H][W] class ids                            */
+} msplat_ground_truth;
+
+/* LossReport (msplat/losses.hpp:40-50), field for field. */
+typedef struct {
+    double l1, ssim, depth, normal, seg, k, combined;
+    double ratio_ssim, ratio_normal, ratio_depth, ratio_seg, ratio_k;
+    double seed_l1, seed_ssim, seed_depth, seed_normal, seed_seg, seed_k;
+} msplat_loss_report;
+
+/* evaluate_frame_losses(frame, nstate, gt, view, cfg)  (core/src/trainer.cpp:171-264)
+ * on the device: l1_rgb, ssim_loss, depth_l1, normal_cosine, cross_entropy_seg,
+ * gradient_factor_loss and combine (core/src/losses.cpp:87-313), then the
+ * seeded pixel gradients: out->dcolor/ddepth/dsemantics/dkmap are overwritten,
+ * and the normal term is pushed through normals_backward into ddepth.  The
+ * frame needs color, depth, semantics, kmap, transmittance and normals (from
+ * msplat_estimate_normals: a non-zero normal marks a valid pixel).
+ * lambdas = (l1, ssim, normal, depth, seg, k); 0 disables a modality.
+ * host_report != NULL: synchronizing copy of the report (and device-error
+ * check); NULL: asynchronous, the report stays on the device
+ * (msplat_loss_report_device) -- graph-capturable. */
+MSPLAT_API msplat_status msplat_frame_losses(msplat_context* ctx, int dtype, int num_classes,
+                                  const msplat_camera* camera, const msplat_normal_config* ncfg,
+                                  const msplat_frame* frame, const msplat_ground_truth* gt,
+                                  const double lambdas[6], msplat_pixel_grads* out,
+                                  msplat_loss_report* host_report);
+/* Device address of the last msplat_frame_losses report (18 doubles in
+ * msplat_loss_report order); valid until the next call on this context. */
+MSPLAT_API const double* msplat_loss_report_device(msplat_context* ctx);
+
 /* adam_step(scene, grads, state, cfg)   (core/src/trainer.cpp:98-133) on packed
  * n*P buffers (msplat_param_layout); lr[7] per parameter group; step is the
  * post-increment optimizer step. */

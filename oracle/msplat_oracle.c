@@ -851,6 +851,252 @@ int mo_normals_backward(const double* dL_dnormals, const double* depth,
     return st;
 }
 
+/* ------------------------------------------------------------ losses */
+/* core/src/losses.cpp restated; evaluate_frame_losses (trainer.cpp:171-264). */
+static double sign_of(double v) { return v > 0 ? 1.0 : (v < 0 ? -1.0 : 0.0); }
+
+/* losses.cpp:24-35 */
+static void ssim_window(double* w) {
+    double sum = 0;
+    for (int i = 0; i < 11; ++i) {
+        const double d = i - (11 - 1) / 2.0;
+        w[i] = exp(-d * d / (2.0 * 1.5 * 1.5));
+        sum += w[i];
+    }
+    for (int i = 0; i < 11; ++i) w[i] /= sum;
+}
+
+/* conv_valid (losses.cpp:39-58): along x, then along y; out is (W-10)x(H-10). */
+static void conv_valid(const double* in, int W, int H, const double* w, double* tmp, double* out) {
+    const int Wv = W - 10, Hv = H - 10;
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < Wv; ++x) {
+            double acc = 0;
+            for (int i = 0; i < 11; ++i) acc += w[i] * in[(size_t)y * W + x + i];
+            tmp[(size_t)y * Wv + x] = acc;
+        }
+    for (int y = 0; y < Hv; ++y)
+        for (int x = 0; x < Wv; ++x) {
+            double acc = 0;
+            for (int i = 0; i < 11; ++i) acc += w[i] * tmp[(size_t)(y + i) * Wv + x];
+            out[(size_t)y * Wv + x] = acc;
+        }
+}
+
+/* conv_valid_adjoint (losses.cpp:61-83) */
+static void conv_valid_adjoint(const double* in, int W, int H, const double* w, double* tmp, double* out) {
+    const int Wv = W - 10, Hv = H - 10;
+    memset(out, 0, sizeof(double) * (size_t)W * H);
+    memset(tmp, 0, sizeof(double) * (size_t)W * Hv);
+    for (int y = 0; y < Hv; ++y)
+        for (int x = 0; x < Wv; ++x) {
+            const double v = in[(size_t)y * Wv + x];
+            if (v == 0) continue;
+            for (int i = 0; i < 11; ++i) tmp[(size_t)y * W + x + i] += w[i] * v;
+        }
+    for (int y = 0; y < Hv; ++y)
+        for (int x = 0; x < W; ++x) {
+            const double v = tmp[(size_t)y * W + x];
+            if (v == 0) continue;
+            for (int i = 0; i < 11; ++i) out[(size_t)(y + i) * W + x] += w[i] * v;
+        }
+}
+
+/* ssim_loss (losses.cpp:104-170) on HWC x/y with 3 channels; grad HWC. */
+static double ssim_loss(const double* X, const double* Y, int W, int H, double* grad) {
+    const int C = 3, Wv = W - 10, Hv = H - 10;
+    const size_t n = (size_t)W * H, nv = (size_t)Wv * Hv;
+    const double inv_count = 1.0 / ((double)nv * C), C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+    double w[11];
+    ssim_window(w);
+    double *x = malloc(sizeof(double) * n), *y = malloc(sizeof(double) * n), *xy = malloc(sizeof(double) * n),
+           *x2 = malloc(sizeof(double) * n), *y2 = malloc(sizeof(double) * n), *tmp = malloc(sizeof(double) * n),
+           *mx = malloc(sizeof(double) * nv), *my = malloc(sizeof(double) * nv), *ex2 = malloc(sizeof(double) * nv),
+           *ey2 = malloc(sizeof(double) * nv), *exy = malloc(sizeof(double) * nv), *gm = malloc(sizeof(double) * nv),
+           *g2 = malloc(sizeof(double) * nv), *gxy = malloc(sizeof(double) * nv), *back = malloc(sizeof(double) * n);
+    memset(grad, 0, sizeof(double) * n * C);
+    double ssim_sum = 0;
+    for (int ch = 0; ch < C; ++ch) {
+        for (size_t i = 0; i < n; ++i) {
+            x[i] = X[i * C + ch];
+            y[i] = Y[i * C + ch];
+            xy[i] = x[i] * y[i];
+            x2[i] = x[i] * x[i];
+            y2[i] = y[i] * y[i];
+        }
+        conv_valid(x, W, H, w, tmp, mx);
+        conv_valid(y, W, H, w, tmp, my);
+        conv_valid(x2, W, H, w, tmp, ex2);
+        conv_valid(y2, W, H, w, tmp, ey2);
+        conv_valid(xy, W, H, w, tmp, exy);
+        for (size_t i = 0; i < nv; ++i) {
+            const double a_ = mx[i], b_ = my[i];
+            const double sx = ex2[i] - a_ * a_, sy = ey2[i] - b_ * b_, sxy = exy[i] - a_ * b_;
+            const double a1 = 2 * a_ * b_ + C1, a2 = 2 * sxy + C2;
+            const double b1 = a_ * a_ + b_ * b_ + C1, b2 = sx + sy + C2;
+            const double s = (a1 * a2) / (b1 * b2);
+            ssim_sum += s;
+            const double dS = -inv_count;
+            gm[i] = dS * (2 * b_ * (a2 - a1) / (b1 * b2) - 2 * a_ * s * (1 / b1 - 1 / b2));
+            g2[i] = dS * (-s / b2);
+            gxy[i] = dS * (2 * a1 / (b1 * b2));
+        }
+        conv_valid_adjoint(gm, W, H, w, tmp, back);
+        for (size_t i = 0; i < n; ++i) grad[i * C + ch] += back[i];
+        conv_valid_adjoint(g2, W, H, w, tmp, back);
+        for (size_t i = 0; i < n; ++i) grad[i * C + ch] += 2 * x[i] * back[i];
+        conv_valid_adjoint(gxy, W, H, w, tmp, back);
+        for (size_t i = 0; i < n; ++i) grad[i * C + ch] += y[i] * back[i];
+    }
+    free(x); free(y); free(xy); free(x2); free(y2); free(tmp); free(mx); free(my); free(ex2); free(ey2);
+    free(exy); free(gm); free(g2); free(gxy); free(back);
+    return 1.0 - ssim_sum * inv_count;
+}
+
+int mo_frame_losses(int W, int H, int C, const mo_camera* camera, const mo_normal_cfg* ncfg,
+                    const double* color, const double* depth, const double* semantics, const double* kmap,
+                    const double* transmittance, const double* gt_rgb, const double* gt_depth,
+                    const double* gt_normal, const uint8_t* gt_labels, const double* lambdas, double* report,
+                    double* dcolor, double* ddepth, double* dsemantics, double* dkmap, double* normals_out) {
+    cam_t c;
+    int st = make_cam(camera, &c);
+    if (st) return st;
+    const size_t n = (size_t)W * H;
+    double* normals = calloc(3 * n, sizeof(double));
+    nstate_t ns;
+    memset(&ns, 0, sizeof ns);
+    st = estimate_normals(depth, transmittance, &c, ncfg, normals, &ns);  /* trainer.cpp:296-297 */
+    if (normals_out && !st) memcpy(normals_out, normals, sizeof(double) * 3 * n);
+    double* gssim = NULL;
+    double* gnorm = NULL;
+    double v[6] = {0, 0, 0, 0, 0, 0}; /* l1, ssim, normal, depth, seg, k (lambda order) */
+    double cnt_depth = 0, cnt_normal = 0;
+#define EN(i) (lambdas[i] > 0)
+    if (!st && (EN(0) || EN(1)) && !gt_rgb)
+        st = fail(2, "rgb loss enabled but the frame has no rgb ground truth (<missing>)");
+    if (!st && EN(2) && !gt_normal)
+        st = fail(2, "normal loss enabled but the frame has no normal ground truth (<missing>)");
+    if (!st && EN(3) && !gt_depth)
+        st = fail(2, "depth loss enabled but the frame has no depth ground truth (<missing>)");
+    if (!st && EN(4) && !gt_labels)
+        st = fail(2, "segmentation loss enabled but the frame has no label ground truth (<missing>)");
+    if (!st && EN(1) && (W < 11 || H < 11)) st = fail(1, "ssim_loss: frame smaller than the 11x11 window");
+    if (!st && EN(4) && C < 1) st = fail(1, "cross_entropy_seg: no semantic channels");
+    if (!st && EN(4))
+        for (size_t p = 0; p < n && !st; ++p)
+            if (gt_labels[p] >= C)
+                st = fail(1, "cross_entropy_seg: label %d out of range at pixel (%d,%d)", (int)gt_labels[p],
+                          (int)(p % W), (int)(p / W));
+    if (!st) {
+        if (EN(0)) { /* l1_rgb (losses.cpp:87-102) */
+            double sum = 0;
+            for (size_t i = 0; i < 3 * n; ++i) sum += fabs(color[i] - gt_rgb[i]);
+            v[0] = sum / (double)(3 * n);
+        }
+        if (EN(1)) {
+            gssim = malloc(sizeof(double) * 3 * n);
+            v[1] = ssim_loss(color, gt_rgb, W, H, gssim);
+        }
+        if (EN(2)) { /* normal_cosine (losses.cpp:198-222) over valid && gt != 0 */
+            gnorm = calloc(3 * n, sizeof(double));
+            double dot = 0;
+            for (size_t p = 0; p < n; ++p) {
+                const int ok = ns.valid[p] && (gt_normal[3 * p] != 0 || gt_normal[3 * p + 1] != 0 || gt_normal[3 * p + 2] != 0);
+                if (ok) cnt_normal += 1;
+            }
+            if (cnt_normal > 0) {
+                for (size_t p = 0; p < n; ++p) {
+                    const int ok = ns.valid[p] && (gt_normal[3 * p] != 0 || gt_normal[3 * p + 1] != 0 || gt_normal[3 * p + 2] != 0);
+                    if (!ok) continue;
+                    for (int ch = 0; ch < 3; ++ch) {
+                        dot += normals[3 * p + ch] * gt_normal[3 * p + ch];
+                        gnorm[3 * p + ch] = -gt_normal[3 * p + ch] / cnt_normal;
+                    }
+                }
+                v[2] = 1.0 - dot / cnt_normal;
+            }
+        }
+        if (EN(3)) { /* depth_l1 (losses.cpp:172-196) over gt > 0 */
+            double sum = 0;
+            for (size_t p = 0; p < n; ++p) if (gt_depth[p] > 0) cnt_depth += 1;
+            if (cnt_depth > 0) {
+                for (size_t p = 0; p < n; ++p)
+                    if (gt_depth[p] > 0) sum += fabs(depth[p] - gt_depth[p]);
+                v[3] = sum / cnt_depth;
+            }
+        }
+        if (EN(4)) { /* cross_entropy_seg (losses.cpp:224-267), all pixels */
+            double sum = 0;
+            for (size_t p = 0; p < n; ++p) {
+                const double* l = semantics + p * C;
+                double mx = l[0];
+                for (int ch = 1; ch < C; ++ch) mx = l[ch] > mx ? l[ch] : mx;
+                double z = 0;
+                for (int ch = 0; ch < C; ++ch) z += exp(l[ch] - mx);
+                sum += log(z) - (l[gt_labels[p]] - mx);
+            }
+            v[4] = sum / (double)n;
+        }
+        if (EN(5)) { /* gradient_factor_loss (losses.cpp:269-283) */
+            double sum = 0;
+            for (size_t p = 0; p < n; ++p) sum += fabs(kmap[p] - 1.0);
+            v[5] = sum / (double)n;
+        }
+        /* combine (losses.cpp:285-313); report in LossReport order */
+        const double l1 = v[0], ssim = v[1], normal = v[2], dep = v[3], seg = v[4], kk = v[5];
+        const double mag = fabs(l1);
+#define RATIO(x) (fabs(x) < 1e-12 ? 0.0 : mag / fabs(x))
+        double r[18];
+        r[0] = l1; r[1] = ssim; r[2] = dep; r[3] = normal; r[4] = seg; r[5] = kk;
+        r[7] = RATIO(ssim); r[8] = RATIO(normal); r[9] = RATIO(dep); r[10] = RATIO(seg); r[11] = RATIO(kk);
+#undef RATIO
+        r[12] = lambdas[0];
+        r[13] = lambdas[1] * r[7];
+        r[15] = lambdas[2] * r[8];
+        r[14] = lambdas[3] * r[9];
+        r[16] = lambdas[4] * r[10];
+        r[17] = lambdas[5] * r[11];
+        r[6] = lambdas[0] * l1 + r[13] * ssim + r[15] * normal + r[14] * dep + r[16] * seg + r[17] * kk;
+        if (report) memcpy(report, r, sizeof r);
+        /* seed assembly (trainer.cpp:229-262) */
+        memset(dcolor, 0, sizeof(double) * 3 * n);
+        memset(ddepth, 0, sizeof(double) * n);
+        if (dsemantics && C > 0) memset(dsemantics, 0, sizeof(double) * n * C);
+        memset(dkmap, 0, sizeof(double) * n);
+        if (EN(0))
+            for (size_t i = 0; i < 3 * n; ++i) dcolor[i] += r[12] * (sign_of(color[i] - gt_rgb[i]) / (double)(3 * n));
+        if (EN(1) && r[13] != 0)
+            for (size_t i = 0; i < 3 * n; ++i) dcolor[i] += r[13] * gssim[i];
+        if (EN(3) && r[14] != 0 && cnt_depth > 0)
+            for (size_t p = 0; p < n; ++p)
+                if (gt_depth[p] > 0) ddepth[p] += r[14] * (sign_of(depth[p] - gt_depth[p]) / cnt_depth);
+        if (EN(4) && r[16] != 0)
+            for (size_t p = 0; p < n; ++p) {
+                const double* l = semantics + p * C;
+                double mx = l[0];
+                for (int ch = 1; ch < C; ++ch) mx = l[ch] > mx ? l[ch] : mx;
+                double z = 0;
+                for (int ch = 0; ch < C; ++ch) z += exp(l[ch] - mx);
+                for (int ch = 0; ch < C; ++ch)
+                    dsemantics[p * C + ch] += r[16] * ((exp(l[ch] - mx) / z - (ch == gt_labels[p] ? 1.0 : 0.0)) / (double)n);
+            }
+        if (EN(5) && r[17] != 0)
+            for (size_t p = 0; p < n; ++p) dkmap[p] += r[17] * (sign_of(kmap[p] - 1.0) / (double)n);
+        if (EN(2) && r[15] != 0) {
+            double* dD = malloc(sizeof(double) * n);
+            normals_backward(gnorm, &ns, &c, ncfg, dD);
+            for (size_t p = 0; p < n; ++p) ddepth[p] += r[15] * dD[p];
+            free(dD);
+        }
+    }
+#undef EN
+    free(gssim);
+    free(gnorm);
+    free(normals);
+    free_nstate(&ns);
+    return st;
+}
+
 /* ------------------------------------------------------------ backward */
 static void zero_grads(const mo_scene* S, mo_grads* g) {
     const int64_t n = S->n;

@@ -120,6 +120,19 @@ int mo_fwd_bwd(const mo_scene* s, const mo_camera* cam, const mo_render_cfg* cfg
                double* color, double* depth, double* semantics, double* kmap,
                double* transmittance, double* normals, mo_grads* out, double* ms_out);
 
+/* evaluate_frame_losses (trainer.cpp:171-264) on a rendered frame: normals are
+ * estimated from depth/T first (estimate_normals), exactly as the trainer does,
+ * then l1_rgb, ssim_loss, normal_cosine, depth_l1, cross_entropy_seg,
+ * gradient_factor_loss and combine (losses.cpp).  All maps HWC; ground truth
+ * NULL = absent; lambdas[6] = (l1, ssim, normal, depth, seg, k).  report[18] in
+ * LossReport order; pixel gradients HWC (dsemantics may be NULL when C = 0);
+ * normals_out (optional) receives the estimated normals. */
+int mo_frame_losses(int width, int height, int num_classes, const mo_camera* cam, const mo_normal_cfg* ncfg,
+                    const double* color, const double* depth, const double* semantics, const double* kmap,
+                    const double* transmittance, const double* gt_rgb, const double* gt_depth,
+                    const double* gt_normal, const uint8_t* gt_labels, const double* lambdas, double* report,
+                    double* dcolor, double* ddepth, double* dsemantics, double* dkmap, double* normals_out);
+
 /* Adam on raw parameters (trainer.cpp:90-133).  params/grads/m/v share the
  * scene layout; lr[7] = position, rotation, scale, opacity, sh, semantics, k. */
 int mo_adam(int64_t n, int num_classes, int sh_degree, double* means, double* quats,

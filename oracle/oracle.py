@@ -185,6 +185,34 @@ class Oracle:
                                                  ct.byref(self.normal_cfg(ncfg)), _p(dD)))
         return dD
 
+    LOSS_FIELDS = ("l1", "ssim", "depth", "normal", "seg", "k", "combined", "ratio_ssim", "ratio_normal",
+                   "ratio_depth", "ratio_seg", "ratio_k", "seed_l1", "seed_ssim", "seed_depth", "seed_normal",
+                   "seed_seg", "seed_k")
+
+    def frame_losses(self, frame, gt, cam, lambdas, ncfg=None):
+        """evaluate_frame_losses (trainer.cpp:171-264) after estimate_normals on
+        the frame's depth/T.  frame: HWC color/depth/semantics/kmap/transmittance;
+        gt: dict with optional rgb/depth/normal (HWC) and labels (uint8 HxW).
+        Returns (report dict, pixel-gradient dict HWC, normals HWC)."""
+        W, H = int(cam["width"]), int(cam["height"])
+        C = int(frame["semantics"].shape[2]) if frame["semantics"].ndim == 3 else 0
+        f = {k: _f64(frame[k]) for k in ("color", "depth", "kmap", "transmittance")}
+        sem = _f64(frame["semantics"]) if C else None
+        g = {k: (_f64(gt[k]) if gt.get(k) is not None else None) for k in ("rgb", "depth", "normal")}
+        labels = np.ascontiguousarray(gt["labels"], np.uint8) if gt.get("labels") is not None else None
+        rep = np.zeros(18)
+        out = {"dcolor": np.zeros((H, W, 3)), "ddepth": np.zeros((H, W)), "dsemantics": np.zeros((H, W, C)),
+               "dkmap": np.zeros((H, W))}
+        nrm = np.zeros((H, W, 3))
+        lam = np.asarray(lambdas, np.float64)
+        pn = lambda a: _p(a) if a is not None else None  # noqa: E731
+        self._check(self.lib.mo_frame_losses(
+            W, H, C, ct.byref(self.camera(cam)), ct.byref(self.normal_cfg(ncfg)), _p(f["color"]), _p(f["depth"]),
+            pn(sem), _p(f["kmap"]), _p(f["transmittance"]), pn(g["rgb"]), pn(g["depth"]), pn(g["normal"]),
+            _p(labels, _u8p) if labels is not None else None, _p(lam), _p(rep), _p(out["dcolor"]),
+            _p(out["ddepth"]), _p(out["dsemantics"]) if C else None, _p(out["dkmap"]), _p(nrm)))
+        return dict(zip(self.LOSS_FIELDS, rep.tolist())), out, nrm
+
     def backward(self, s, cam, pix, cfg=None, threads=1):
         sc, keep = self.scene(s)
         K = (int(s["sh_degree"]) + 1) ** 2

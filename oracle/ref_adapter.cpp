@@ -459,3 +459,54 @@ int64_t mo_prune_mask(int64_t n, const double* k, double threshold, int keep_sma
 }
 
 } // extern "C"
+
+// evaluate_frame_losses (core/src/trainer.cpp:171-264) on a given frame, with
+// the normals estimated first as train() does (trainer.cpp:296-297).
+extern "C" int mo_frame_losses(int W, int H, int C, const mo_camera* cam, const mo_normal_cfg* ncfg,
+                               const double* color, const double* depth, const double* semantics,
+                               const double* kmap, const double* transmittance, const double* gt_rgb,
+                               const double* gt_depth, const double* gt_normal, const uint8_t* gt_labels,
+                               const double* lambdas, double* report, double* dcolor, double* ddepth,
+                               double* dsemantics, double* dkmap, double* normals_out) {
+    return guarded([&] {
+        const CameraView view = to_camera(cam);
+        MultimodalFrame f;
+        f.width = W;
+        f.height = H;
+        f.num_classes = C;
+        f.color = grid_from(color, W, H, 3);
+        f.depth = grid_from(depth, W, H, 1);
+        f.semantics = C ? grid_from(semantics, W, H, C) : GridF(W, H, 0, 0.0);
+        f.kmap = grid_from(kmap, W, H, 1);
+        f.transmittance = grid_from(transmittance, W, H, 1);
+        const NormalState ns = estimate_normals(f.depth, f.transmittance, view, to_ncfg(ncfg), f.normals);
+        if (normals_out)
+            grid_to(f.normals, normals_out);
+        FrameRecord gt;
+        if (gt_rgb)
+            gt.rgb = grid_from(gt_rgb, W, H, 3);
+        if (gt_depth)
+            gt.depth = grid_from(gt_depth, W, H, 1);
+        if (gt_normal)
+            gt.normal = grid_from(gt_normal, W, H, 3);
+        if (gt_labels) {
+            gt.labels = GridU8(W, H, 1, 0);
+            std::memcpy(gt.labels.data(), gt_labels, size_t(W) * H);
+        }
+        TrainConfig cfg;
+        for (int i = 0; i < 6; ++i)
+            cfg.lambdas[size_t(i)] = lambdas[i];
+        const FrameLossResult r = evaluate_frame_losses(f, ns, gt, view, cfg);
+        const LossReport& q = r.report;
+        const double rep[18] = {q.l1, q.ssim, q.depth, q.normal, q.seg, q.k, q.combined, q.ratio_ssim,
+                                q.ratio_normal, q.ratio_depth, q.ratio_seg, q.ratio_k, q.seed_l1, q.seed_ssim,
+                                q.seed_depth, q.seed_normal, q.seed_seg, q.seed_k};
+        if (report)
+            std::memcpy(report, rep, sizeof rep);
+        grid_to(r.pixel_grads.dcolor, dcolor);
+        grid_to(r.pixel_grads.ddepth, ddepth);
+        if (C && dsemantics)
+            grid_to(r.pixel_grads.dsemantics, dsemantics);
+        grid_to(r.pixel_grads.dkmap, dkmap);
+    });
+}

@@ -71,6 +71,19 @@ class MsplatCounters(ct.Structure):
                 ("tiles", ct.c_int64), ("max_tile_list", ct.c_int64)]
 
 
+class MsplatGroundTruth(ct.Structure):
+    _fields_ = [("rgb", _vp), ("depth", _vp), ("normal", _vp), ("labels", _vp)]
+
+
+LOSS_REPORT_FIELDS = ("l1", "ssim", "depth", "normal", "seg", "k", "combined", "ratio_ssim", "ratio_normal",
+                      "ratio_depth", "ratio_seg", "ratio_k", "seed_l1", "seed_ssim", "seed_depth", "seed_normal",
+                      "seed_seg", "seed_k")
+
+
+class MsplatLossReport(ct.Structure):
+    _fields_ = [(f, ct.c_double) for f in LOSS_REPORT_FIELDS]
+
+
 class LogicError(RuntimeError):
     """std::logic_error of the reference (e.g. chaining an already-raw buffer)."""
 
@@ -113,6 +126,10 @@ def _sig(lib):
                                                 P(_i64), P(ct.c_int32), _i64, P(_i64)]),
         ("msplat_context_set_timing", ct.c_int, [_vp, ct.c_int]),
         ("msplat_context_set_deterministic", ct.c_int, [_vp, ct.c_int]),
+        ("msplat_frame_losses", ct.c_int, [_vp, ct.c_int, ct.c_int, P(MsplatCamera), P(MsplatNormalConfig),
+                                           P(MsplatFrame), P(MsplatGroundTruth), P(ct.c_double),
+                                           P(MsplatPixelGrads), P(MsplatLossReport)]),
+        ("msplat_loss_report_device", _vp, [_vp]),
         ("msplat_context_timings", ct.c_int, [_vp, P(ct.c_double), P(_i64)]),
         ("msplat_kernel_launches", _i64, []),
     ]

@@ -144,6 +144,8 @@ struct msplat_context {
     unsigned long long* h_u64 = nullptr;  // pinned scratch
     // scratch owned by the context (shared by calls on its stream)
     DevBuf acc_dcolor, acc16, ddepth_total, normal_dv, kept;
+    // frame losses (msplat_frame_losses)
+    DevBuf loss_acc, loss_report, ssim_maps, ssim_grad, loss_dN;
     // deterministic backward (msplat_context_set_deterministic)
     int deterministic = 0;
     DevBuf det_partial, det_keys, det_keys_alt, det_vals, det_vals_alt, det_range;
@@ -269,6 +271,10 @@ msplat_status drain_device_error(msplat_context* ctx, int W) {
         case kErrInstanceOverflow:
             snprintf(buf, sizeof buf, "internal: tile-instance capacity %lld exceeded (needed %lld)", e.b, e.a);
             return set_error(MSPLAT_ERR_RUNTIME, buf);
+        case kErrLabelRange:
+            snprintf(buf, sizeof buf, "cross_entropy_seg: label %lld out of range at pixel (%lld,%lld)", e.b, e.a % w,
+                     e.a / w);
+            return set_error(MSPLAT_ERR_INVALID_ARGUMENT, buf);
         default:
             snprintf(buf, sizeof buf, "device error %d", e.code);
             return set_error(MSPLAT_ERR_RUNTIME, buf);
@@ -620,6 +626,66 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
 }  // namespace
 
 // =====================================================================  ABI
+namespace {
+
+template <typename Real>
+msplat_status frame_losses_impl(msplat_context* ctx, int C, const Cam& cam, const msplat_normal_config* ncfg,
+                                const msplat_frame* f, const msplat_ground_truth* gt, const double lambdas[6],
+                                msplat_pixel_grads* out) {
+    const size_t HW = size_t(cam.W) * cam.H, R = sizeof(Real);
+    LossArgs<Real> a{};
+    a.W = cam.W;
+    a.H = cam.H;
+    a.C = C;
+    for (int i = 0; i < 6; ++i) {
+        a.lambdas[i] = lambdas[i];
+        a.en[i] = lambdas[i] > 0;
+    }
+    // losses.cpp:24-35: normalised Gaussian window, sigma 1.5
+    double wsum = 0;
+    for (int i = 0; i < 11; ++i) {
+        const double d = i - 5.0;
+        a.ssim_w[i] = std::exp(-d * d / (2.0 * 1.5 * 1.5));
+        wsum += a.ssim_w[i];
+    }
+    for (int i = 0; i < 11; ++i) a.ssim_w[i] /= wsum;
+    const size_t nv = a.en[1] ? size_t(cam.W - 10) * (cam.H - 10) : 0;
+    a.ssim_inv_count = a.en[1] ? 1.0 / (double(nv) * 3) : 0;
+    a.color = static_cast<const Real*>(f->color);
+    a.depth = static_cast<const Real*>(f->depth);
+    a.sem = static_cast<const Real*>(f->semantics);
+    a.kmap = static_cast<const Real*>(f->kmap);
+    a.normals = static_cast<const Real*>(f->normals);
+    a.gt_rgb = static_cast<const Real*>(gt->rgb);
+    a.gt_depth = static_cast<const Real*>(gt->depth);
+    a.gt_normal = static_cast<const Real*>(gt->normal);
+    a.labels = gt->labels;
+    CUDA_TRY(ctx->loss_acc.ensure(8 * sizeof(double)));
+    CUDA_TRY(ctx->loss_report.ensure(20 * sizeof(double)));
+    a.acc = ctx->loss_acc.as<double>();
+    a.report = ctx->loss_report.as<double>();
+    if (a.en[1]) {
+        CUDA_TRY(ctx->ssim_maps.ensure(9 * nv * R));
+        CUDA_TRY(ctx->ssim_grad.ensure(3 * HW * R));
+        a.ssim_maps = ctx->ssim_maps.as<Real>();
+        a.ssim_grad = ctx->ssim_grad.as<Real>();
+    }
+    a.dcolor = static_cast<Real*>(const_cast<void*>(out->dcolor));
+    a.ddepth = static_cast<Real*>(const_cast<void*>(out->ddepth));
+    a.dsem = C > 0 ? static_cast<Real*>(const_cast<void*>(out->dsemantics)) : nullptr;
+    a.dkmap = static_cast<Real*>(const_cast<void*>(out->dkmap));
+    if (a.en[2]) {
+        CUDA_TRY(ctx->loss_dN.ensure(3 * HW * R));
+        a.dN = ctx->loss_dN.as<Real>();
+    }
+    a.err = ctx->d_err;
+    launch_frame_losses<Real>(a, ctx->stream);
+    CUDA_TRY(cudaGetLastError());
+    return MSPLAT_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* msplat_last_error(void) { return g_error.c_str(); }
@@ -652,7 +718,8 @@ msplat_status msplat_context_create(int device, void* cuda_stream, msplat_contex
 void msplat_context_destroy(msplat_context* ctx) {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->stream);
-    for (DevBuf* b : {&ctx->acc_dcolor, &ctx->acc16, &ctx->ddepth_total, &ctx->normal_dv,
+    for (DevBuf* b : {&ctx->acc_dcolor, &ctx->acc16, &ctx->loss_acc, &ctx->loss_report, &ctx->ssim_maps, &ctx->ssim_grad, &ctx->loss_dN,
+                       &ctx->ddepth_total, &ctx->normal_dv,
                       &ctx->kept})
         b->release();
     cudaFree(ctx->d_err);
@@ -895,6 +962,57 @@ msplat_status msplat_context_set_timing(msplat_context* ctx, int enable) {
     if (!ctx) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null context");
     ctx->timer.enabled = enable != 0;
     return MSPLAT_OK;
+}
+
+msplat_status msplat_frame_losses(msplat_context* ctx, int dtype, int num_classes, const msplat_camera* camera,
+                                  const msplat_normal_config* ncfg, const msplat_frame* frame,
+                                  const msplat_ground_truth* gt, const double lambdas[6], msplat_pixel_grads* out,
+                                  msplat_loss_report* host_report) {
+    if (!ctx || !frame || !gt || !lambdas || !out) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "frame_losses: null argument");
+    if (dtype != MSPLAT_F32 && dtype != MSPLAT_F64)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "frame_losses: dtype must be MSPLAT_F32 or MSPLAT_F64");
+    Cam c;
+    msplat_status st = make_cam(camera, c);
+    if (st != MSPLAT_OK) return st;
+    if ((st = check_ncfg(ncfg)) != MSPLAT_OK) return st;
+    // trainer.cpp:181-224: an enabled modality needs its ground truth
+    if ((lambdas[0] > 0 || lambdas[1] > 0) && !gt->rgb)
+        return set_error(MSPLAT_ERR_RUNTIME, "rgb loss enabled but the frame has no rgb ground truth (<missing>)");
+    if (lambdas[2] > 0 && !gt->normal)
+        return set_error(MSPLAT_ERR_RUNTIME, "normal loss enabled but the frame has no normal ground truth (<missing>)");
+    if (lambdas[3] > 0 && !gt->depth)
+        return set_error(MSPLAT_ERR_RUNTIME, "depth loss enabled but the frame has no depth ground truth (<missing>)");
+    if (lambdas[4] > 0 && !gt->labels)
+        return set_error(MSPLAT_ERR_RUNTIME,
+                         "segmentation loss enabled but the frame has no label ground truth (<missing>)");
+    if (lambdas[1] > 0 && (c.W < 11 || c.H < 11))
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "ssim_loss: frame smaller than the 11x11 window");
+    if (lambdas[4] > 0 && num_classes < 1)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "cross_entropy_seg: no semantic channels");
+    if (!frame->color || !frame->depth || !frame->kmap || !frame->transmittance ||
+        (lambdas[2] > 0 && !frame->normals) || (num_classes > 0 && !frame->semantics) || !out->dcolor ||
+        !out->ddepth || !out->dkmap || (num_classes > 0 && !out->dsemantics))
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "frame_losses: missing frame or gradient buffer");
+    st = dtype == MSPLAT_F64 ? frame_losses_impl<double>(ctx, num_classes, c, ncfg, frame, gt, lambdas, out)
+                             : frame_losses_impl<float>(ctx, num_classes, c, ncfg, frame, gt, lambdas, out);
+    if (st != MSPLAT_OK) return st;
+    // The normal term reaches the Gaussians through the depth map
+    // (trainer.cpp:258-262): dD += normals_backward(seed_normal * dL/dN).
+    if (lambdas[2] > 0) {
+        st = msplat_normals_backward(ctx, dtype, ctx->loss_dN.p, frame->depth, frame->transmittance, camera, ncfg, 1.0,
+                                     const_cast<void*>(out->ddepth));
+        if (st != MSPLAT_OK) return st;
+    }
+    if (host_report) {
+        CUDA_TRY(cudaMemcpyAsync(host_report, ctx->loss_report.p, sizeof(msplat_loss_report), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        return drain_device_error(ctx, c.W);
+    }
+    return MSPLAT_OK;
+}
+
+const double* msplat_loss_report_device(msplat_context* ctx) {
+    return ctx ? static_cast<const double*>(ctx->loss_report.p) : nullptr;
 }
 
 msplat_status msplat_context_set_deterministic(msplat_context* ctx, int enable) {

@@ -25,6 +25,7 @@ enum ErrCode : int {
     kErrZeroQuat = 5,          // scene.cpp:49-51 (b = primitive)
     kErrNonFiniteParam = 6,    // scene.cpp:36-38 (b = primitive)
     kErrInstanceOverflow = 7,  // internal: tile-instance buffer too small (a = needed)
+    kErrLabelRange = 8,        // losses.cpp:245-249 (a = pixel, b = label)
 };
 
 struct DeviceError {

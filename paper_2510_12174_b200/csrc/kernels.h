@@ -105,6 +105,27 @@ struct ForwardArgs {
 template <typename Real>
 void launch_forward(const ForwardArgs<Real>& a, int ntiles, cudaStream_t s);
 
+// K12: frame losses + seed assembly (core/src/trainer.cpp:171-264, losses.cpp).
+template <typename Real>
+struct LossArgs {
+    int W, H, C;
+    int en[6];          // lambda > 0, order (l1, ssim, normal, depth, seg, k)
+    double lambdas[6];
+    double ssim_w[11];  // normalised Gaussian window (losses.cpp:24-35)
+    double ssim_inv_count;
+    const Real *color, *depth, *sem, *kmap, *normals;  // rendered frame, planar
+    const Real *gt_rgb, *gt_depth, *gt_normal;         // ground truth, planar
+    const uint8_t* labels;
+    double* acc;        // [8] reduced sums / counts
+    double* report;     // [20] msplat_loss_report + 2 counts
+    Real* ssim_maps;    // [3 maps][3][Hv][Wv]
+    Real* ssim_grad;    // [3][H][W]
+    Real *dcolor, *ddepth, *dsem, *dkmap, *dN;  // outputs (dN: seeded normal-loss gradient)
+    DeviceError* err;
+};
+template <typename Real>
+void launch_frame_losses(const LossArgs<Real>& a, cudaStream_t s);
+
 // Normals (K7, K8).
 template <typename Real>
 struct NormalArgs {

@@ -35,7 +35,7 @@ __all__ = [
     "MultimodalFrame", "ReplayState", "PixelGradients", "GradientBuffer", "TileBins",
     "OptimizerState", "TrainConfig", "rasterize", "rasterize_backward", "estimate_normals",
     "normals_backward", "chain_activations", "adam_step", "prune", "bin_and_sort", "fwd_bwd",
-    "LogicError", "param_layout",
+    "LogicError", "param_layout", "GroundTruth", "LossReport", "frame_losses",
 ]
 
 
@@ -443,6 +443,70 @@ def normals_backward(dL_dnormals: torch.Tensor, depth: torch.Tensor, transmittan
                                              ct.byref(view._abi()), ct.byref(ncfg._abi()), 1.0,
                                              dD.data_ptr()))
     return dD
+
+
+# ----------------------------------------------------------------- losses
+@dataclass
+class GroundTruth:
+    """The supervision of one frame (dataset.hpp FrameRecord), planar device
+    tensors in the frame's dtype; None = modality absent."""
+    rgb: torch.Tensor | None = None       # [3, H, W]
+    depth: torch.Tensor | None = None     # [H, W], pixels with depth > 0 supervised
+    normal: torch.Tensor | None = None    # [3, H, W], non-zero normals supervised
+    labels: torch.Tensor | None = None    # [H, W] uint8 class ids
+
+    def _abi(self):
+        p = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        if self.labels is not None and self.labels.dtype != torch.uint8:
+            raise ValueError("GroundTruth: labels must be uint8")
+        return _lib.MsplatGroundTruth(p(self.rgb), p(self.depth), p(self.normal), p(self.labels))
+
+
+@dataclass
+class LossReport:
+    """msplat::LossReport (losses.hpp:40-50)."""
+    l1: float = 0.0
+    ssim: float = 0.0
+    depth: float = 0.0
+    normal: float = 0.0
+    seg: float = 0.0
+    k: float = 0.0
+    combined: float = 0.0
+    ratio_ssim: float = 0.0
+    ratio_normal: float = 0.0
+    ratio_depth: float = 0.0
+    ratio_seg: float = 0.0
+    ratio_k: float = 0.0
+    seed_l1: float = 0.0
+    seed_ssim: float = 0.0
+    seed_depth: float = 0.0
+    seed_normal: float = 0.0
+    seed_seg: float = 0.0
+    seed_k: float = 0.0
+
+
+def frame_losses(frame: MultimodalFrame, gt: GroundTruth, view: CameraView, ncfg: NormalConfig,
+                 lambdas=(1.0, 0.1, 0.1, 0.1, 0.1, 0.1), out: PixelGradients | None = None,
+                 sync: bool = True):
+    """evaluate_frame_losses (trainer.cpp:171-264) on the device.
+
+    `frame.normals` must come from estimate_normals (a non-zero normal marks a
+    valid pixel).  lambdas = (l1, ssim, normal, depth, seg, k).  Returns
+    (LossReport, PixelGradients); the normal term is already pushed through
+    normals_backward into ddepth.  sync=False keeps the report on the device
+    (LossReport is then None) -- the call is graph-capturable."""
+    dev = frame.color.device
+    if out is None:
+        out = PixelGradients.zero(frame.width, frame.height, frame.num_classes, frame.color.dtype, dev)
+    ctx = _Context.get(dev.index)
+    lam = (ct.c_double * 6)(*[float(x) for x in lambdas])
+    rep = _lib.MsplatLossReport()
+    check(_lib.lib().msplat_frame_losses(ctx.h, _dtype_code(frame.color.dtype), frame.num_classes,
+                                         ct.byref(view._abi()), ct.byref(ncfg._abi()), ct.byref(frame._abi()),
+                                         ct.byref(gt._abi()), lam, ct.byref(out._abi()),
+                                         ct.byref(rep) if sync else None))
+    report = LossReport(**{f: getattr(rep, f) for f in _lib.LOSS_REPORT_FIELDS}) if sync else None
+    return report, out
 
 
 def rasterize_backward(scene: Scene, view: CameraView, frame: MultimodalFrame, replay: ReplayState,
