@@ -277,6 +277,23 @@ MSPLAT_API msplat_status msplat_prune_mask(msplat_context* ctx, int dtype, int64
                                 double threshold, int keep_small, uint8_t* keep_device,
                                 int64_t* kept);
 
+/* init_scene(points, colors, C, cfg)  (core/src/trainer.cpp:42-86) into a packed
+ * parameter buffer (msplat_param_layout order, `dtype`): one Gaussian per
+ * point, identity rotation, opacity 0.1, DC colour, zero semantics, k = k_reset,
+ * isotropic scale from the mean distance to the three nearest neighbours
+ * (device search, exact FP64).  points/colors: HOST [n][3]; synchronizing. */
+MSPLAT_API msplat_status msplat_init_scene(msplat_context* ctx, int dtype, int64_t n, const double* points,
+                                const double* colors, int num_classes, int sh_degree, double k_reset,
+                                void* params);
+
+/* prune() compaction (core/src/trainer.cpp:150-168): with the keep mask of
+ * msplat_prune_mask (kept survivors), stably compacts up to three packed
+ * buffers in[b] -> out[b] (parameters, Adam m, Adam v; out sized for `kept`;
+ * in[1]/in[2] may be NULL) and resets k := k_reset in out[0]. */
+MSPLAT_API msplat_status msplat_prune_compact(msplat_context* ctx, int dtype, int64_t n, int num_classes,
+                                   int sh_degree, const uint8_t* keep, int64_t kept,
+                                   const void* const in[3], void* const out[3], double k_reset);
+
 /* ------------------------------------------------------ instrumentation */
 /* Stage ids for msplat_context_timings. */
 enum {

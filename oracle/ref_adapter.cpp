@@ -510,3 +510,101 @@ extern "C" int mo_frame_losses(int W, int H, int C, const mo_camera* cam, const 
         grid_to(r.pixel_grads.dkmap, dkmap);
     });
 }
+
+// train (core/src/trainer.cpp:266-331) on flat arrays; the same contract as the
+// drop-in's msplat_train_flat (cfg: 32 doubles, see there; log rows of 21).
+extern "C" int mo_train(int n_points, const double* points, const double* colors, int num_classes, int n_frames,
+                        const mo_camera* cams, const double* rgb, const double* depth, const double* normal,
+                        const uint8_t* labels, const uint8_t* is_test, const double* c, double* params_out,
+                        int64_t* n_out, double* log_out, int* completed, int* halted) {
+    return guarded([&] {
+        SceneDataset ds;
+        ds.num_classes = num_classes;
+        for (int i = 0; i < n_points; ++i) {
+            ds.points.emplace_back(points[3 * i], points[3 * i + 1], points[3 * i + 2]);
+            ds.point_colors.emplace_back(colors[3 * i], colors[3 * i + 1], colors[3 * i + 2]);
+        }
+        size_t o3 = 0, o1 = 0;
+        for (int f = 0; f < n_frames; ++f) {
+            FrameRecord fr;
+            fr.view = to_camera(&cams[f]);
+            fr.split = is_test && is_test[f] ? "test" : "train";
+            const int W = cams[f].width, H = cams[f].height;
+            const size_t HW = size_t(W) * H;
+            fr.rgb = grid_from(rgb + o3, W, H, 3);
+            fr.depth = grid_from(depth + o1, W, H, 1);
+            fr.normal = grid_from(normal + o3, W, H, 3);
+            fr.labels = GridU8(W, H, 1, 0);
+            std::memcpy(fr.labels.data(), labels + o1, HW);
+            o3 += 3 * HW;
+            o1 += HW;
+            ds.frames.push_back(std::move(fr));
+            ds.width = W;
+            ds.height = H;
+        }
+        TrainConfig t;
+        t.iterations = int(c[0]);
+        t.lr_position = c[1];
+        t.lr_rotation = c[2];
+        t.lr_scale = c[3];
+        t.lr_opacity = c[4];
+        t.lr_sh = c[5];
+        t.lr_semantics = c[6];
+        t.lr_k = c[7];
+        for (int i = 0; i < 6; ++i)
+            t.lambdas[size_t(i)] = c[8 + i];
+        t.prune_interval = int(c[14]);
+        t.prune_threshold = c[15];
+        t.prune_enabled = c[16] != 0;
+        t.prune_keep_small = c[17] != 0;
+        t.k_reset = c[18];
+        t.step1 = int(c[19]);
+        t.step2 = int(c[20]);
+        t.lambda_fuse = c[21];
+        t.mask_threshold = c[22];
+        t.sigma_scale = c[23];
+        t.early_stop_transmittance = c[24];
+        t.background = Vec3(c[25], c[26], c[27]);
+        t.sh_degree = int(c[28]);
+        t.seed = uint64_t(c[29]);
+        t.threads = int(c[30]);
+        t.deterministic = c[31] != 0;
+        const TrainResult r = train(ds, t);
+        const Scene& s = r.scene;
+        const int K = s.sh_coeff_count(), C = s.num_classes;
+        const int64_t n = int64_t(s.size());
+        const int64_t sizes[7] = {3, 4, 3, 1, 1, 3 * K, C};
+        int64_t off[8];
+        off[0] = 0;
+        for (int i = 0; i < 7; ++i)
+            off[i + 1] = off[i] + n * sizes[i];
+        for (int64_t i = 0; i < n; ++i) {
+            const GaussianPrimitive& g = s.gaussians[size_t(i)];
+            for (int j = 0; j < 3; ++j) {
+                params_out[off[0] + 3 * i + j] = g.position[j];
+                params_out[off[2] + 3 * i + j] = g.log_scale[j];
+            }
+            for (int j = 0; j < 4; ++j)
+                params_out[off[1] + 4 * i + j] = g.rotation[j];
+            params_out[off[3] + i] = g.opacity_logit;
+            params_out[off[4] + i] = g.gradient_factor;
+            for (int ch = 0; ch < 3; ++ch)
+                for (int j = 0; j < K; ++j)
+                    params_out[off[5] + (3 * i + ch) * K + j] = g.sh(ch, j);
+            for (int ch = 0; ch < C; ++ch)
+                params_out[off[6] + i * C + ch] = g.semantic_logits[ch];
+        }
+        *n_out = n;
+        for (size_t it = 0; it < r.log.size(); ++it) {
+            const IterationLog& e = r.log[it];
+            const LossReport& q = e.losses;
+            const double vals[21] = {double(e.iteration), double(e.view_index), double(e.gaussian_count), q.l1,
+                                     q.ssim, q.depth, q.normal, q.seg, q.k, q.combined, q.ratio_ssim,
+                                     q.ratio_normal, q.ratio_depth, q.ratio_seg, q.ratio_k, q.seed_l1, q.seed_ssim,
+                                     q.seed_depth, q.seed_normal, q.seed_seg, q.seed_k};
+            std::memcpy(log_out + it * 21, vals, sizeof vals);
+        }
+        *completed = r.completed_iterations;
+        *halted = r.halted_non_finite ? 1 : 0;
+    });
+}

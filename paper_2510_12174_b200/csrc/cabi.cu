@@ -146,6 +146,8 @@ struct msplat_context {
     DevBuf acc_dcolor, acc16, ddepth_total, normal_dv, kept;
     // frame losses (msplat_frame_losses)
     DevBuf loss_acc, loss_report, ssim_maps, ssim_grad, loss_dN;
+    // trainer support (msplat_init_scene, msplat_prune_compact)
+    DevBuf init_pts, init_cols, init_logs, cmp_k32, cmp_idx, cmp_tiles, cmp_total;
     // deterministic backward (msplat_context_set_deterministic)
     int deterministic = 0;
     DevBuf det_partial, det_keys, det_keys_alt, det_vals, det_vals_alt, det_range;
@@ -718,7 +720,8 @@ msplat_status msplat_context_create(int device, void* cuda_stream, msplat_contex
 void msplat_context_destroy(msplat_context* ctx) {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->stream);
-    for (DevBuf* b : {&ctx->acc_dcolor, &ctx->acc16, &ctx->loss_acc, &ctx->loss_report, &ctx->ssim_maps, &ctx->ssim_grad, &ctx->loss_dN,
+    for (DevBuf* b : {&ctx->acc_dcolor, &ctx->acc16, &ctx->loss_acc, &ctx->loss_report, &ctx->ssim_maps, &ctx->ssim_grad, &ctx->loss_dN, &ctx->init_pts,
+                       &ctx->init_cols, &ctx->init_logs, &ctx->cmp_k32, &ctx->cmp_idx, &ctx->cmp_tiles, &ctx->cmp_total,
                        &ctx->ddepth_total, &ctx->normal_dv,
                       &ctx->kept})
         b->release();
@@ -1013,6 +1016,64 @@ msplat_status msplat_frame_losses(msplat_context* ctx, int dtype, int num_classe
 
 const double* msplat_loss_report_device(msplat_context* ctx) {
     return ctx ? static_cast<const double*>(ctx->loss_report.p) : nullptr;
+}
+
+msplat_status msplat_init_scene(msplat_context* ctx, int dtype, int64_t n, const double* points, const double* colors,
+                                int num_classes, int sh_degree, double k_reset, void* params) {
+    if (!ctx || !params) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "init_scene: null argument");
+    if (n <= 0 || !points) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "init_scene: empty point list");
+    if (!colors) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "init_scene: point/color count mismatch");
+    if (num_classes < 0 || sh_degree < 0 || sh_degree > 3)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "init_scene: bad class count or SH degree");
+    if (dtype != MSPLAT_F32 && dtype != MSPLAT_F64)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "init_scene: dtype must be MSPLAT_F32 or MSPLAT_F64");
+    const size_t nn = size_t(n);
+    CUDA_TRY(ctx->init_pts.ensure(nn * 3 * 8));
+    CUDA_TRY(ctx->init_cols.ensure(nn * 3 * 8));
+    CUDA_TRY(ctx->init_logs.ensure(nn * 8));
+    CUDA_TRY(cudaMemcpyAsync(ctx->init_pts.p, points, nn * 3 * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(ctx->init_cols.p, colors, nn * 3 * 8, cudaMemcpyHostToDevice, ctx->stream));
+    if (dtype == MSPLAT_F64)
+        launch_init_scene<double>(n, num_classes, sh_degree, ctx->init_pts.as<double>(), ctx->init_cols.as<double>(),
+                                  ctx->init_logs.as<double>(), k_reset, static_cast<double*>(params), ctx->stream);
+    else
+        launch_init_scene<float>(n, num_classes, sh_degree, ctx->init_pts.as<double>(), ctx->init_cols.as<double>(),
+                                 ctx->init_logs.as<double>(), k_reset, static_cast<float*>(params), ctx->stream);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // the host point arrays may be released
+    return MSPLAT_OK;
+}
+
+msplat_status msplat_prune_compact(msplat_context* ctx, int dtype, int64_t n, int num_classes, int sh_degree,
+                                   const uint8_t* keep, int64_t kept, const void* const in[3], void* const out[3],
+                                   double k_reset) {
+    if (!ctx || !keep || !in || !out || !in[0] || !out[0])
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "prune: null argument");
+    if (kept <= 0) return set_error(MSPLAT_ERR_RUNTIME, "prune: every gaussian would be removed");
+    if (kept > n || num_classes < 0 || sh_degree < 0 || sh_degree > 3)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "prune: bad size");
+    const size_t nn = size_t(n);
+    CUDA_TRY(ctx->cmp_k32.ensure(nn * 4));
+    CUDA_TRY(ctx->cmp_idx.ensure(nn * 4));
+    CUDA_TRY(ctx->cmp_tiles.ensure((nn + kScanTile - 1) / kScanTile * 4 + 8));
+    CUDA_TRY(ctx->cmp_total.ensure(8));
+    if (dtype == MSPLAT_F64) {
+        const double* const i3[3] = {static_cast<const double*>(in[0]), static_cast<const double*>(in[1]),
+                                     static_cast<const double*>(in[2])};
+        double* const o3[3] = {static_cast<double*>(out[0]), static_cast<double*>(out[1]), static_cast<double*>(out[2])};
+        launch_prune_compact<double>(n, num_classes, sh_degree, keep, kept, i3, o3, k_reset, ctx->cmp_k32.as<uint32_t>(),
+                                     ctx->cmp_idx.as<uint32_t>(), ctx->cmp_tiles.as<uint32_t>(),
+                                     ctx->cmp_total.as<uint32_t>(), ctx->stream);
+    } else {
+        const float* const i3[3] = {static_cast<const float*>(in[0]), static_cast<const float*>(in[1]),
+                                    static_cast<const float*>(in[2])};
+        float* const o3[3] = {static_cast<float*>(out[0]), static_cast<float*>(out[1]), static_cast<float*>(out[2])};
+        launch_prune_compact<float>(n, num_classes, sh_degree, keep, kept, i3, o3, k_reset, ctx->cmp_k32.as<uint32_t>(),
+                                    ctx->cmp_idx.as<uint32_t>(), ctx->cmp_tiles.as<uint32_t>(),
+                                    ctx->cmp_total.as<uint32_t>(), ctx->stream);
+    }
+    CUDA_TRY(cudaGetLastError());
+    return MSPLAT_OK;
 }
 
 msplat_status msplat_context_set_deterministic(msplat_context* ctx, int enable) {

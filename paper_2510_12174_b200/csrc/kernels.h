@@ -126,6 +126,15 @@ struct LossArgs {
 template <typename Real>
 void launch_frame_losses(const LossArgs<Real>& a, cudaStream_t s);
 
+// K13: trainer support (core/src/trainer.cpp:42-86, 150-168).
+template <typename Real>
+void launch_init_scene(int64_t n, int C, int deg, const double* pts_dev, const double* cols_dev, double* log_scale_dev,
+                       double k_reset, Real* params, cudaStream_t s);
+template <typename Real>
+void launch_prune_compact(int64_t n, int C, int deg, const uint8_t* keep, int64_t kept, const Real* const in[3],
+                          Real* const out[3], double k_reset, uint32_t* k32, uint32_t* newidx, uint32_t* scan_tiles,
+                          uint32_t* d_total, cudaStream_t s);
+
 // Normals (K7, K8).
 template <typename Real>
 struct NormalArgs {
