@@ -277,6 +277,25 @@ MSPLAT_API msplat_status msplat_prune_mask(msplat_context* ctx, int dtype, int64
                                 double threshold, int keep_small, uint8_t* keep_device,
                                 int64_t* kept);
 
+/* MetricReport (msplat/metrics.hpp:12-17) image metrics; has_* = 0 is nullopt. */
+typedef struct {
+    double psnr, ssim, abs_rel, rmse, cos_simi, miou;
+    int has_psnr, has_ssim, has_abs_rel, has_rmse, has_cos_simi, has_miou;
+} msplat_metric_report;
+
+/* Evaluation metrics (core/src/metrics.cpp:68-187) of one frame, planar device
+ * buffers: psnr + ssim_metric (color vs gt_rgb), abs_rel + rmse (depth, masked),
+ * cos_simi (normals, masked), argmax_labels + miou (semantic logits vs labels,
+ * masked).  A metric whose inputs are NULL is skipped (has_* = 0).
+ * Synchronizing (the result is a handful of host scalars). */
+MSPLAT_API msplat_status msplat_frame_metrics(msplat_context* ctx, int dtype, int width, int height,
+                                   int num_classes, const void* color, const void* gt_rgb,
+                                   const void* depth, const void* gt_depth, const uint8_t* depth_mask,
+                                   const void* normals, const void* gt_normal,
+                                   const uint8_t* normal_mask, const void* semantics,
+                                   const uint8_t* gt_labels, const uint8_t* label_mask,
+                                   msplat_metric_report* out);
+
 /* init_scene(points, colors, C, cfg)  (core/src/trainer.cpp:42-86) into a packed
  * parameter buffer (msplat_param_layout order, `dtype`): one Gaussian per
  * point, identity rotation, opacity 0.1, DC colour, zero semantics, k = k_reset,

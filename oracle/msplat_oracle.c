@@ -1097,6 +1097,89 @@ int mo_frame_losses(int W, int H, int C, const mo_camera* camera, const mo_norma
     return st;
 }
 
+/* metrics.cpp:68-187 */
+int mo_metrics(int W, int H, int C, const double* color, const double* gt_rgb, const double* depth,
+               const double* gt_depth, const uint8_t* depth_mask, const double* normals, const double* gt_normal,
+               const uint8_t* normal_mask, const double* semantics, const uint8_t* gt_labels,
+               const uint8_t* label_mask, double* vals, int* has) {
+    const size_t n = (size_t)W * H;
+    for (int i = 0; i < 6; ++i) { vals[i] = 0; has[i] = 0; }
+    if (color && gt_rgb) {
+        if (W < 11 || H < 11) return fail(1, "ssim_loss: frame smaller than the 11x11 window");
+        double mse = 0;
+        for (size_t i = 0; i < 3 * n; ++i) {
+            const double d = color[i] - gt_rgb[i];
+            mse += d * d;
+        }
+        mse /= (double)(3 * n);
+        vals[0] = mse <= 1e-10 ? 100.0 : fmin(100.0, 10.0 * log10(1.0 / mse));
+        has[0] = 1;
+        double* g = malloc(sizeof(double) * 3 * n);
+        vals[1] = 1.0 - ssim_loss(color, gt_rgb, W, H, g);
+        has[1] = 1;
+        free(g);
+    }
+    if (depth && gt_depth && depth_mask) {
+        double sa = 0, sr = 0;
+        size_t ca = 0, cr = 0;
+        for (size_t p = 0; p < n; ++p) {
+            if (!depth_mask[p]) continue;
+            if (gt_depth[p] > 1e-3) {
+                sa += fabs(depth[p] - gt_depth[p]) / gt_depth[p];
+                ++ca;
+            }
+            const double d = depth[p] - gt_depth[p];
+            sr += d * d;
+            ++cr;
+        }
+        if (ca) { vals[2] = sa / (double)ca; has[2] = 1; }
+        if (cr) { vals[3] = sqrt(sr / (double)cr); has[3] = 1; }
+    }
+    if (normals && gt_normal && normal_mask) {
+        double sum = 0;
+        size_t cnt = 0;
+        for (size_t p = 0; p < n; ++p) {
+            if (!normal_mask[p]) continue;
+            for (int ch = 0; ch < 3; ++ch) sum += normals[3 * p + ch] * gt_normal[3 * p + ch];
+            ++cnt;
+        }
+        if (cnt) { vals[4] = sum / (double)cnt; has[4] = 1; }
+    }
+    if (semantics && gt_labels && label_mask && C > 0) {
+        size_t* inter = calloc((size_t)C, sizeof(size_t));
+        size_t* pc = calloc((size_t)C, sizeof(size_t));
+        size_t* gc = calloc((size_t)C, sizeof(size_t));
+        size_t valid = 0;
+        int st = 0;
+        for (size_t p = 0; p < n && !st; ++p) {
+            if (!label_mask[p]) continue;
+            ++valid;
+            int best = 0;  /* argmax_labels: first maximum */
+            for (int ch = 1; ch < C; ++ch)
+                if (semantics[p * C + ch] > semantics[p * C + best]) best = ch;
+            const int g = gt_labels[p];
+            if (best >= C || g >= C) { st = fail(1, "miou: label out of range"); break; }
+            ++pc[best];
+            ++gc[g];
+            if (best == g) ++inter[best];
+        }
+        if (!st && valid) {
+            double sum = 0;
+            int classes = 0;
+            for (int c = 0; c < C; ++c) {
+                const size_t uni = pc[c] + gc[c] - inter[c];
+                if (uni == 0) continue;
+                sum += (double)inter[c] / (double)uni;
+                ++classes;
+            }
+            if (classes) { vals[5] = sum / classes; has[5] = 1; }
+        }
+        free(inter); free(pc); free(gc);
+        if (st) return st;
+    }
+    return 0;
+}
+
 /* ------------------------------------------------------------ backward */
 static void zero_grads(const mo_scene* S, mo_grads* g) {
     const int64_t n = S->n;

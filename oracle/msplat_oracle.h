@@ -133,6 +133,14 @@ int mo_frame_losses(int width, int height, int num_classes, const mo_camera* cam
                     const double* gt_normal, const uint8_t* gt_labels, const double* lambdas, double* report,
                     double* dcolor, double* ddepth, double* dsemantics, double* dkmap, double* normals_out);
 
+/* Image metrics (core/src/metrics.cpp:68-187), HWC inputs; a metric whose
+ * inputs are NULL is skipped.  vals[6] = psnr, ssim, abs_rel, rmse, cos_simi,
+ * miou; has[6] = 0 for nullopt / skipped. */
+int mo_metrics(int width, int height, int num_classes, const double* color, const double* gt_rgb,
+               const double* depth, const double* gt_depth, const uint8_t* depth_mask, const double* normals,
+               const double* gt_normal, const uint8_t* normal_mask, const double* semantics,
+               const uint8_t* gt_labels, const uint8_t* label_mask, double* vals, int* has);
+
 /* Adam on raw parameters (trainer.cpp:90-133).  params/grads/m/v share the
  * scene layout; lr[7] = position, rotation, scale, opacity, sh, semantics, k. */
 int mo_adam(int64_t n, int num_classes, int sh_degree, double* means, double* quats,

@@ -213,6 +213,24 @@ class Oracle:
             _p(out["ddepth"]), _p(out["dsemantics"]) if C else None, _p(out["dkmap"]), _p(nrm)))
         return dict(zip(self.LOSS_FIELDS, rep.tolist())), out, nrm
 
+    METRIC_FIELDS = ("psnr", "ssim", "abs_rel", "rmse", "cos_simi", "miou")
+
+    def metrics(self, W, H, C, color=None, gt_rgb=None, depth=None, gt_depth=None, depth_mask=None, normals=None,
+                gt_normal=None, normal_mask=None, semantics=None, labels=None, label_mask=None):
+        """metrics.cpp:68-187 on HWC arrays -> {name: value or None}."""
+        args = [_f64(a) if a is not None else None
+                for a in (color, gt_rgb, depth, gt_depth, normals, gt_normal, semantics)]
+        um = [np.ascontiguousarray(a, np.uint8) if a is not None else None
+              for a in (depth_mask, normal_mask, labels, label_mask)]
+        vals = np.zeros(6)
+        has = np.zeros(6, np.int32)
+        pa = lambda a: _p(a) if a is not None else None  # noqa: E731
+        pu = lambda a: _p(a, _u8p) if a is not None else None  # noqa: E731
+        self._check(self.lib.mo_metrics(W, H, C, pa(args[0]), pa(args[1]), pa(args[2]), pa(args[3]), pu(um[0]),
+                                        pa(args[4]), pa(args[5]), pu(um[1]), pa(args[6]), pu(um[2]), pu(um[3]),
+                                        _p(vals), has.ctypes.data_as(ct.POINTER(ct.c_int))))
+        return {k: (float(vals[i]) if has[i] else None) for i, k in enumerate(self.METRIC_FIELDS)}
+
     def backward(self, s, cam, pix, cfg=None, threads=1):
         sc, keep = self.scene(s)
         K = (int(s["sh_degree"]) + 1) ** 2

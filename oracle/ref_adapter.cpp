@@ -8,6 +8,7 @@
 // marshals back.
 #include "msplat_oracle.h"
 
+#include "msplat/metrics.hpp"
 #include "msplat/normals.hpp"
 #include "msplat/rasterizer.hpp"
 #include "msplat/scene.hpp"
@@ -606,5 +607,44 @@ extern "C" int mo_train(int n_points, const double* points, const double* colors
         }
         *completed = r.completed_iterations;
         *halted = r.halted_non_finite ? 1 : 0;
+    });
+}
+
+// metrics.cpp:68-187 through the reference's own functions.
+extern "C" int mo_metrics(int W, int H, int C, const double* color, const double* gt_rgb, const double* depth,
+                          const double* gt_depth, const uint8_t* depth_mask, const double* normals,
+                          const double* gt_normal, const uint8_t* normal_mask, const double* semantics,
+                          const uint8_t* gt_labels, const uint8_t* label_mask, double* vals, int* has) {
+    return guarded([&] {
+        for (int i = 0; i < 6; ++i) {
+            vals[i] = 0;
+            has[i] = 0;
+        }
+        auto mask_of = [&](const uint8_t* m) {
+            GridU8 g(W, H, 1, 0);
+            std::memcpy(g.data(), m, size_t(W) * H);
+            return g;
+        };
+        auto set = [&](int i, std::optional<Scalar> v) {
+            if (v) {
+                vals[i] = *v;
+                has[i] = 1;
+            }
+        };
+        if (color && gt_rgb) {
+            const GridF a = grid_from(color, W, H, 3), b = grid_from(gt_rgb, W, H, 3);
+            set(0, psnr(a, b));
+            set(1, ssim_metric(a, b));
+        }
+        if (depth && gt_depth && depth_mask) {
+            const GridF d = grid_from(depth, W, H, 1), g = grid_from(gt_depth, W, H, 1);
+            const GridU8 m = mask_of(depth_mask);
+            set(2, abs_rel(d, g, m));
+            set(3, rmse(d, g, m));
+        }
+        if (normals && gt_normal && normal_mask)
+            set(4, cos_simi(grid_from(normals, W, H, 3), grid_from(gt_normal, W, H, 3), mask_of(normal_mask)));
+        if (semantics && gt_labels && label_mask && C > 0)
+            set(5, miou(argmax_labels(grid_from(semantics, W, H, C)), mask_of(gt_labels), mask_of(label_mask), C));
     });
 }

@@ -84,6 +84,13 @@ class MsplatLossReport(ct.Structure):
     _fields_ = [(f, ct.c_double) for f in LOSS_REPORT_FIELDS]
 
 
+METRIC_FIELDS = ("psnr", "ssim", "abs_rel", "rmse", "cos_simi", "miou")
+
+
+class MsplatMetricReport(ct.Structure):
+    _fields_ = [(f, ct.c_double) for f in METRIC_FIELDS] + [("has_" + f, ct.c_int) for f in METRIC_FIELDS]
+
+
 class LogicError(RuntimeError):
     """std::logic_error of the reference (e.g. chaining an already-raw buffer)."""
 
@@ -130,6 +137,9 @@ def _sig(lib):
                                            P(MsplatFrame), P(MsplatGroundTruth), P(ct.c_double),
                                            P(MsplatPixelGrads), P(MsplatLossReport)]),
         ("msplat_loss_report_device", _vp, [_vp]),
+        ("msplat_frame_metrics", ct.c_int, [_vp, ct.c_int, ct.c_int, ct.c_int, ct.c_int, _vp, _vp, _vp, _vp, _vp,
+                                            _vp, _vp, _vp, _vp, _vp, _vp, P(MsplatMetricReport)]),
+        ("msplat_init_scene", ct.c_int, [_vp, ct.c_int, _i64, _vp, _vp, ct.c_int, ct.c_int, ct.c_double, _vp]),
         ("msplat_context_timings", ct.c_int, [_vp, P(ct.c_double), P(_i64)]),
         ("msplat_kernel_launches", _i64, []),
     ]

@@ -146,6 +146,7 @@ struct msplat_context {
     DevBuf acc_dcolor, acc16, ddepth_total, normal_dv, kept;
     // frame losses (msplat_frame_losses)
     DevBuf loss_acc, loss_report, ssim_maps, ssim_grad, loss_dN;
+    DevBuf metric_acc, metric_hist;
     // trainer support (msplat_init_scene, msplat_prune_compact)
     DevBuf init_pts, init_cols, init_logs, cmp_k32, cmp_idx, cmp_tiles, cmp_total;
     // deterministic backward (msplat_context_set_deterministic)
@@ -273,6 +274,8 @@ msplat_status drain_device_error(msplat_context* ctx, int W) {
         case kErrInstanceOverflow:
             snprintf(buf, sizeof buf, "internal: tile-instance capacity %lld exceeded (needed %lld)", e.b, e.a);
             return set_error(MSPLAT_ERR_RUNTIME, buf);
+        case kErrMiouLabel:
+            return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "miou: label out of range");
         case kErrLabelRange:
             snprintf(buf, sizeof buf, "cross_entropy_seg: label %lld out of range at pixel (%lld,%lld)", e.b, e.a % w,
                      e.a / w);
@@ -720,7 +723,7 @@ msplat_status msplat_context_create(int device, void* cuda_stream, msplat_contex
 void msplat_context_destroy(msplat_context* ctx) {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->stream);
-    for (DevBuf* b : {&ctx->acc_dcolor, &ctx->acc16, &ctx->loss_acc, &ctx->loss_report, &ctx->ssim_maps, &ctx->ssim_grad, &ctx->loss_dN, &ctx->init_pts,
+    for (DevBuf* b : {&ctx->acc_dcolor, &ctx->acc16, &ctx->loss_acc, &ctx->loss_report, &ctx->metric_acc, &ctx->metric_hist, &ctx->ssim_maps, &ctx->ssim_grad, &ctx->loss_dN, &ctx->init_pts,
                        &ctx->init_cols, &ctx->init_logs, &ctx->cmp_k32, &ctx->cmp_idx, &ctx->cmp_tiles, &ctx->cmp_total,
                        &ctx->ddepth_total, &ctx->normal_dv,
                       &ctx->kept})
@@ -1016,6 +1019,110 @@ msplat_status msplat_frame_losses(msplat_context* ctx, int dtype, int num_classe
 
 const double* msplat_loss_report_device(msplat_context* ctx) {
     return ctx ? static_cast<const double*>(ctx->loss_report.p) : nullptr;
+}
+
+msplat_status msplat_frame_metrics(msplat_context* ctx, int dtype, int width, int height, int num_classes,
+                                   const void* color, const void* gt_rgb, const void* depth, const void* gt_depth,
+                                   const uint8_t* depth_mask, const void* normals, const void* gt_normal,
+                                   const uint8_t* normal_mask, const void* semantics, const uint8_t* gt_labels,
+                                   const uint8_t* label_mask, msplat_metric_report* out) {
+    if (!ctx || !out) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "frame_metrics: null argument");
+    if (width < 1 || height < 1 || num_classes < 0)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "frame_metrics: bad frame size");
+    if (dtype != MSPLAT_F32 && dtype != MSPLAT_F64)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "frame_metrics: dtype must be MSPLAT_F32 or MSPLAT_F64");
+    const bool do_rgb = color && gt_rgb, do_depth = depth && gt_depth && depth_mask,
+               do_normal = normals && gt_normal && normal_mask,
+               do_sem = semantics && gt_labels && label_mask && num_classes > 0;
+    if (do_rgb && (width < 11 || height < 11))
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "ssim_loss: frame smaller than the 11x11 window");
+    CUDA_TRY(ctx->metric_acc.ensure(9 * sizeof(double)));
+    CUDA_TRY(ctx->metric_hist.ensure(3 * size_t(std::max(num_classes, 1)) * 8));
+    double w[11], wsum = 0;
+    for (int i = 0; i < 11; ++i) {
+        const double d = i - 5.0;
+        w[i] = std::exp(-d * d / (2.0 * 1.5 * 1.5));
+        wsum += w[i];
+    }
+    auto fill = [&](auto& a, auto tag) {
+        using Real = decltype(tag);
+        a.W = width;
+        a.H = height;
+        a.C = do_sem ? num_classes : 0;
+        for (int i = 0; i < 11; ++i) a.ssim_w[i] = w[i] / wsum;
+        a.color = do_rgb ? static_cast<const Real*>(color) : nullptr;
+        a.gt_rgb = static_cast<const Real*>(gt_rgb);
+        a.depth = do_depth ? static_cast<const Real*>(depth) : nullptr;
+        a.gt_depth = static_cast<const Real*>(gt_depth);
+        a.depth_mask = depth_mask;
+        a.normals = do_normal ? static_cast<const Real*>(normals) : nullptr;
+        a.gt_normal = static_cast<const Real*>(gt_normal);
+        a.normal_mask = normal_mask;
+        a.sem = do_sem ? static_cast<const Real*>(semantics) : nullptr;
+        a.labels = gt_labels;
+        a.label_mask = label_mask;
+        a.acc = ctx->metric_acc.as<double>();
+        a.hist = ctx->metric_hist.as<unsigned long long>();
+        a.err = ctx->d_err;
+    };
+    if (dtype == MSPLAT_F64) {
+        MetricArgs<double> a{};
+        fill(a, double{});
+        launch_frame_metrics<double>(a, ctx->stream);
+    } else {
+        MetricArgs<float> a{};
+        fill(a, float{});
+        launch_frame_metrics<float>(a, ctx->stream);
+    }
+    CUDA_TRY(cudaGetLastError());
+    double acc[9];
+    std::vector<unsigned long long> hist(3 * size_t(std::max(num_classes, 1)), 0);
+    CUDA_TRY(cudaMemcpyAsync(acc, ctx->metric_acc.p, sizeof acc, cudaMemcpyDeviceToHost, ctx->stream));
+    if (do_sem)
+        CUDA_TRY(cudaMemcpyAsync(hist.data(), ctx->metric_hist.p, hist.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    msplat_status st = drain_device_error(ctx, width);
+    if (st != MSPLAT_OK) return st;
+    *out = msplat_metric_report{};
+    const double HW = double(width) * height;
+    if (do_rgb) {  // metrics.cpp:68-82, 84
+        const double mse = acc[0] / (3 * HW);
+        out->psnr = mse <= 1e-10 ? 100.0 : std::min(100.0, 10.0 * std::log10(1.0 / mse));
+        out->has_psnr = 1;
+        const double inv = 1.0 / (double(width - 10) * double(height - 10) * 3);
+        out->ssim = 1.0 - (1.0 - acc[8] * inv);
+        out->has_ssim = 1;
+    }
+    if (do_depth) {  // metrics.cpp:86-119
+        if (acc[2] > 0) {
+            out->abs_rel = acc[1] / acc[2];
+            out->has_abs_rel = 1;
+        }
+        if (acc[4] > 0) {
+            out->rmse = std::sqrt(acc[3] / acc[4]);
+            out->has_rmse = 1;
+        }
+    }
+    if (do_normal && acc[6] > 0) {  // metrics.cpp:121-137
+        out->cos_simi = acc[5] / acc[6];
+        out->has_cos_simi = 1;
+    }
+    if (do_sem && acc[7] > 0) {  // metrics.cpp:152-187
+        double sum = 0;
+        int classes = 0;
+        for (int c = 0; c < num_classes; ++c) {
+            const unsigned long long inter = hist[size_t(c)], pred = hist[size_t(num_classes + c)],
+                                     truth = hist[size_t(2 * num_classes + c)];
+            const unsigned long long uni = pred + truth - inter;
+            if (uni == 0) continue;
+            sum += double(inter) / double(uni);
+            ++classes;
+        }
+        if (classes > 0) {
+            out->miou = sum / classes;
+            out->has_miou = 1;
+        }
+    }
+    return MSPLAT_OK;
 }
 
 msplat_status msplat_init_scene(msplat_context* ctx, int dtype, int64_t n, const double* points, const double* colors,

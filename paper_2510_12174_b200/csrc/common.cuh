@@ -26,6 +26,7 @@ enum ErrCode : int {
     kErrNonFiniteParam = 6,    // scene.cpp:36-38 (b = primitive)
     kErrInstanceOverflow = 7,  // internal: tile-instance buffer too small (a = needed)
     kErrLabelRange = 8,        // losses.cpp:245-249 (a = pixel, b = label)
+    kErrMiouLabel = 9,         // metrics.cpp:165-166 (a = pixel, b = label)
 };
 
 struct DeviceError {

@@ -126,6 +126,25 @@ struct LossArgs {
 template <typename Real>
 void launch_frame_losses(const LossArgs<Real>& a, cudaStream_t s);
 
+// Evaluation metrics (core/src/metrics.cpp:68-187); NULL inputs skip a metric.
+template <typename Real>
+struct MetricArgs {
+    int W, H, C;
+    double ssim_w[11];
+    const Real *color, *gt_rgb;                       // psnr, ssim_metric
+    const Real *depth, *gt_depth;                     // abs_rel, rmse
+    const uint8_t* depth_mask;
+    const Real *normals, *gt_normal;                  // cos_simi
+    const uint8_t* normal_mask;
+    const Real* sem;                                  // argmax_labels + miou
+    const uint8_t *labels, *label_mask;
+    double* acc;                                      // [9]
+    unsigned long long* hist;                         // [3][C]
+    DeviceError* err;
+};
+template <typename Real>
+void launch_frame_metrics(const MetricArgs<Real>& a, cudaStream_t s);
+
 // K13: trainer support (core/src/trainer.cpp:42-86, 150-168).
 template <typename Real>
 void launch_init_scene(int64_t n, int C, int deg, const double* pts_dev, const double* cols_dev, double* log_scale_dev,

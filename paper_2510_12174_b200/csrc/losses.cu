@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(kThreadsL) ssim_fwd_kernel(const __grid_consta
         const Real b1 = mx * mx + my * my + C1, b2 = sx + sy + C2;
         const Real s = (a1 * a2) / (b1 * b2);
         ssum += double(s);
+        if (!a.ssim_maps) continue;  // metric only
         const Real dS = -Real(a.ssim_inv_count);
         Real* G = a.ssim_maps + size_t(c) * nv + r;  // [3 maps][3 ch][nv]
         G[0] = dS * (Real(2) * my * (a2 - a1) / (b1 * b2) - Real(2) * mx * s * (Real(1) / b1 - Real(1) / b2));
@@ -269,6 +270,61 @@ __global__ void __launch_bounds__(kThreadsL) assemble_kernel(const __grid_consta
     }
 }
 
+// Evaluation metrics (core/src/metrics.cpp:68-187): one pass of masked sums,
+// counts and per-class label histograms.  acc: 0 sq err (rgb), 1 abs_rel sum,
+// 2 abs_rel count, 3 depth sq err, 4 depth count, 5 cos sum, 6 cos count,
+// 7 label-valid count; hist: [3][C] (intersection, predicted, truth).
+template <typename Real>
+__global__ void __launch_bounds__(kThreadsL) metric_pixel_kernel(const __grid_constant__ MetricArgs<Real> a) {
+    extern __shared__ unsigned int hist_s[];  // [3][C]
+    const size_t HW = size_t(a.W) * a.H;
+    for (int i = threadIdx.x; i < 3 * a.C; i += blockDim.x) hist_s[i] = 0;
+    __syncthreads();
+    double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (size_t p = size_t(blockIdx.x) * blockDim.x + threadIdx.x; p < HW; p += size_t(gridDim.x) * blockDim.x) {
+        if (a.color)
+            for (int c = 0; c < 3; ++c) {
+                const double d = double(a.color[c * HW + p]) - double(a.gt_rgb[c * HW + p]);
+                v[0] += d * d;
+            }
+        if (a.depth && a.depth_mask[p]) {
+            const double d = double(a.depth[p]), g = double(a.gt_depth[p]);
+            if (g > 1e-3) {
+                v[1] += fabs(d - g) / g;
+                v[2] += 1;
+            }
+            v[3] += (d - g) * (d - g);
+            v[4] += 1;
+        }
+        if (a.normals && a.normal_mask[p]) {
+            for (int c = 0; c < 3; ++c) v[5] += double(a.normals[c * HW + p]) * double(a.gt_normal[c * HW + p]);
+            v[6] += 1;
+        }
+        if (a.sem && a.label_mask[p]) {
+            int best = 0;  // argmax_labels: the first maximum
+            Real bv = a.sem[p];
+            for (int c = 1; c < a.C; ++c)
+                if (a.sem[size_t(c) * HW + p] > bv) {
+                    bv = a.sem[size_t(c) * HW + p];
+                    best = c;
+                }
+            const int g = a.labels[p];
+            v[7] += 1;
+            if (g >= a.C) {
+                raise_error(a.err, kErrMiouLabel, (long long)p, g);
+            } else {
+                atomicAdd(&hist_s[a.C + best], 1u);
+                atomicAdd(&hist_s[2 * a.C + g], 1u);
+                if (best == g) atomicAdd(&hist_s[best], 1u);
+            }
+        }
+    }
+    block_accumulate<8>(v, a.acc);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 3 * a.C; i += blockDim.x)
+        if (hist_s[i]) atomicAdd(reinterpret_cast<unsigned long long*>(a.hist) + i, (unsigned long long)hist_s[i]);
+}
+
 unsigned grid_for(size_t n) {
     const size_t b = (n + kThreadsL - 1) / kThreadsL;
     return unsigned(b < size_t(148 * 8) ? (b ? b : 1) : size_t(148 * 8));
@@ -293,6 +349,29 @@ void launch_frame_losses(const LossArgs<Real>& a, cudaStream_t s) {
     count_launches(2);
 }
 
+template <typename Real>
+void launch_frame_metrics(const MetricArgs<Real>& a, cudaStream_t s) {
+    const size_t HW = size_t(a.W) * a.H;
+    cudaMemsetAsync(a.acc, 0, 9 * sizeof(double), s);
+    if (a.C > 0) cudaMemsetAsync(a.hist, 0, 3 * size_t(a.C) * sizeof(unsigned long long), s);
+    metric_pixel_kernel<Real><<<grid_for(HW), kThreadsL, 3 * size_t(a.C > 0 ? a.C : 1) * sizeof(unsigned int), s>>>(a);
+    count_launches(1);
+    if (a.color && a.W >= 11 && a.H >= 11) {  // ssim_metric = mean SSIM over valid windows
+        LossArgs<Real> l{};
+        l.W = a.W;
+        l.H = a.H;
+        for (int i = 0; i < 11; ++i) l.ssim_w[i] = a.ssim_w[i];
+        l.color = a.color;
+        l.gt_rgb = a.gt_rgb;
+        l.acc = a.acc + 7;  // ssim sum lands in acc[8]
+        const size_t nv = size_t(a.W - 10) * (a.H - 10);
+        ssim_fwd_kernel<Real><<<grid_for(3 * nv), kThreadsL, 0, s>>>(l);
+        count_launches(1);
+    }
+}
+
+template void launch_frame_metrics<float>(const MetricArgs<float>&, cudaStream_t);
+template void launch_frame_metrics<double>(const MetricArgs<double>&, cudaStream_t);
 template void launch_frame_losses<float>(const LossArgs<float>&, cudaStream_t);
 template void launch_frame_losses<double>(const LossArgs<double>&, cudaStream_t);
 

@@ -35,7 +35,7 @@ __all__ = [
     "MultimodalFrame", "ReplayState", "PixelGradients", "GradientBuffer", "TileBins",
     "OptimizerState", "TrainConfig", "rasterize", "rasterize_backward", "estimate_normals",
     "normals_backward", "chain_activations", "adam_step", "prune", "bin_and_sort", "fwd_bwd",
-    "LogicError", "param_layout", "GroundTruth", "LossReport", "frame_losses",
+    "LogicError", "param_layout", "GroundTruth", "LossReport", "frame_losses", "frame_metrics",
 ]
 
 
@@ -507,6 +507,28 @@ def frame_losses(frame: MultimodalFrame, gt: GroundTruth, view: CameraView, ncfg
                                          ct.byref(rep) if sync else None))
     report = LossReport(**{f: getattr(rep, f) for f in _lib.LOSS_REPORT_FIELDS}) if sync else None
     return report, out
+
+
+def frame_metrics(frame: MultimodalFrame, gt: GroundTruth, depth_mask: torch.Tensor | None = None,
+                  normal_mask: torch.Tensor | None = None, label_mask: torch.Tensor | None = None) -> dict:
+    """Image metrics of metrics.cpp:68-187 on the device: psnr, ssim (against
+    gt.rgb), abs_rel, rmse (depth, masked), cos_simi (normals, masked), miou
+    (argmax of the semantic logits vs gt.labels, masked).  A metric without its
+    inputs (ground truth or mask) is None, as is an empty mask."""
+    ctx = _Context.get(frame.color.device.index)
+    p = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    for m in (depth_mask, normal_mask, label_mask):
+        if m is not None and m.dtype != torch.uint8:
+            raise ValueError("frame_metrics: masks must be uint8")
+    rep = _lib.MsplatMetricReport()
+    have_sem = frame.num_classes > 0 and gt.labels is not None and label_mask is not None
+    check(_lib.lib().msplat_frame_metrics(
+        ctx.h, _dtype_code(frame.color.dtype), frame.width, frame.height, frame.num_classes,
+        p(frame.color) if gt.rgb is not None else None, p(gt.rgb),
+        p(frame.depth) if gt.depth is not None else None, p(gt.depth), p(depth_mask),
+        p(frame.normals) if gt.normal is not None else None, p(gt.normal), p(normal_mask),
+        p(frame.semantics) if have_sem else None, p(gt.labels), p(label_mask), ct.byref(rep)))
+    return {f: (getattr(rep, f) if getattr(rep, "has_" + f) else None) for f in _lib.METRIC_FIELDS}
 
 
 def rasterize_backward(scene: Scene, view: CameraView, frame: MultimodalFrame, replay: ReplayState,

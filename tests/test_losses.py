@@ -136,3 +136,59 @@ def test_device_frame_losses_errors(port):
         M.frame_losses(frame, g, view, ncfg)
     with pytest.raises(RuntimeError, match="rgb loss enabled"):
         M.frame_losses(frame, M.GroundTruth(None, g.depth, g.normal, g.labels), view, ncfg)
+
+
+# ------------------------------------------------------------ metrics
+def metric_case(port, seed=0):
+    """Rendered frame + ground truth + the masks evaluation uses."""
+    s, cam, f, gt = loss_case(port, seed)
+    nrm, valid, _ = port.normals(f["depth"], f["transmittance"], cam)
+    H, W = f["depth"].shape
+    rng = np.random.default_rng(10 + seed)
+    masks = {"depth_mask": (gt["depth"] > 0).astype(np.uint8), "normal_mask": valid,
+             "label_mask": (rng.random((H, W)) < 0.8).astype(np.uint8)}
+    return s, cam, f, gt, nrm, masks
+
+
+def _metric_inputs(f, gt, nrm, masks):
+    return dict(color=f["color"], gt_rgb=gt["rgb"], depth=f["depth"], gt_depth=gt["depth"], normals=nrm,
+                gt_normal=gt["normal"], semantics=f["semantics"], labels=gt["labels"], **masks)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_port_metrics_equal_reference(port, reference, seed):
+    s, cam, f, gt, nrm, masks = metric_case(port, seed)
+    H, W = f["depth"].shape
+    kw = _metric_inputs(f, gt, nrm, masks)
+    mp = port.metrics(W, H, int(s["num_classes"]), **kw)
+    mr = reference.metrics(W, H, int(s["num_classes"]), **kw)
+    assert all(v is not None for v in mr.values())  # every metric evaluated
+    for k in mr:
+        assert mp[k] == pytest.approx(mr[k], rel=1e-12, abs=1e-15), k
+    # an empty mask is nullopt, as in the reference
+    z = np.zeros((H, W), np.uint8)
+    e = reference.metrics(W, H, int(s["num_classes"]), depth=f["depth"], gt_depth=gt["depth"], depth_mask=z)
+    assert e["abs_rel"] is None and e["rmse"] is None
+    assert port.metrics(W, H, 0, depth=f["depth"], gt_depth=gt["depth"], depth_mask=z)["rmse"] is None
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,tol", [("float64", 1e-11), ("float32", 1e-5)])
+def test_device_metrics_match_reference(port, reference, dtype, tol):
+    import torch
+    import paper_2510_12174_b200 as M
+    s, cam, f, gt, nrm, masks = metric_case(port, 1)
+    H, W = f["depth"].shape
+    C = int(s["num_classes"])
+    dt = torch.float64 if dtype == "float64" else torch.float32
+    frame = M.MultimodalFrame(W, H, C, _planar(f["color"], dt), _planar(f["depth"], dt), _planar(f["semantics"], dt),
+                              _planar(f["kmap"], dt), _planar(f["transmittance"], dt), _planar(nrm, dt),
+                              torch.zeros(H, W, dtype=torch.int32, device="cuda"))
+    g = M.GroundTruth(_planar(gt["rgb"], dt), _planar(gt["depth"], dt), _planar(gt["normal"], dt),
+                      torch.as_tensor(gt["labels"], device="cuda"))
+    u8 = lambda a: torch.as_tensor(a, dtype=torch.uint8, device="cuda")  # noqa: E731
+    got = M.frame_metrics(frame, g, u8(masks["depth_mask"]), u8(masks["normal_mask"]), u8(masks["label_mask"]))
+    ref = reference.metrics(W, H, C, **_metric_inputs(f, gt, nrm, masks))
+    for k, v in ref.items():
+        assert v is not None and got[k] is not None, k
+        assert got[k] == pytest.approx(v, rel=tol, abs=1e-12), k
