@@ -52,6 +52,35 @@ def parse():
     return p.parse_args()
 
 
+def pair_counters(frame, replay, early_stop):
+    """SURVEY.md section 8d pair counts of one render (view of `frame`):
+    Pc = blended pairs (sum of contributors), Pb = backward-visited pairs (sum
+    of terminus), Pf = forward-visited pairs (terminus where the pixel
+    terminated early, else its tile's whole list)."""
+    import numpy as np
+    W, H = frame.width, frame.height
+    term = replay.terminus().astype(np.int64)
+    off, _ = replay.bins()
+    tiles_x = (W + 15) // 16
+    ty, tx = np.meshgrid(np.arange(H) // 16, np.arange(W) // 16, indexing="ij")
+    t = ty * tiles_x + tx
+    L = (off[t + 1] - off[t]).astype(np.int64)
+    T = frame.transmittance.double().cpu().numpy()
+    Pc = int(frame.contributors.long().sum().item())
+    Pb = int(term.sum())
+    Pf = int(np.where(T < early_stop, term, L).sum())
+    return Pc, Pb, Pf
+
+
+def fp32_peak_tflops():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f)["sm_max_mhz"])
+    except Exception:
+        mhz = 1965.0
+    return 148 * 128 * 2 * mhz * 1e6 / 1e12, f"nominal: 148 SM x 128 FP32 lanes x 2 x {mhz:.0f} MHz"
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -280,6 +309,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize(dev)
     R.check_device_errors(local_rank)
     counters = replay.counters()
+    Pc, Pb, Pf = pair_counters(frame, replay, rc.early_stop_transmittance)
 
     graph = None
     if not args.no_graph:
@@ -362,6 +392,10 @@ def run_ours(args, rank, world, local_rank):
         pass
     render_ms = sum(per_launch[k] for k in per_launch if k != "optim")
     rb = render_alg_bytes(n, P, HW, C, I)
+    # SURVEY.md 8d algorithmic FP32 flops per fwd+bwd render (FMA = 2)
+    F_alg = 12 * (Pf + Pb) + Pc * (53 + 2 * C) + Pc * (264 + 8 * C)
+    fpk, fpk_src = fp32_peak_tflops()
+    t_hbm, t_fp32 = rb / (peak * 1e9), F_alg / (fpk * 1e12)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -375,9 +409,15 @@ def run_ours(args, rank, world, local_rank):
                      "alg_bytes_per_launch": bytes_dom, "avg_launch_ms": per_launch[dom]},
         "render_roofline": {"alg_bytes_per_render": rb, "render_device_ms": render_ms,
                             "achieved_gbs": rb / (render_ms / 1000.0) / 1e9,
-                            "frac_of_hbm": rb / (render_ms / 1000.0) / 1e9 / peak},
+                            "frac_of_hbm": rb / (render_ms / 1000.0) / 1e9 / peak,
+                            "alg_fp32_flops_per_render": F_alg,
+                            "achieved_tflops": F_alg / (render_ms / 1000.0) / 1e12,
+                            "fp32_peak_tflops": fpk, "fp32_peak_source": fpk_src,
+                            "frac_of_fp32": F_alg / (render_ms / 1000.0) / 1e12 / fpk,
+                            "roofline_bound_frac": max(t_hbm, t_fp32) / (render_ms / 1000.0)},
         "stage_ms_per_view": {k: round(v, 4) for k, v in per_launch.items()},
-        "counters": dict(counters, pixels=HW, P=P),
+        "counters": dict(counters, pixels=HW, P=P, Pc_blended_pairs=Pc, Pb_backward_pairs=Pb,
+                         Pf_forward_pairs=Pf),
     }
     return line
 
