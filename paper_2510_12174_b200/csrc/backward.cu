@@ -9,6 +9,57 @@
 namespace msplat_cuda {
 
 // ------------------------------------------------------------------ K10
+// SH colour adjoint (sh.cpp:45-73, 86-99) for a compile-time degree: dsh +=
+// g (x) basis, and the view-direction gradient through the basis Jacobian.
+template <typename Real, int DEG>
+__device__ __forceinline__ void sh_adjoint(const ProjBackwardArgs<Real>& a, int64_t i, Real dx, Real dy, Real dz,
+                                           const Real* g3, Real* ddir) {
+    constexpr int K = (DEG + 1) * (DEG + 1);
+    Real b[K], Jb[K][3];
+    const Real C0 = Real(0.28209479177387814), C1 = Real(0.4886025119029199);
+    const Real k0 = Real(1.0925484305920792), k1 = Real(-1.0925484305920792), k2 = Real(0.31539156525252005),
+               k3 = Real(-1.0925484305920792), k4 = Real(0.5462742152960396);
+    const Real m0 = Real(-0.5900435899266435), m1 = Real(2.890611442640554), m2 = Real(-0.4570457994644658),
+               m3 = Real(0.3731763325901154), m4 = Real(-0.4570457994644658), m5 = Real(1.445305721320277),
+               m6 = Real(-0.5900435899266435);
+#pragma unroll
+    for (int j = 0; j < K; ++j) Jb[j][0] = Jb[j][1] = Jb[j][2] = Real(0);
+    const Real xx = dx * dx, yy = dy * dy, zz = dz * dz;
+    b[0] = C0;
+    if constexpr (DEG >= 1) {
+        b[1] = -C1 * dy; b[2] = C1 * dz; b[3] = -C1 * dx;
+        Jb[1][1] = -C1; Jb[2][2] = C1; Jb[3][0] = -C1;
+    }
+    if constexpr (DEG >= 2) {
+        b[4] = k0 * dx * dy; b[5] = k1 * dy * dz; b[6] = k2 * (2 * zz - xx - yy);
+        b[7] = k3 * dx * dz; b[8] = k4 * (xx - yy);
+        Jb[4][0] = k0 * dy; Jb[4][1] = k0 * dx;
+        Jb[5][1] = k1 * dz; Jb[5][2] = k1 * dy;
+        Jb[6][0] = -2 * k2 * dx; Jb[6][1] = -2 * k2 * dy; Jb[6][2] = 4 * k2 * dz;
+        Jb[7][0] = k3 * dz; Jb[7][2] = k3 * dx;
+        Jb[8][0] = 2 * k4 * dx; Jb[8][1] = -2 * k4 * dy;
+    }
+    if constexpr (DEG >= 3) {
+        b[9] = m0 * dy * (3 * xx - yy); b[10] = m1 * dx * dy * dz; b[11] = m2 * dy * (4 * zz - xx - yy);
+        b[12] = m3 * dz * (2 * zz - 3 * xx - 3 * yy); b[13] = m4 * dx * (4 * zz - xx - yy);
+        b[14] = m5 * dz * (xx - yy); b[15] = m6 * dx * (xx - 3 * yy);
+        Jb[9][0] = m0 * 6 * dx * dy; Jb[9][1] = m0 * (3 * xx - 3 * yy);
+        Jb[10][0] = m1 * dy * dz; Jb[10][1] = m1 * dx * dz; Jb[10][2] = m1 * dx * dy;
+        Jb[11][0] = -2 * m2 * dx * dy; Jb[11][1] = m2 * (4 * zz - xx - 3 * yy); Jb[11][2] = 8 * m2 * dy * dz;
+        Jb[12][0] = -6 * m3 * dx * dz; Jb[12][1] = -6 * m3 * dy * dz; Jb[12][2] = m3 * (6 * zz - 3 * xx - 3 * yy);
+        Jb[13][0] = m4 * (4 * zz - 3 * xx - yy); Jb[13][1] = -2 * m4 * dx * dy; Jb[13][2] = 8 * m4 * dx * dz;
+        Jb[14][0] = 2 * m5 * dx * dz; Jb[14][1] = -2 * m5 * dy * dz; Jb[14][2] = m5 * (xx - yy);
+        Jb[15][0] = m6 * (3 * xx - 3 * yy); Jb[15][1] = -6 * m6 * dx * dy;
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const Real shg = a.sh[(i * 3 + 0) * K + j] * g3[0] + a.sh[(i * 3 + 1) * K + j] * g3[1] +
+                         a.sh[(i * 3 + 2) * K + j] * g3[2];
+        for (int k = 0; k < 3; ++k) ddir[k] += Jb[j][k] * shg;
+        for (int ch = 0; ch < 3; ++ch) a.g_sh[(i * 3 + ch) * K + j] += g3[ch] * b[j];
+    }
+}
+
 template <typename Real>
 __global__ void __launch_bounds__(256) projection_backward_kernel(const __grid_constant__ ProjBackwardArgs<Real> a) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -129,48 +180,12 @@ __global__ void __launch_bounds__(256) projection_backward_kernel(const __grid_c
                 const uint8_t cl = a.clamped_bits[i];
                 for (int ch = 0; ch < 3; ++ch)
                     if (cl & (1 << ch)) g3[ch] = 0;
-                const int deg = a.deg, K = a.K;
-                Real b[16], Jb[16][3];
-                const Real C0 = Real(0.28209479177387814), C1 = Real(0.4886025119029199);
-                const Real k0 = Real(1.0925484305920792), k1 = Real(-1.0925484305920792), k2 = Real(0.31539156525252005),
-                           k3 = Real(-1.0925484305920792), k4 = Real(0.5462742152960396);
-                const Real m0 = Real(-0.5900435899266435), m1 = Real(2.890611442640554), m2 = Real(-0.4570457994644658),
-                           m3 = Real(0.3731763325901154), m4 = Real(-0.4570457994644658), m5 = Real(1.445305721320277),
-                           m6 = Real(-0.5900435899266435);
-                for (int j = 0; j < 16; ++j) Jb[j][0] = Jb[j][1] = Jb[j][2] = Real(0);
-                const Real xx = dx * dx, yy = dy * dy, zz = dz * dz;
-                b[0] = C0;
-                if (deg >= 1) {
-                    b[1] = -C1 * dy; b[2] = C1 * dz; b[3] = -C1 * dx;
-                    Jb[1][1] = -C1; Jb[2][2] = C1; Jb[3][0] = -C1;
-                }
-                if (deg >= 2) {
-                    b[4] = k0 * dx * dy; b[5] = k1 * dy * dz; b[6] = k2 * (2 * zz - xx - yy);
-                    b[7] = k3 * dx * dz; b[8] = k4 * (xx - yy);
-                    Jb[4][0] = k0 * dy; Jb[4][1] = k0 * dx;
-                    Jb[5][1] = k1 * dz; Jb[5][2] = k1 * dy;
-                    Jb[6][0] = -2 * k2 * dx; Jb[6][1] = -2 * k2 * dy; Jb[6][2] = 4 * k2 * dz;
-                    Jb[7][0] = k3 * dz; Jb[7][2] = k3 * dx;
-                    Jb[8][0] = 2 * k4 * dx; Jb[8][1] = -2 * k4 * dy;
-                }
-                if (deg >= 3) {
-                    b[9] = m0 * dy * (3 * xx - yy); b[10] = m1 * dx * dy * dz; b[11] = m2 * dy * (4 * zz - xx - yy);
-                    b[12] = m3 * dz * (2 * zz - 3 * xx - 3 * yy); b[13] = m4 * dx * (4 * zz - xx - yy);
-                    b[14] = m5 * dz * (xx - yy); b[15] = m6 * dx * (xx - 3 * yy);
-                    Jb[9][0] = m0 * 6 * dx * dy; Jb[9][1] = m0 * (3 * xx - 3 * yy);
-                    Jb[10][0] = m1 * dy * dz; Jb[10][1] = m1 * dx * dz; Jb[10][2] = m1 * dx * dy;
-                    Jb[11][0] = -2 * m2 * dx * dy; Jb[11][1] = m2 * (4 * zz - xx - 3 * yy); Jb[11][2] = 8 * m2 * dy * dz;
-                    Jb[12][0] = -6 * m3 * dx * dz; Jb[12][1] = -6 * m3 * dy * dz; Jb[12][2] = m3 * (6 * zz - 3 * xx - 3 * yy);
-                    Jb[13][0] = m4 * (4 * zz - 3 * xx - yy); Jb[13][1] = -2 * m4 * dx * dy; Jb[13][2] = 8 * m4 * dx * dz;
-                    Jb[14][0] = 2 * m5 * dx * dz; Jb[14][1] = -2 * m5 * dy * dz; Jb[14][2] = m5 * (xx - yy);
-                    Jb[15][0] = m6 * (3 * xx - 3 * yy); Jb[15][1] = -6 * m6 * dx * dy;
-                }
                 Real ddir[3] = {0, 0, 0};
-                for (int j = 0; j < K; ++j) {
-                    const Real shg = a.sh[(i * 3 + 0) * K + j] * g3[0] + a.sh[(i * 3 + 1) * K + j] * g3[1] +
-                                     a.sh[(i * 3 + 2) * K + j] * g3[2];
-                    for (int k = 0; k < 3; ++k) ddir[k] += Jb[j][k] * shg;
-                    for (int ch = 0; ch < 3; ++ch) a.g_sh[(i * 3 + ch) * K + j] += g3[ch] * b[j];
+                switch (a.deg) {  // compile-time K: basis and Jacobian stay in registers
+                    case 0: sh_adjoint<Real, 0>(a, i, dx, dy, dz, g3, ddir); break;
+                    case 1: sh_adjoint<Real, 1>(a, i, dx, dy, dz, g3, ddir); break;
+                    case 2: sh_adjoint<Real, 2>(a, i, dx, dy, dz, g3, ddir); break;
+                    default: sh_adjoint<Real, 3>(a, i, dx, dy, dz, g3, ddir); break;
                 }
                 const Real dirv[3] = {dx, dy, dz};
                 const Real dd = dx * ddir[0] + dy * ddir[1] + dz * ddir[2];
