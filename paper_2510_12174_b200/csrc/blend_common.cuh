@@ -301,6 +301,35 @@ __device__ __forceinline__ void stage_F_wait_prev() {
     __syncwarp();
 }
 
+// ---- warp-level tensor-core helpers (mma.sync m16n8k8 TF32, FP32 accumulate)
+// with a hi/lo operand split: a.b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi, i.e.
+// FP32-level accuracy for the blend contractions.
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+    const float r = x - __uint_as_float(hi);
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+// d += A B with the 3-term split (A: 4 fp32 fragment values, B: 2).
+__device__ __forceinline__ void mma_3xtf32(float (&d)[4], const float (&a)[4], const float (&b)[2]) {
+    uint32_t ah[4], al[4], bh[2], bl[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) split_tf32(a[i], ah[i], al[i]);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) split_tf32(b[i], bh[i], bl[i]);
+    mma_tf32(d, al, bh);
+    mma_tf32(d, ah, bl);
+    mma_tf32(d, ah, bh);
+}
+
 __device__ __forceinline__ int tile_pixel_x(int warp, int lane) { return (warp & 1) * 8 + (lane & 7); }
 __device__ __forceinline__ int tile_pixel_y(int warp, int lane) { return (warp >> 1) * 4 + (lane >> 3); }
 __device__ __forceinline__ int tile_pixel_index(int warp, int lane) {
