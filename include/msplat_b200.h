@@ -296,6 +296,18 @@ MSPLAT_API msplat_status msplat_frame_metrics(msplat_context* ctx, int dtype, in
                                    const uint8_t* gt_labels, const uint8_t* label_mask,
                                    msplat_metric_report* out);
 
+/* Extended-PLY scene I/O (msplat/io_ply.hpp, core/src/io_ply.cpp:122-263) to and
+ * from the packed parameter layout (msplat_param_layout) on the device: the
+ * payload moves in one bulk transfer and is transposed AoS <-> SoA by a kernel.
+ * Files are binary little-endian; written as float64 (exact round trip);
+ * read from any of double/float/(u)int8/16/32 columns, missing semantics = 0,
+ * missing grad_k = 0.9.  Errors carry the reference's texts ("<path>: ...",
+ * "Scene: primitive i has non-finite fields").  Synchronizing. */
+MSPLAT_API msplat_status msplat_ply_scene_info(const char* path, int64_t* n, int* num_classes, int* sh_degree);
+MSPLAT_API msplat_status msplat_load_scene_ply(msplat_context* ctx, const char* path, int dtype, void* params);
+MSPLAT_API msplat_status msplat_save_scene_ply(msplat_context* ctx, const char* path, int dtype, int64_t n,
+                                    int num_classes, int sh_degree, const void* params);
+
 /* init_scene(points, colors, C, cfg)  (core/src/trainer.cpp:42-86) into a packed
  * parameter buffer (msplat_param_layout order, `dtype`): one Gaussian per
  * point, identity rotation, opacity 0.1, DC colour, zero semantics, k = k_reset,

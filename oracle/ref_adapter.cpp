@@ -8,6 +8,7 @@
 // marshals back.
 #include "msplat_oracle.h"
 
+#include "msplat/io_ply.hpp"
 #include "msplat/metrics.hpp"
 #include "msplat/normals.hpp"
 #include "msplat/rasterizer.hpp"
@@ -646,5 +647,45 @@ extern "C" int mo_metrics(int W, int H, int C, const double* color, const double
             set(4, cos_simi(grid_from(normals, W, H, 3), grid_from(gt_normal, W, H, 3), mask_of(normal_mask)));
         if (semantics && gt_labels && label_mask && C > 0)
             set(5, miou(argmax_labels(grid_from(semantics, W, H, C)), mask_of(gt_labels), mask_of(label_mask), C));
+    });
+}
+
+// io_ply.cpp through the reference (save_scene_ply / load_scene_ply).
+extern "C" int mo_ply_save(const char* path, const mo_scene* s) {
+    return guarded([&] { save_scene_ply(path, to_scene(s)); });
+}
+
+// Loads into the packed layout (means quats log_scales opacity k sh sem).
+extern "C" int mo_ply_load(const char* path, int64_t cap, double* packed, int64_t* n_out, int* C_out, int* deg_out) {
+    return guarded([&] {
+        const Scene s = load_scene_ply(path);
+        const int K = s.sh_coeff_count(), C = s.num_classes;
+        const int64_t n = int64_t(s.size());
+        const int64_t sizes[7] = {3, 4, 3, 1, 1, 3 * K, C};
+        int64_t off[8];
+        off[0] = 0;
+        for (int i = 0; i < 7; ++i)
+            off[i + 1] = off[i] + n * sizes[i];
+        *n_out = n;
+        *C_out = C;
+        *deg_out = s.sh_degree;
+        if (off[7] > cap)
+            return;
+        for (int64_t i = 0; i < n; ++i) {
+            const GaussianPrimitive& g = s.gaussians[size_t(i)];
+            for (int j = 0; j < 3; ++j) {
+                packed[off[0] + 3 * i + j] = g.position[j];
+                packed[off[2] + 3 * i + j] = g.log_scale[j];
+            }
+            for (int j = 0; j < 4; ++j)
+                packed[off[1] + 4 * i + j] = g.rotation[j];
+            packed[off[3] + i] = g.opacity_logit;
+            packed[off[4] + i] = g.gradient_factor;
+            for (int ch = 0; ch < 3; ++ch)
+                for (int j = 0; j < K; ++j)
+                    packed[off[5] + (3 * i + ch) * K + j] = g.sh(ch, j);
+            for (int ch = 0; ch < C; ++ch)
+                packed[off[6] + i * C + ch] = g.semantic_logits[ch];
+        }
     });
 }

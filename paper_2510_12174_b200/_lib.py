@@ -139,6 +139,9 @@ def _sig(lib):
         ("msplat_loss_report_device", _vp, [_vp]),
         ("msplat_frame_metrics", ct.c_int, [_vp, ct.c_int, ct.c_int, ct.c_int, ct.c_int, _vp, _vp, _vp, _vp, _vp,
                                             _vp, _vp, _vp, _vp, _vp, _vp, P(MsplatMetricReport)]),
+        ("msplat_ply_scene_info", ct.c_int, [ct.c_char_p, P(_i64), P(ct.c_int), P(ct.c_int)]),
+        ("msplat_load_scene_ply", ct.c_int, [_vp, ct.c_char_p, ct.c_int, _vp]),
+        ("msplat_save_scene_ply", ct.c_int, [_vp, ct.c_char_p, ct.c_int, _i64, ct.c_int, ct.c_int, _vp]),
         ("msplat_init_scene", ct.c_int, [_vp, ct.c_int, _i64, _vp, _vp, ct.c_int, ct.c_int, ct.c_double, _vp]),
         ("msplat_context_timings", ct.c_int, [_vp, P(ct.c_double), P(_i64)]),
         ("msplat_kernel_launches", _i64, []),

@@ -1125,6 +1125,37 @@ msplat_status msplat_frame_metrics(msplat_context* ctx, int dtype, int width, in
     return MSPLAT_OK;
 }
 
+static msplat_status io_status(const IoResult& r) {
+    if (r.code == 0) return MSPLAT_OK;
+    if (r.code == 1) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, r.msg.c_str());
+    if (r.code == 4) return set_error(MSPLAT_ERR_CUDA, r.msg.c_str());
+    return set_error(MSPLAT_ERR_RUNTIME, r.msg.c_str());
+}
+
+msplat_status msplat_ply_scene_info(const char* path, int64_t* n, int* num_classes, int* sh_degree) {
+    if (!path || !n || !num_classes || !sh_degree) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "ply: null argument");
+    return io_status(ply_scene_info(path, n, num_classes, sh_degree));
+}
+
+msplat_status msplat_load_scene_ply(msplat_context* ctx, const char* path, int dtype, void* params) {
+    if (!ctx || !path || !params) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "load_scene_ply: null argument");
+    if (dtype == MSPLAT_F64) return io_status(ply_load_scene<double>(path, static_cast<double*>(params), ctx->stream, ctx->d_err));
+    if (dtype == MSPLAT_F32) return io_status(ply_load_scene<float>(path, static_cast<float*>(params), ctx->stream, ctx->d_err));
+    return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "load_scene_ply: dtype must be MSPLAT_F32 or MSPLAT_F64");
+}
+
+msplat_status msplat_save_scene_ply(msplat_context* ctx, const char* path, int dtype, int64_t n, int num_classes,
+                                    int sh_degree, const void* params) {
+    if (!ctx || !path || (n > 0 && !params)) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "save_scene_ply: null argument");
+    if (sh_degree < 0 || sh_degree > 3) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "Scene: sh_degree must be in [0,3]");
+    if (num_classes < 0) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "Scene: num_classes must be >= 0");
+    if (dtype == MSPLAT_F64)
+        return io_status(ply_save_scene<double>(path, n, num_classes, sh_degree, static_cast<const double*>(params), ctx->stream));
+    if (dtype == MSPLAT_F32)
+        return io_status(ply_save_scene<float>(path, n, num_classes, sh_degree, static_cast<const float*>(params), ctx->stream));
+    return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "save_scene_ply: dtype must be MSPLAT_F32 or MSPLAT_F64");
+}
+
 msplat_status msplat_init_scene(msplat_context* ctx, int dtype, int64_t n, const double* points, const double* colors,
                                 int num_classes, int sh_degree, double k_reset, void* params) {
     if (!ctx || !params) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "init_scene: null argument");

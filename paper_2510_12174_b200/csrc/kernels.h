@@ -3,6 +3,8 @@
 // optim.cu) and the C-ABI layer (cabi.cu).
 #pragma once
 
+#include <string>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -153,6 +155,18 @@ template <typename Real>
 void launch_prune_compact(int64_t n, int C, int deg, const uint8_t* keep, int64_t kept, const Real* const in[3],
                           Real* const out[3], double k_reset, uint32_t* k32, uint32_t* newidx, uint32_t* scan_tiles,
                           uint32_t* d_total, cudaStream_t s);
+
+// Extended-PLY scene I/O (core/src/io_ply.cpp) to / from the packed layout.
+// code: 0 ok, 1 invalid_argument, 2 runtime_error, 4 CUDA error.
+struct IoResult {
+    int code = 0;
+    std::string msg;
+};
+IoResult ply_scene_info(const char* path, int64_t* n, int* C, int* deg);
+template <typename Real>
+IoResult ply_load_scene(const char* path, Real* packed, cudaStream_t s, DeviceError* err);
+template <typename Real>
+IoResult ply_save_scene(const char* path, int64_t n, int C, int deg, const Real* packed, cudaStream_t s);
 
 // Normals (K7, K8).
 template <typename Real>

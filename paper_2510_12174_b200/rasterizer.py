@@ -36,6 +36,7 @@ __all__ = [
     "OptimizerState", "TrainConfig", "rasterize", "rasterize_backward", "estimate_normals",
     "normals_backward", "chain_activations", "adam_step", "prune", "bin_and_sort", "fwd_bwd",
     "LogicError", "param_layout", "GroundTruth", "LossReport", "frame_losses", "frame_metrics",
+    "load_scene_ply", "save_scene_ply",
 ]
 
 
@@ -529,6 +530,34 @@ def frame_metrics(frame: MultimodalFrame, gt: GroundTruth, depth_mask: torch.Ten
         p(frame.normals) if gt.normal is not None else None, p(gt.normal), p(normal_mask),
         p(frame.semantics) if have_sem else None, p(gt.labels), p(label_mask), ct.byref(rep)))
     return {f: (getattr(rep, f) if getattr(rep, "has_" + f) else None) for f in _lib.METRIC_FIELDS}
+
+
+# ------------------------------------------------------------ scene I/O
+def load_scene_ply(path: str, dtype=torch.float32, device="cuda") -> Scene:
+    """load_scene_ply (io_ply.hpp, io_ply.cpp:165-263): the payload is decoded
+    on the device straight into one packed parameter buffer; the Scene fields
+    are views of it."""
+    n, C, deg = ct.c_int64(), ct.c_int(), ct.c_int()
+    check(_lib.lib().msplat_ply_scene_info(str(path).encode(), ct.byref(n), ct.byref(C), ct.byref(deg)))
+    n, C, deg = n.value, C.value, deg.value
+    off = param_layout(n, C, deg)
+    dev = torch.device(device)
+    flat = torch.empty(max(off[7], 1), dtype=dtype, device=dev)
+    ctx = _Context.get(dev.index)
+    check(_lib.lib().msplat_load_scene_ply(ctx.h, str(path).encode(), _dtype_code(dtype), flat.data_ptr()))
+    K = (deg + 1) ** 2
+    seg = lambda i, *shape: flat[off[i]:off[i + 1]].view(*shape)  # noqa: E731
+    return Scene(means=seg(0, n, 3), quats=seg(1, n, 4), log_scales=seg(2, n, 3), opacity_logits=seg(3, n),
+                 k=seg(4, n), sh=seg(5, n, 3, K), semantics=seg(6, n, C), num_classes=C, sh_degree=deg)
+
+
+def save_scene_ply(path: str, scene: Scene) -> None:
+    """save_scene_ply (io_ply.cpp:122-163): float64 rows encoded on the device."""
+    n = scene.size()
+    flat = pack_scene(scene) if n else torch.zeros(1, dtype=scene.dtype, device=scene.means.device)
+    ctx = _Context.get(scene.means.device.index)
+    check(_lib.lib().msplat_save_scene_ply(ctx.h, str(path).encode(), _dtype_code(scene.dtype), n,
+                                           scene.num_classes, scene.sh_degree, flat.data_ptr()))
 
 
 def rasterize_backward(scene: Scene, view: CameraView, frame: MultimodalFrame, replay: ReplayState,
