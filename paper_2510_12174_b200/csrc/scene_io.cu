@@ -209,7 +209,7 @@ struct SceneLayout {
 };
 
 // io_ply.cpp:170-211: required columns, SH degree, class count.
-std::string scene_layout(const Header& h, SceneLayout& L, const std::string& path) {
+std::string scene_layout(const Header& h, SceneLayout& L, const std::string& path, bool warn) {
     for (size_t i = 0; i < h.props.size(); ++i) L.index[h.props[i].name] = int(i);
     for (const char* r : {"x", "y", "z", "f_dc_0", "f_dc_1", "f_dc_2", "opacity", "scale_0", "scale_1", "scale_2",
                           "rot_0", "rot_1", "rot_2", "rot_3"})
@@ -223,7 +223,7 @@ std::string scene_layout(const Header& h, SceneLayout& L, const std::string& pat
     while (L.index.count("sem_" + std::to_string(L.C))) ++L.C;
     L.has_k = L.index.count("grad_k") > 0;
     const size_t known = 14 + size_t(L.rest) + size_t(L.C) + (L.has_k ? 1 : 0);
-    if (h.props.size() > known)
+    if (warn && h.props.size() > known)
         for (const Prop& p : h.props) {
             const std::string& n = p.name;
             const bool recognized = n == "x" || n == "y" || n == "z" || n == "opacity" || n == "grad_k" ||
@@ -245,7 +245,7 @@ IoResult ply_scene_info(const char* path, int64_t* n, int* C, int* deg) {
     std::fclose(f);
     if (!err.empty()) return {2, std::string(path) + ": " + err};
     SceneLayout L;
-    if (!(err = scene_layout(h, L, path)).empty()) return {2, std::string(path) + ": " + err};
+    if (!(err = scene_layout(h, L, path, false)).empty()) return {2, std::string(path) + ": " + err};
     *n = int64_t(h.vertex_count);
     *C = L.C;
     *deg = L.deg;
@@ -259,7 +259,7 @@ IoResult ply_load_scene(const char* path, Real* packed, cudaStream_t s, DeviceEr
     Header h;
     std::string err = read_header(f, h);
     SceneLayout L;
-    if (err.empty()) err = scene_layout(h, L, path);
+    if (err.empty()) err = scene_layout(h, L, path, true);
     if (!err.empty()) {
         std::fclose(f);
         return {2, std::string(path) + ": " + err};
