@@ -483,8 +483,16 @@ struct WarpSmemTC {
     uint32_t gid[32];
     uint32_t emask[32];
     uint32_t pos[32];
-    float dD[32];
-    PairQueueTC q;
+    float Tf[32], bgd[32];  // per-pixel T_final and background . dC
+};
+
+// Phase B reads the pair records phase A left in global memory through the
+// same interface as the shared-memory queues.
+struct PairRecords {
+    static constexpr bool kConic = false;
+    const uint32_t *meta, *gid;
+    const float *w, *da, *al, *gs;
+    __device__ float weight(int i) const { return w[i]; }
 };
 
 __host__ __device__ inline int tc_stage_floats(int C) {
@@ -552,7 +560,6 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
     float* const Fb = warp_seed + size_t(32) * sp;  // [kSub][sp] F rows; then FS [kSub][36] in place
     float* const FSs = Fb;
     float* const Wb = Fb + tc_stage_floats(C);      // [kSub][36] blend weights
-    PairQueueTC& Q = ws->q;
 
     const int tile = blockIdx.x;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
@@ -583,13 +590,21 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
     }
     // rasterize_backward.cpp:156-171: nothing to do without blends or seeds.
     if (!(inside && term > 0 && any)) term = 0;
-    ws->dD[lane] = dD;
+    (void)dD;
+    const size_t seg = size_t(tile) * 8 + warp;  // this warp's pair-record segment
     const unsigned act_mask = __ballot_sync(0xffffffffu, term > 0);
-    if (act_mask == 0) return;
+    if (act_mask == 0) {
+        if (lane == 0) a.pair_n[seg] = 0;
+        return;
+    }
     __syncwarp();
 
-    const float pxf = float(x) + 0.5f, pyf = float(y) + 0.5f;
-    const float bg_dot = float(a.rp.bg[0]) * my_seed[0] + float(a.rp.bg[1]) * my_seed[1] + float(a.rp.bg[2]) * my_seed[2];
+    // Read-only per-pixel values live in shared memory and the pixel centre is
+    // recomputed where used: the event loop keeps only the recursion state
+    // (T, accA, lastFS, last_alpha) in registers, so nothing spills to local
+    // memory (whose reloads miss the small L1 left by the carve-out).
+    ws->Tf[lane] = T_final;
+    ws->bgd[lane] = float(a.rp.bg[0]) * my_seed[0] + float(a.rp.bg[1]) * my_seed[1] + float(a.rp.bg[2]) * my_seed[2];
     float T = T_final, accA = 0.f, lastFS = 0.f, last_alpha = 0.f;
     const uint2 range = a.tile_range[tile];
     const uint32_t list0 = range.x;
@@ -597,6 +612,8 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
     const uint2* const evl = a.ev_list + size_t(8) * list0 + size_t(warp) * (range.y - list0);
     const int mtiles2 = (S + 15) / 16;  // GEMM2 channel tiles
     int qn = 0;
+    const int64_t pbase = a.pair_off[seg];
+    const int64_t pcap = a.pair_cap - pbase;  // records this segment may hold
 
     for (int cb = int(nev) - 1; cb >= 0; cb -= 32) {
         __syncwarp();
@@ -641,7 +658,8 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
                 const unsigned fmask = ws->emask[s0 + e];
                 AlphaEval<float> ae;
                 ae.pass = false;
-                if ((fmask >> lane) & 1u) ae = eval_alpha<float>(ws->rec[e], pxf, pyf);
+                if ((fmask >> lane) & 1u)
+                    ae = eval_alpha<float>(ws->rec[e], float(bx + (lane & 7)) + 0.5f, float(by + (lane >> 3)) + 0.5f);
                 const unsigned mask = __ballot_sync(0xffffffffu, ae.pass);
                 float wv = 0.f;
                 if (ae.pass) {
@@ -650,36 +668,27 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
                     const float w = ae.alpha * T;
                     const float FS = FSs[e * kTilePitch + lane];
                     accA = last_alpha * lastFS + (1.f - last_alpha) * accA;
-                    const float dalpha = (FS - accA) * T - T_final * inv * bg_dot;
+                    const float dalpha = (FS - accA) * T - ws->Tf[lane] * inv * ws->bgd[lane];
                     lastFS = FS;
                     last_alpha = ae.alpha;
-                    const int qe = qn + __popc(mask & ((1u << lane) - 1u));
-                    Q.meta[qe] = uint32_t(lane) | (ae.clamped ? (1u << 8) : 0u);
-                    Q.gid[qe] = ws->gid[s0 + e];
-                    Q.w[qe] = w;
-                    Q.da[qe] = dalpha;
-                    Q.al[qe] = ae.alpha;
-                    Q.gs[qe] = ae.gauss;
+                    // the pair record for phase B (backward_pairs_kernel)
+                    const int64_t qe = qn + __popc(mask & ((1u << lane) - 1u));
+                    if (qe < pcap) {
+                        const int64_t o = pbase + qe;
+                        a.pr_meta[o] = uint32_t(lane) | (ae.clamped ? (1u << 8) : 0u);
+                        a.pr_gid[o] = ws->gid[s0 + e];
+                        a.pr_w[o] = w;
+                        a.pr_da[o] = dalpha;
+                        a.pr_al[o] = ae.alpha;
+                        a.pr_gs[o] = ae.gauss;
+                    } else {
+                        raise_error(a.err, kErrPairOverflow, pbase + qe, a.pair_cap);
+                    }
                     wv = w;
                 }
                 Wb[e * kTilePitch + lane] = wv;
                 qn += __popc(mask);
                 __syncwarp();
-                if (qn >= 32) {
-                    flush_pairs<float, false>(a, Q, ws->dD, 32, bx, by);
-                    const int rest = qn - 32;
-                    if (lane < rest) {  // reads >= 32, writes < 32
-                        const int s2 = 32 + lane;
-                        Q.meta[lane] = Q.meta[s2];
-                        Q.gid[lane] = Q.gid[s2];
-                        Q.w[lane] = Q.w[s2];
-                        Q.da[lane] = Q.da[s2];
-                        Q.al[lane] = Q.al[s2];
-                        Q.gs[lane] = Q.gs[s2];
-                    }
-                    qn = rest;
-                    __syncwarp();
-                }
             }
             for (int e = ns; e < kSub; ++e) Wb[e * kTilePitch + lane] = 0.f;
             __syncwarp();
@@ -712,7 +721,33 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
             }
         }
     }
-    if (qn > 0) flush_pairs<float, false>(a, Q, ws->dD, qn, bx, by);
+    if (lane == 0) a.pair_n[seg] = uint32_t(qn < pcap ? qn : pcap);
+}
+
+// K9 phase B (FP32): one warp per (tile, warp) pair-record segment, the
+// geometric gradients of every blended pair 32 at a time (flush_pairs: the
+// depth chain through the ray-ellipsoid adjoint, dopacity / dmean2d / dconic),
+// reduced per Gaussian inside the warp into the acc16 rows.  Split from phase A
+// so that neither carries the other's registers.
+__global__ void __launch_bounds__(256) backward_pairs_kernel(const __grid_constant__ BackwardArgs<float> a, int nseg) {
+    __shared__ float dD_s[8][32];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int seg = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+    if (seg >= nseg) return;
+    const uint32_t n = a.pair_n[seg];
+    if (n == 0) return;
+    const int tile = seg >> 3, w = seg & 7;
+    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    const int bx = tx * kTile + (w & 1) * 8, by = ty * kTile + (w >> 1) * 4;
+    const int x = bx + (lane & 7), y = by + (lane >> 3);
+    dD_s[wib][lane] = (x < a.W && y < a.H) ? a.ddepth[size_t(y) * a.W + x] : 0.f;
+    __syncwarp();
+    const int64_t base = a.pair_off[seg];
+    for (uint32_t k0 = 0; k0 < n; k0 += 32) {
+        const int64_t o = base + k0;
+        const PairRecords q{a.pr_meta + o, a.pr_gid + o, a.pr_w + o, a.pr_da + o, a.pr_al + o, a.pr_gs + o};
+        flush_pairs<float, false>(a, q, dD_s[wib], int(n - k0 < 32 ? n - k0 : 32), bx, by);
+    }
 }
 
 template <typename Real>
@@ -733,6 +768,8 @@ void launch_backward_blend(const BackwardArgs<Real>& a, int ntiles, cudaStream_t
             tc_configured = true;
         }
         backward_kernel_tc<<<ntiles, kThreads, backward_tc_smem_bytes(a.C), s>>>(a);
+        backward_pairs_kernel<<<unsigned((ntiles * 8 + 7) / 8), 256, 0, s>>>(a, ntiles * 8);
+        count_launches(1);
     } else {
         backward_kernel<Real, false><<<ntiles, kThreads, backward_smem_bytes<Real>(a.C), s>>>(a);
     }

@@ -169,7 +169,9 @@ struct msplat_replay {
     DevBuf arec, brec, visible, clamped, depth_key, depth_key_alt, order, order_alt, tile_count, tile_rect,
         count_sorted, offset_sorted, inst_tile, inst_tile_alt, inst_gauss, inst_gauss_alt, tile_range,
         d_inst_count, d_inst_total32, hist, hist_scanned, scan_tiles, terminus, weight_sums, saved_means,
-        saved_k, cap_center, cap_conic, cap_depth, cap_radius, cap_rgb, visible_count, ev_list, ev_count;
+        saved_k, cap_center, cap_conic, cap_depth, cap_radius, cap_rgb, visible_count, ev_list, ev_count, ev_npairs,
+        pair_off, pair_n, pair_scan, pair_total, pr_gid, pr_meta, pr_w, pr_da, pr_al, pr_gs;
+    int64_t pair_cap = 0;  // pair-record capacity of the FP32 split backward
     uint32_t* sorted_gauss = nullptr;
 
     void release_all() {
@@ -178,7 +180,8 @@ struct msplat_replay {
                           &inst_gauss, &inst_gauss_alt, &tile_range, &d_inst_count, &d_inst_total32, &hist,
                           &hist_scanned, &scan_tiles, &terminus, &weight_sums, &saved_means, &saved_k,
                           &cap_center, &cap_conic, &cap_depth, &cap_radius, &cap_rgb, &visible_count, &ev_list,
-                          &ev_count})
+                          &ev_count, &ev_npairs, &pair_off, &pair_n, &pair_scan, &pair_total, &pr_gid, &pr_meta,
+                          &pr_w, &pr_da, &pr_al, &pr_gs})
             b->release();
     }
 };
@@ -274,6 +277,9 @@ msplat_status drain_device_error(msplat_context* ctx, int W) {
         case kErrInstanceOverflow:
             snprintf(buf, sizeof buf, "internal: tile-instance capacity %lld exceeded (needed %lld)", e.b, e.a);
             return set_error(MSPLAT_ERR_RUNTIME, buf);
+        case kErrPairOverflow:
+            snprintf(buf, sizeof buf, "internal: pair-record capacity %lld exceeded", e.b);
+            return set_error(MSPLAT_ERR_RUNTIME, buf);
         case kErrMiouLabel:
             return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "miou: label out of range");
         case kErrLabelRange:
@@ -317,6 +323,7 @@ msplat_status size_replay(msplat_replay* r, int dtype, int64_t n, int C, int deg
     CUDA_TRY(r->inst_tile_alt.ensure(ic * 4));
     CUDA_TRY(r->ev_list.ensure(ic * 8 * sizeof(uint2)));  // 8 warps x (position, mask) per instance
     CUDA_TRY(r->ev_count.ensure(size_t(tiles) * 8 * 4));
+    CUDA_TRY(r->ev_npairs.ensure(size_t(tiles) * 8 * 4));
     CUDA_TRY(r->inst_gauss.ensure(ic * 4));
     CUDA_TRY(r->inst_gauss_alt.ensure(ic * 4));
     CUDA_TRY(r->tile_range.ensure(size_t(tiles) * 8));
@@ -478,6 +485,7 @@ msplat_status rasterize_impl(msplat_context* ctx, const msplat_scene* s, const m
     a.weight_sums = (r->capture & 2) ? r->weight_sums.as<Real>() : nullptr;
     a.ev_list = r->ev_list.as<uint2>();
     a.ev_count = r->ev_count.as<uint32_t>();
+    a.ev_npairs = r->ev_npairs.as<uint32_t>();
     a.err = ctx->d_err;
     ctx->timer.begin(MSPLAT_STAGE_FORWARD, ctx->stream);
     launch_forward<Real>(a, r->tiles_x * r->tiles_y, ctx->stream);
@@ -589,6 +597,43 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
                          ctx->det_vals.as<uint32_t>(), ctx->det_vals_alt.as<uint32_t>(),
                          ctx->det_range.as<uint2>(), r->hist.as<uint32_t>(), r->hist_scanned.as<uint32_t>(),
                          r->scan_tiles.as<uint32_t>()};
+    }
+    if (sizeof(Real) == 4 && !ctx->deterministic) {
+        // FP32 split backward: segment offsets of the pair records (scan of the
+        // forward's per-warp pair counts) and their capacity, grown whenever
+        // the stream is not being captured.
+        msplat_replay* rw = const_cast<msplat_replay*>(r);  // device scratch of the replay
+        const int64_t nseg = int64_t(r->tiles_x) * r->tiles_y * 8;
+        CUDA_TRY(rw->pair_off.ensure(size_t(nseg) * 4));
+        CUDA_TRY(rw->pair_n.ensure(size_t(nseg) * 4));
+        CUDA_TRY(rw->pair_scan.ensure((size_t(nseg) + kScanTile - 1) / kScanTile * 4 + 8));
+        CUDA_TRY(rw->pair_total.ensure(8));
+        device_exclusive_scan<uint32_t>(r->ev_npairs.as<uint32_t>(), rw->pair_off.as<uint32_t>(), nullptr, nseg,
+                                        rw->pair_scan.as<uint32_t>(), rw->pair_total.as<uint32_t>(), st);
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        CUDA_TRY(cudaStreamIsCapturing(st, &cs));
+        if (cs == cudaStreamCaptureStatusNone) {
+            CUDA_TRY(cudaMemcpyAsync(ctx->h_u64, rw->pair_total.p, 4, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            const int64_t need = int64_t(*reinterpret_cast<uint32_t*>(ctx->h_u64));
+            if (need > rw->pair_cap) {
+                const int64_t cap = need + need / 4 + 4096;
+                for (DevBuf* b : {&rw->pr_gid, &rw->pr_meta, &rw->pr_w, &rw->pr_da, &rw->pr_al, &rw->pr_gs})
+                    CUDA_TRY(b->ensure(size_t(cap) * 4));
+                rw->pair_cap = cap;
+            }
+        }
+        if (rw->pair_cap == 0) return set_error(MSPLAT_ERR_RUNTIME, "rasterize_backward: capture before any eager call");
+        BackwardArgs<float>& af = reinterpret_cast<BackwardArgs<float>&>(a);
+        af.pair_off = rw->pair_off.as<uint32_t>();
+        af.pair_n = rw->pair_n.as<uint32_t>();
+        af.pr_gid = rw->pr_gid.as<uint32_t>();
+        af.pr_meta = rw->pr_meta.as<uint32_t>();
+        af.pr_w = rw->pr_w.as<float>();
+        af.pr_da = rw->pr_da.as<float>();
+        af.pr_al = rw->pr_al.as<float>();
+        af.pr_gs = rw->pr_gs.as<float>();
+        af.pair_cap = rw->pair_cap;
     }
     ctx->timer.begin(MSPLAT_STAGE_BACKWARD, st);
     launch_backward_blend<Real>(a, r->tiles_x * r->tiles_y, st);

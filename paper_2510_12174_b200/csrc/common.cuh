@@ -27,6 +27,7 @@ enum ErrCode : int {
     kErrInstanceOverflow = 7,  // internal: tile-instance buffer too small (a = needed)
     kErrLabelRange = 8,        // losses.cpp:245-249 (a = pixel, b = label)
     kErrMiouLabel = 9,         // metrics.cpp:165-166 (a = pixel, b = label)
+    kErrPairOverflow = 10,     // internal: pair-record buffer too small (a = needed, b = capacity)
 };
 
 struct DeviceError {

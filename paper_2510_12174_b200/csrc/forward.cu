@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kThreads, 2) forward_kernel(const __grid_const
     int qn = 0;
     unsigned long long own = 0;  // queue entries owned by this pixel
     uint2* const evl = a.ev_list ? a.ev_list + size_t(8) * range.x + size_t(warp) * len : nullptr;
-    uint32_t n_ev = 0;
+    uint32_t n_ev = 0, n_pairs = 0;
 
     for (int c = 0; c * 32 < len; ++c) {
         if (__all_sync(0xffffffffu, done)) break;
@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(kThreads, 2) forward_kernel(const __grid_const
             if (evl) {  // the backward replays exactly these events
                 if (lane == 0) evl[n_ev] = make_uint2(uint32_t(c * 32 + slot), mask);
                 ++n_ev;
+                n_pairs += __popc(mask);
             }
             const uint32_t g = ws->gid[slot];
             if (ae.pass) {
@@ -214,7 +215,10 @@ __global__ void __launch_bounds__(kThreads, 2) forward_kernel(const __grid_const
         }
     }
     if (qn > 0) flush_depth<Real>(a, ws, qn, bx, by, dep, unsigned(own));
-    if (a.ev_count && lane == 0) a.ev_count[size_t(tile) * 8 + warp] = n_ev;
+    if (a.ev_count && lane == 0) {
+        a.ev_count[size_t(tile) * 8 + warp] = n_ev;
+        a.ev_npairs[size_t(tile) * 8 + warp] = n_pairs;
+    }
     if (!inside) return;
     col0 += T * Real(a.rp.bg[0]);
     col1 += T * Real(a.rp.bg[1]);

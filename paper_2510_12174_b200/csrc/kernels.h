@@ -102,6 +102,7 @@ struct ForwardArgs {
     // entries; ev_count[tile * 8 + warp] = number of events.
     uint2* ev_list;
     uint32_t* ev_count;
+    uint32_t* ev_npairs;  // blended pairs per (tile, warp): the backward's pair-record segments
     DeviceError* err;
 };
 template <typename Real>
@@ -203,6 +204,13 @@ struct BackwardArgs {
     RawParams<Real> raw;
     const uint2* ev_list;     // the forward's blend-event log (ForwardArgs::ev_list)
     const uint32_t* ev_count;
+    // FP32 split backward: per-(tile, warp) pair-record segments written by the
+    // tensor-core phase A and consumed by the phase-B kernel (SoA, pair_cap).
+    const uint32_t* pair_off;  // [tiles * 8] exclusive scan of ev_npairs
+    uint32_t* pair_n;          // [tiles * 8] pairs phase A wrote
+    uint32_t *pr_gid, *pr_meta;
+    float *pr_w, *pr_da, *pr_al, *pr_gs;
+    int64_t pair_cap;
     const Real* T_final;
     const int32_t* terminus;
     const Real *dcolor, *ddepth, *dsem, *dkmap;  // planar pixel grads
