@@ -728,8 +728,9 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
 // geometric gradients of every blended pair 32 at a time (flush_pairs: the
 // depth chain through the ray-ellipsoid adjoint, dopacity / dmean2d / dconic),
 // reduced per Gaussian inside the warp into the acc16 rows.  Split from phase A
-// so that neither carries the other's registers.
-__global__ void __launch_bounds__(256) backward_pairs_kernel(const __grid_constant__ BackwardArgs<float> a, int nseg) {
+// so that neither carries the other's registers; 5 blocks/SM (48 registers,
+// spills hit the large L1 this kernel leaves) hides its gather latency best.
+__global__ void __launch_bounds__(256, 5) backward_pairs_kernel(const __grid_constant__ BackwardArgs<float> a, int nseg) {
     __shared__ float dD_s[8][32];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int seg = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
