@@ -43,11 +43,13 @@ out.append(f"| **total** | {sum(v[0] for v in agg.values())} | {tot:.1f} | 100% 
            f"{sum(v[2] for v in agg.values()) / 1e6:.1f} MB (all) |")
 open(sys.argv[2], "w").write("\n".join(out) + "\n")
 print("\n".join(out))
+# per-launch DRAM traffic of each timed stage (a stage may be several kernels:
+# K9 = tensor-core phase A + pair-record phase B)
 traffic = {}
 for k, v in agg.items():
-    for stage, pref in (("backward", "backward_kernel"), ("forward", "forward_kernel"),
-                        ("preprocess", "preprocess_kernel"), ("proj_bwd", "projection_backward_kernel")):
-        if k.startswith(pref):
-            traffic[stage] = v[2] / v[0]
+    for stage, prefs in (("backward", ("backward_kernel", "backward_pairs_kernel")), ("forward", ("forward_kernel",)),
+                         ("preprocess", ("preprocess_kernel",)), ("proj_bwd", ("projection_backward_kernel",))):
+        if any(k.startswith(pref) for pref in prefs):
+            traffic[stage] = traffic.get(stage, 0.0) + v[2] / v[0]
 path = os.path.join(os.path.dirname(sys.argv[2]), "ncu_traffic.json")
 json.dump(traffic, open(path, "w"), indent=1)
