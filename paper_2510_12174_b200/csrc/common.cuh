@@ -67,7 +67,7 @@ struct Vec3T {
 // Per-visible-Gaussian records written by K1 and gathered per tile by K6/K9.
 // Alpha-test record (everything a visited pair needs), 12 Reals.
 template <typename Real>
-struct __align__(16) AlphaRec {  // 48 B (FP32): three 16-byte stores / loads
+struct __align__(16) AlphaRec {  // 64 B (FP32): four 16-byte stores / loads
     Real cx, cy;      // splat centre (pixels)
     Real ca, cb, cc;  // conic (xx, xy, yy)
     Real opacity;     // activated alpha (logistic of the logit)
@@ -77,6 +77,9 @@ struct __align__(16) AlphaRec {  // 48 B (FP32): three 16-byte stores / loads
     // power >= log_thr - 1e-3 grown by 0.1% + 1e-3 px).  Used only to skip
     // pairs that would fail the alpha test anyway: results are unchanged.
     Real bx0, bx1, by0, by1;
+    // View-dependent colour and gradient factor: the forward reads them with
+    // the record it already stages (no per-event gather from BlendRec).
+    Real rgb[3], k;
 };
 
 // Blend record (everything a blended pair needs beyond the alpha test).

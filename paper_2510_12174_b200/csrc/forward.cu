@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, 2) forward_kernel(const __grid_const
                     raise_error(a.err, kErrNonFiniteBlend, (long long)y * a.W + x, g);
                     done = true;
                 }
-                const BlendRec<Real>& br = a.brec[g];
+                const AlphaRec<Real>& br = ws->rec[slot];
                 const Real w = ae.alpha * T;
                 col0 += w * br.rgb[0];
                 col1 += w * br.rgb[1];

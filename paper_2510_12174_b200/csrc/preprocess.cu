@@ -299,6 +299,8 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(const __grid_co
             ar.bx1 = ar.by1 = Real(-1e30);
         }
     }
+    for (int j = 0; j < 3; ++j) ar.rgb[j] = Real(rgb[j]);
+    ar.k = a.k[i];
     a.arec[i] = ar;
 
     BlendRec<Real> br;
