@@ -48,6 +48,7 @@ def parse():
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-train-step", action="store_true", help="skip the full training-iteration measurement")
     p.add_argument("--ref-budget-s", type=float, default=150.0, help="wall budget of the reference arm")
     return p.parse_args()
 
@@ -372,6 +373,12 @@ def run_ours(args, rank, world, local_rank):
         e2e = run_e2e(args, rank, world, dev, scene, grads, gflat, flat, opt, tc, rc, nc, cams, frame, replay,
                       pixs, step_fn=None)
 
+    train_step = None
+    if rank == 0 and world == 1 and not args.no_train_step:
+        try:
+            train_step = run_train_step(args, dev, scene, flat, opt, tc, rc, nc, cams)
+        except Exception as e:  # noqa: BLE001
+            train_step = {"error": str(e)}
     if rank != 0:
         return None
     HW = Wd * Ht
@@ -416,10 +423,59 @@ def run_ours(args, rank, world, local_rank):
                             "frac_of_fp32": F_alg / (render_ms / 1000.0) / 1e12 / fpk,
                             "roofline_bound_frac": max(t_hbm, t_fp32) / (render_ms / 1000.0)},
         "stage_ms_per_view": {k: round(v, 4) for k, v in per_launch.items()},
+        "train_step": train_step,
         "counters": dict(counters, pixels=HW, P=P, Pc_blended_pairs=Pc, Pb_backward_pairs=Pb,
                          Pf_forward_pairs=Pf),
     }
     return line
+
+
+def run_train_step(args, dev, scene, flat, opt, tc, rc, nc, cams, iters=8, warm=2):
+    """One full device-resident training iteration per view, as trainer.cpp:289-328
+    (SURVEY.md 8f #1-#2): rasterize, estimate_normals, frame_losses (the six
+    losses, combine, seed assembly and the normal chain), rasterize_backward,
+    chain_activations and adam_step, through the public API on synthetic ground
+    truth.  Timed with CUDA events on the launching stream (informational; the
+    headline metric is the reference-comparable fwd+bwd step)."""
+    import torch
+    import paper_2510_12174_b200 as M
+    W, H, C = args.width, args.height, args.classes
+    g = torch.Generator(device=dev).manual_seed(5)
+    gts = []
+    for _ in range(2):
+        normal = torch.randn(3, H, W, generator=g, device=dev)
+        normal = normal / normal.norm(dim=0, keepdim=True)
+        gts.append(M.GroundTruth(torch.rand(3, H, W, generator=g, device=dev),
+                                 1.5 + 3.0 * torch.rand(H, W, generator=g, device=dev), normal,
+                                 torch.randint(0, C, (H, W), generator=g, device=dev).to(torch.uint8)))
+    replay = M.ReplayState()
+    lambdas = (1.0, 0.1, 0.1, 0.1, 0.1, 0.1)
+
+    def one(i):
+        view = cams[i % len(cams)]
+        frame = M.rasterize(scene, view, rc, replay)
+        M.estimate_normals(frame.depth, frame.transmittance, view, nc, frame.normals)
+        _, pix = M.frame_losses(frame, gts[i % 2], view, nc, lambdas, sync=False)
+        gb = M.rasterize_backward(scene, view, frame, replay, pix)
+        M.chain_activations(gb, scene)
+        M.adam_step(scene, gb, opt, tc, packed_params=flat, packed_grads=M.rasterizer.pack_grads(gb))
+
+    for i in range(warm):
+        one(i)
+    torch.cuda.synchronize(dev)
+    st = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for i in range(iters):
+        one(warm + i)
+    e1.record(st)
+    torch.cuda.synchronize(dev)
+    M.rasterizer.check_device_errors(dev.index)
+    ms = e0.elapsed_time(e1) / iters
+    return {"ms_per_iteration": ms, "iterations_per_s": 1000.0 / ms, "iterations": iters,
+            "includes": "rasterize, estimate_normals, frame_losses (l1, ssim, normal, depth, seg, k + combine + "
+                        "seed assembly + normal chain), rasterize_backward, chain_activations, adam_step; one view "
+                        "per iteration (trainer.cpp:289-328), public Python API, synthetic ground truth"}
 
 
 def run_e2e(args, rank, world, dev, scene, grads, gflat, flat, opt, tc, rc, nc, cams, frame, replay, pixs,

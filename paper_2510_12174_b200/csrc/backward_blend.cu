@@ -470,19 +470,11 @@ namespace {
 constexpr int kSub = 8;         // events per sub-batch (mma N)
 constexpr int kTilePitch = 36;  // FS / W tiles [kSub][36]: conflict-free fragment stores and row reads
 
-struct PairQueueTC {
-    static constexpr bool kConic = false;  // centre / conic re-read from the splat record
-    __device__ float weight(int i) const { return w[i]; }
-    uint32_t meta[kQueue];
-    uint32_t gid[kQueue];
-    float w[kQueue], da[kQueue], al[kQueue], gs[kQueue];
-};
 
 struct WarpSmemTC {
     AlphaRec<float> rec[kSub];
     uint32_t gid[32];
     uint32_t emask[32];
-    uint32_t pos[32];
     float Tf[32], bgd[32];  // per-pixel T_final and background . dC
 };
 
@@ -623,7 +615,6 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
                 const uint2 ev = evl[e];
                 ws->gid[lane] = a.inst_gauss[list0 + ev.x];
                 ws->emask[lane] = ev.y & act_mask;
-                ws->pos[lane] = ev.x;
             }
         }
         __syncwarp();
