@@ -25,8 +25,8 @@ for r in csv.reader(io.StringIO(src)):
     if r[0] == "Line No":
         hdr = r
         continue
-    if hdr and r[0] != "":
-        per.setdefault(func, []).append((fname, r))
+    if hdr and r[0] != "":  # headers differ per file section: key each row by its own
+        per.setdefault(func, []).append((fname, {**dict(zip(hdr, r)), "Source": r[1]}))
 
 
 def f(x):
@@ -36,18 +36,19 @@ def f(x):
         return 0.0
 
 
-reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
-idx = {k: hdr.index(k) for k in reasons}
-tot_i = hdr.index("Warp Stall Sampling (All Samples)")
-ins_i = hdr.index("Instructions Executed")
+reasons = sorted({h for rows in per.values() for _, r in rows for h in r
+                  if h.startswith("stall_") and "Not Issued" not in h})
+idx = {k: k for k in reasons}
+tot_i = "Warp Stall Sampling (All Samples)"
+ins_i = "Instructions Executed"
 for func, rows in per.items():
     if want not in func:
         continue
     T = sum(f(r[tot_i]) for _, r in rows) or 1
-    agg = {k: sum(f(r[idx[k]]) for _, r in rows) / T * 100 for k in reasons}
+    agg = {k: sum(f(r.get(idx[k], '0')) for _, r in rows) / T * 100 for k in reasons}
     print(f"== {func}  (samples {int(T)})")
     print("overall:", ", ".join(f"{k[6:]} {v:.1f}%" for k, v in sorted(agg.items(), key=lambda kv: -kv[1]) if v > 0.5))
     for fn, r in sorted(rows, key=lambda x: -f(x[1][tot_i]))[:top]:
-        parts = sorted(((f(r[idx[k]]), k[6:]) for k in reasons), reverse=True)[:3]
-        print(f"{f(r[tot_i]) / T * 100:5.1f}% {fn}:{r[0]:>4} inst={int(f(r[ins_i])):>10} "
-              + " ".join(f"{n}={v / max(f(r[tot_i]), 1) * 100:.0f}%" for v, n in parts if v > 0) + f" | {r[1].strip()[:70]}")
+        parts = sorted(((f(r.get(idx[k], '0')), k[6:]) for k in reasons), reverse=True)[:3]
+        print(f"{f(r[tot_i]) / T * 100:5.1f}% {fn}:{r["Line No"]:>4} inst={int(f(r[ins_i])):>10} "
+              + " ".join(f"{n}={v / max(f(r[tot_i]), 1) * 100:.0f}%" for v, n in parts if v > 0) + f" | {r["Source"].strip()[:70]}")
