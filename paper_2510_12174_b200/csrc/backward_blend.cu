@@ -111,6 +111,81 @@ __device__ __forceinline__ Real seg_sum(Real v, const bool* same) {
     return v;
 }
 
+// The depth chain of one blended pair (rasterizer_backward.cpp:205-218): the
+// ray-ellipsoid midpoint depth's adjoint into dmean (v[6..8]), drotation
+// (v[9..12]) and dscale (v[13..15]); dd = dL/ddepth(pixel) * w.
+template <typename Real>
+__device__ __forceinline__ void depth_chain_adjoint(const BackwardArgs<Real>& a, uint32_t g, int xL, int yL, Real dd,
+                                                    Real (&v)[16]) {
+    const Real sigma = Real(a.rp.sigma_scale);
+    const BlendRec<Real>& br = a.brec[g];
+    const PixelRay<Real> ray = make_ray<Real>(a.cam, xL, yL);
+    const HitEval<Real> h = intersect<Real>(br, ray, a.cam, a.raw, g);
+    if (h.hit) {
+        if constexpr (sizeof(Real) == 4) {
+            // Adjoint around the small midpoint offset p_l = v_l + t d_l
+            // (p_s = p_l / axes), algebraically the reference's:
+            //   g_vs = -k d_s, g_ds = -k (p_s + t d_s), k = g_t / a
+            //   dscale = 2k (d_s o p_s) / s
+            //   dR = -k [(R p_l)(d_s/axes)^T + d (p_s/axes)^T]
+            if (!(fabsf(h.a) < 1e-12f)) {
+                const Real kk = dd * ray.dz / h.a;
+                const Real t = h.t_mid;
+                Real ps[3], pl[3], ga[3], gb[3];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    pl[i] = br.vl[i] + t * h.dl[i];
+                    ps[i] = pl[i] * br.inv_axes[i];
+                    v[13 + i] = Real(2) * kk * h.ds[i] * ps[i] * sigma * br.inv_axes[i];
+                    ga[i] = h.ds[i] * br.inv_axes[i];
+                    gb[i] = ps[i] * br.inv_axes[i];
+                }
+                Real Rp[3];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    v[6 + i] = kk * (br.Rt[0 * 3 + i] * ga[0] + br.Rt[1 * 3 + i] * ga[1] + br.Rt[2 * 3 + i] * ga[2]);
+                    Rp[i] = br.Rt[0 * 3 + i] * pl[0] + br.Rt[1 * 3 + i] * pl[1] + br.Rt[2 * 3 + i] * pl[2];
+                }
+                Real G[9];
+#pragma unroll
+                for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+                    for (int cc2 = 0; cc2 < 3; ++cc2)
+                        G[rr * 3 + cc2] = -kk * (Rp[rr] * ga[cc2] + ray.d[rr] * gb[cc2]);
+                quat_rotation_backward<Real>(br.q, G, v + 9);
+            }
+        } else if (!(fabs(h.a) < 1e-12)) {
+            // The reference's formulation (geometry.cpp:70-105).
+            const Real g_t = dd * ray.dz;
+            Real gvs[3], gds[3], gvl[3], gdl[3];
+            const Real ba2 = h.b / (h.a * h.a);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                gvs[i] = g_t * (-h.ds[i] / h.a);
+                gds[i] = g_t * (ba2 * h.ds[i] - br.vs[i] / h.a);
+                v[13 + i] = -((gvs[i] * br.vs[i] + gds[i] * h.ds[i]) * sigma / br.axes[i]);
+                gvl[i] = gvs[i] / br.axes[i];
+                gdl[i] = gds[i] / br.axes[i];
+            }
+            Real vv[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                v[6 + i] = -(br.Rt[0 * 3 + i] * gvl[0] + br.Rt[1 * 3 + i] * gvl[1] + br.Rt[2 * 3 + i] * gvl[2]);
+                vv[i] = br.Rt[0 * 3 + i] * br.vl[0] + br.Rt[1 * 3 + i] * br.vl[1] + br.Rt[2 * 3 + i] * br.vl[2];
+            }
+            Real G[9];
+#pragma unroll
+            for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+                for (int cc2 = 0; cc2 < 3; ++cc2) G[rr * 3 + cc2] = vv[rr] * gvl[cc2] + ray.d[rr] * gdl[cc2];
+            quat_rotation_backward<Real>(br.q, G, v + 9);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) v[6 + i] = dd * Real(a.cam.Rw2c[6 + i]);
+    }
+}
+
 // Phase B on the first n queue entries (n <= 32): per-pair geometric
 // gradients, segmented by Gaussian, one atomic per value per Gaussian.
 template <typename Real, bool DET, typename Queue>
@@ -165,75 +240,7 @@ __device__ __forceinline__ void flush_pairs(const BackwardArgs<Real>& a, const Q
         }
         // Depth chain (rasterizer_backward.cpp:205-218).
         const Real dd = dDw[L] * w;
-        if (dd != Real(0)) {
-            const Real sigma = Real(a.rp.sigma_scale);
-            const BlendRec<Real>& br = a.brec[g];
-            const PixelRay<Real> ray = make_ray<Real>(a.cam, xL, yL);
-            const HitEval<Real> h = intersect<Real>(br, ray, a.cam, a.raw, g);
-            if (h.hit) {
-                if constexpr (sizeof(Real) == 4) {
-                    // Adjoint around the small midpoint offset p_l = v_l + t d_l
-                    // (p_s = p_l / axes), algebraically the reference's:
-                    //   g_vs = -k d_s, g_ds = -k (p_s + t d_s), k = g_t / a
-                    //   dscale = 2k (d_s o p_s) / s
-                    //   dR = -k [(R p_l)(d_s/axes)^T + d (p_s/axes)^T]
-                    if (!(fabsf(h.a) < 1e-12f)) {
-                        const Real kk = dd * ray.dz / h.a;
-                        const Real t = h.t_mid;
-                        Real ps[3], pl[3], ga[3], gb[3];
-#pragma unroll
-                        for (int i = 0; i < 3; ++i) {
-                            pl[i] = br.vl[i] + t * h.dl[i];
-                            ps[i] = pl[i] * br.inv_axes[i];
-                            v[13 + i] = Real(2) * kk * h.ds[i] * ps[i] * sigma * br.inv_axes[i];
-                            ga[i] = h.ds[i] * br.inv_axes[i];
-                            gb[i] = ps[i] * br.inv_axes[i];
-                        }
-                        Real Rp[3];
-#pragma unroll
-                        for (int i = 0; i < 3; ++i) {
-                            v[6 + i] = kk * (br.Rt[0 * 3 + i] * ga[0] + br.Rt[1 * 3 + i] * ga[1] + br.Rt[2 * 3 + i] * ga[2]);
-                            Rp[i] = br.Rt[0 * 3 + i] * pl[0] + br.Rt[1 * 3 + i] * pl[1] + br.Rt[2 * 3 + i] * pl[2];
-                        }
-                        Real G[9];
-#pragma unroll
-                        for (int rr = 0; rr < 3; ++rr)
-#pragma unroll
-                            for (int cc2 = 0; cc2 < 3; ++cc2)
-                                G[rr * 3 + cc2] = -kk * (Rp[rr] * ga[cc2] + ray.d[rr] * gb[cc2]);
-                        quat_rotation_backward<Real>(br.q, G, v + 9);
-                    }
-                } else if (!(fabs(h.a) < 1e-12)) {
-                    // The reference's formulation (geometry.cpp:70-105).
-                    const Real g_t = dd * ray.dz;
-                    Real gvs[3], gds[3], gvl[3], gdl[3];
-                    const Real ba2 = h.b / (h.a * h.a);
-#pragma unroll
-                    for (int i = 0; i < 3; ++i) {
-                        gvs[i] = g_t * (-h.ds[i] / h.a);
-                        gds[i] = g_t * (ba2 * h.ds[i] - br.vs[i] / h.a);
-                        v[13 + i] = -((gvs[i] * br.vs[i] + gds[i] * h.ds[i]) * sigma / br.axes[i]);
-                        gvl[i] = gvs[i] / br.axes[i];
-                        gdl[i] = gds[i] / br.axes[i];
-                    }
-                    Real vv[3];
-#pragma unroll
-                    for (int i = 0; i < 3; ++i) {
-                        v[6 + i] = -(br.Rt[0 * 3 + i] * gvl[0] + br.Rt[1 * 3 + i] * gvl[1] + br.Rt[2 * 3 + i] * gvl[2]);
-                        vv[i] = br.Rt[0 * 3 + i] * br.vl[0] + br.Rt[1 * 3 + i] * br.vl[1] + br.Rt[2 * 3 + i] * br.vl[2];
-                    }
-                    Real G[9];
-#pragma unroll
-                    for (int rr = 0; rr < 3; ++rr)
-#pragma unroll
-                        for (int cc2 = 0; cc2 < 3; ++cc2) G[rr * 3 + cc2] = vv[rr] * gvl[cc2] + ray.d[rr] * gdl[cc2];
-                    quat_rotation_backward<Real>(br.q, G, v + 9);
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 3; ++i) v[6 + i] = dd * Real(a.cam.Rw2c[6 + i]);
-            }
-        }
+        if (dd != Real(0)) depth_chain_adjoint<Real>(a, g, xL, yL, dd, v);
     }
     // Deterministic mode: this (instance, warp) owns a private slot; plain
     // read-modify-write in program order, reduced later in a fixed order.
@@ -263,6 +270,58 @@ __device__ __forceinline__ void flush_pairs(const BackwardArgs<Real>& a, const Q
         }
     }
     __syncwarp();
+}
+
+// K9 phase B on n (<= 32) of the 16-byte pair records phase A wrote
+// ({gid, pixel lane, v0 = G dalpha, dd = dD w}): dopacity = v0, dmean2d / dconic
+// from dpower = opacity v0 (= alpha dalpha; 0 when alpha was clamped), the
+// depth chain from dd; segmented by Gaussian, one vector reduction per row.
+__device__ __forceinline__ void flush_records(const BackwardArgs<float>& a, const uint4* rec, int n, int bx, int by) {
+    const int lane = threadIdx.x & 31;
+    const bool act = lane < n;
+    const uint4 r = act ? rec[lane] : make_uint4(0xffffffffu - lane, 0u, 0u, 0u);  // padding: unique keys
+    const uint32_t g = r.x;
+    bool same[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const uint32_t o = __shfl_down_sync(0xffffffffu, g, 1 << k);
+        same[k] = (lane + (1 << k) < 32) && o == g;
+    }
+    const uint32_t g_prev = __shfl_up_sync(0xffffffffu, g, 1);
+    const bool head = act && (lane == 0 || g_prev != g);
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = 0.f;
+    if (act) {
+        const int L = int(r.y);
+        const int xL = bx + (L & 7), yL = by + (L >> 3);
+        const float v0 = __uint_as_float(r.z), dd = __uint_as_float(r.w);
+        if (v0 != 0.f) {  // rasterizer_backward.cpp:234-244
+            const AlphaRec<float>& ar = a.arec[g];
+            const float4 c0 = *reinterpret_cast<const float4*>(&ar.cx);        // cx, cy, ca, cb
+            const float2 c1 = *reinterpret_cast<const float2*>(&ar.cc);        // cc, opacity
+            const float dx = float(xL) + 0.5f - c0.x, dy = float(yL) + 0.5f - c0.y;
+            const float dpower = c1.y * v0;
+            v[0] = v0;
+            v[1] = dpower * (c0.z * dx + c0.w * dy);
+            v[2] = dpower * (c0.w * dx + c1.x * dy);
+            v[3] = dpower * (-0.5f * dx * dx);
+            v[4] = dpower * (-0.5f * dx * dy);
+            v[5] = dpower * (-0.5f * dy * dy);
+        }
+        if (dd != 0.f) depth_chain_adjoint<float>(a, g, xL, yL, dd, v);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = seg_sum<float>(v[i], same);
+    if (head) {
+        float* const row = a.acc16 + size_t(g) * 16;
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+            if (v[i] != 0.f || v[i + 1] != 0.f || v[i + 2] != 0.f || v[i + 3] != 0.f)
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(row + i), "f"(v[i]), "f"(v[i + 1]),
+                             "f"(v[i + 2]), "f"(v[i + 3])
+                             : "memory");
+    }
 }
 
 }  // namespace
@@ -476,16 +535,9 @@ struct WarpSmemTC {
     uint32_t gid[32];
     uint32_t emask[32];
     float Tf[32], bgd[32];  // per-pixel T_final and background . dC
+    float dDs[32];          // per-pixel dL/ddepth
 };
 
-// Phase B reads the pair records phase A left in global memory through the
-// same interface as the shared-memory queues.
-struct PairRecords {
-    static constexpr bool kConic = false;
-    const uint32_t *meta, *gid;
-    const float *w, *da, *al, *gs;
-    __device__ float weight(int i) const { return w[i]; }
-};
 
 __host__ __device__ inline int tc_stage_floats(int C) {
     const int sp = seed_pitch(C);
@@ -506,35 +558,29 @@ size_t backward_tc_smem_bytes(int C) {
 // pieces of all n rows, so one pass issues every copy.
 __device__ __forceinline__ void stage_rows_tc(float* Fb, int sp, const BlendRec<float>* brec, const float* semantics,
                                               int C, const uint32_t* gid, int n, int lane) {
-    if ((C & 1) == 0) {
-        const int per = 1 + C / 2;  // pieces per row
-        for (int q = lane; q < n * per; q += 32) {
-            const int e = q / per, j = q - e * per;
-            const uint32_t g = gid[e];
-            if (j == 0) {
-                const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + e * sp));
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(&brec[g].rgb[0]) : "memory");
-            } else {
-                const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + e * sp + 4 + 2 * (j - 1)));
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst),
-                             "l"(semantics + size_t(g) * C + 2 * (j - 1))
-                             : "memory");
-            }
+    // Piece q = e * per + j of the batch; lanes advance by 32 pieces without a
+    // division per step.
+    const bool even = (C & 1) == 0;
+    const int per = 1 + (even ? C / 2 : C);
+    int e = lane / per, j = lane - e * per;
+    for (int q = lane; q < n * per; q += 32) {
+        const uint32_t g = gid[e];
+        if (j == 0) {
+            const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + e * sp));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(&brec[g].rgb[0]) : "memory");
+        } else if (even) {
+            const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + e * sp + 4 + 2 * (j - 1)));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(semantics + size_t(g) * C + 2 * (j - 1))
+                         : "memory");
+        } else {
+            const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + e * sp + 4 + (j - 1)));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(semantics + size_t(g) * C + (j - 1))
+                         : "memory");
         }
-    } else {
-        const int per = 1 + C;
-        for (int q = lane; q < n * per; q += 32) {
-            const int e = q / per, j = q - e * per;
-            const uint32_t g = gid[e];
-            if (j == 0) {
-                const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + e * sp));
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(&brec[g].rgb[0]) : "memory");
-            } else {
-                const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + e * sp + 4 + (j - 1)));
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst),
-                             "l"(semantics + size_t(g) * C + (j - 1))
-                             : "memory");
-            }
+        j += 32;
+        while (j >= per) {
+            j -= per;
+            ++e;
         }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -582,7 +628,6 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
     }
     // rasterize_backward.cpp:156-171: nothing to do without blends or seeds.
     if (!(inside && term > 0 && any)) term = 0;
-    (void)dD;
     const size_t seg = size_t(tile) * 8 + warp;  // this warp's pair-record segment
     const unsigned act_mask = __ballot_sync(0xffffffffu, term > 0);
     if (act_mask == 0) {
@@ -596,6 +641,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
     // (T, accA, lastFS, last_alpha) in registers, so nothing spills to local
     // memory (whose reloads miss the small L1 left by the carve-out).
     ws->Tf[lane] = T_final;
+    ws->dDs[lane] = dD;
     ws->bgd[lane] = float(a.rp.bg[0]) * my_seed[0] + float(a.rp.bg[1]) * my_seed[1] + float(a.rp.bg[2]) * my_seed[2];
     float T = T_final, accA = 0.f, lastFS = 0.f, last_alpha = 0.f;
     const uint2 range = a.tile_range[tile];
@@ -665,13 +711,9 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
                     // the pair record for phase B (backward_pairs_kernel)
                     const int64_t qe = qn + __popc(mask & ((1u << lane) - 1u));
                     if (qe < pcap) {
-                        const int64_t o = pbase + qe;
-                        a.pr_meta[o] = uint32_t(lane) | (ae.clamped ? (1u << 8) : 0u);
-                        a.pr_gid[o] = ws->gid[s0 + e];
-                        a.pr_w[o] = w;
-                        a.pr_da[o] = dalpha;
-                        a.pr_al[o] = ae.alpha;
-                        a.pr_gs[o] = ae.gauss;
+                        const float v0 = ae.clamped ? 0.f : ae.gauss * dalpha;
+                        a.pr[pbase + qe] = make_uint4(ws->gid[s0 + e], uint32_t(lane), __float_as_uint(v0),
+                                                      __float_as_uint(ws->dDs[lane] * w));
                     } else {
                         raise_error(a.err, kErrPairOverflow, pbase + qe, a.pair_cap);
                     }
@@ -722,8 +764,6 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
 // so that neither carries the other's registers; 5 blocks/SM (48 registers,
 // spills hit the large L1 this kernel leaves) hides its gather latency best.
 __global__ void __launch_bounds__(256, 5) backward_pairs_kernel(const __grid_constant__ BackwardArgs<float> a, int nseg) {
-    __shared__ float dD_s[8][32];
-    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int seg = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
     if (seg >= nseg) return;
     const uint32_t n = a.pair_n[seg];
@@ -731,15 +771,9 @@ __global__ void __launch_bounds__(256, 5) backward_pairs_kernel(const __grid_con
     const int tile = seg >> 3, w = seg & 7;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     const int bx = tx * kTile + (w & 1) * 8, by = ty * kTile + (w >> 1) * 4;
-    const int x = bx + (lane & 7), y = by + (lane >> 3);
-    dD_s[wib][lane] = (x < a.W && y < a.H) ? a.ddepth[size_t(y) * a.W + x] : 0.f;
-    __syncwarp();
-    const int64_t base = a.pair_off[seg];
-    for (uint32_t k0 = 0; k0 < n; k0 += 32) {
-        const int64_t o = base + k0;
-        const PairRecords q{a.pr_meta + o, a.pr_gid + o, a.pr_w + o, a.pr_da + o, a.pr_al + o, a.pr_gs + o};
-        flush_pairs<float, false>(a, q, dD_s[wib], int(n - k0 < 32 ? n - k0 : 32), bx, by);
-    }
+    const uint4* const rec = a.pr + a.pair_off[seg];
+    for (uint32_t k0 = 0; k0 < n; k0 += 32)
+        flush_records(a, rec + k0, int(n - k0 < 32 ? n - k0 : 32), bx, by);
 }
 
 template <typename Real>

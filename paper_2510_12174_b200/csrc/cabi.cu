@@ -170,7 +170,7 @@ struct msplat_replay {
         count_sorted, offset_sorted, inst_tile, inst_tile_alt, inst_gauss, inst_gauss_alt, tile_range,
         d_inst_count, d_inst_total32, hist, hist_scanned, scan_tiles, terminus, weight_sums, saved_means,
         saved_k, cap_center, cap_conic, cap_depth, cap_radius, cap_rgb, visible_count, ev_list, ev_count, ev_npairs,
-        pair_off, pair_n, pair_scan, pair_total, pr_gid, pr_meta, pr_w, pr_da, pr_al, pr_gs;
+        pair_off, pair_n, pair_scan, pair_total, pair_rec;
     int64_t pair_cap = 0;  // pair-record capacity of the FP32 split backward
     uint32_t* sorted_gauss = nullptr;
 
@@ -180,8 +180,7 @@ struct msplat_replay {
                           &inst_gauss, &inst_gauss_alt, &tile_range, &d_inst_count, &d_inst_total32, &hist,
                           &hist_scanned, &scan_tiles, &terminus, &weight_sums, &saved_means, &saved_k,
                           &cap_center, &cap_conic, &cap_depth, &cap_radius, &cap_rgb, &visible_count, &ev_list,
-                          &ev_count, &ev_npairs, &pair_off, &pair_n, &pair_scan, &pair_total, &pr_gid, &pr_meta,
-                          &pr_w, &pr_da, &pr_al, &pr_gs})
+                          &ev_count, &ev_npairs, &pair_off, &pair_n, &pair_scan, &pair_total, &pair_rec})
             b->release();
     }
 };
@@ -618,8 +617,7 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
             const int64_t need = int64_t(*reinterpret_cast<uint32_t*>(ctx->h_u64));
             if (need > rw->pair_cap) {
                 const int64_t cap = need + need / 4 + 4096;
-                for (DevBuf* b : {&rw->pr_gid, &rw->pr_meta, &rw->pr_w, &rw->pr_da, &rw->pr_al, &rw->pr_gs})
-                    CUDA_TRY(b->ensure(size_t(cap) * 4));
+                CUDA_TRY(rw->pair_rec.ensure(size_t(cap) * sizeof(uint4)));
                 rw->pair_cap = cap;
             }
         }
@@ -627,12 +625,7 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
         BackwardArgs<float>& af = reinterpret_cast<BackwardArgs<float>&>(a);
         af.pair_off = rw->pair_off.as<uint32_t>();
         af.pair_n = rw->pair_n.as<uint32_t>();
-        af.pr_gid = rw->pr_gid.as<uint32_t>();
-        af.pr_meta = rw->pr_meta.as<uint32_t>();
-        af.pr_w = rw->pr_w.as<float>();
-        af.pr_da = rw->pr_da.as<float>();
-        af.pr_al = rw->pr_al.as<float>();
-        af.pr_gs = rw->pr_gs.as<float>();
+        af.pr = rw->pair_rec.as<uint4>();
         af.pair_cap = rw->pair_cap;
     }
     ctx->timer.begin(MSPLAT_STAGE_BACKWARD, st);

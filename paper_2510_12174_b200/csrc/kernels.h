@@ -205,11 +205,12 @@ struct BackwardArgs {
     const uint2* ev_list;     // the forward's blend-event log (ForwardArgs::ev_list)
     const uint32_t* ev_count;
     // FP32 split backward: per-(tile, warp) pair-record segments written by the
-    // tensor-core phase A and consumed by the phase-B kernel (SoA, pair_cap).
+    // tensor-core phase A and consumed by the phase-B kernel: one 16-byte
+    // record per blended pair {gid, pixel lane, G dalpha (0 when alpha was
+    // clamped), dD w}, pair_cap records in all.
     const uint32_t* pair_off;  // [tiles * 8] exclusive scan of ev_npairs
     uint32_t* pair_n;          // [tiles * 8] pairs phase A wrote
-    uint32_t *pr_gid, *pr_meta;
-    float *pr_w, *pr_da, *pr_al, *pr_gs;
+    uint4* pr;
     int64_t pair_cap;
     const Real* T_final;
     const int32_t* terminus;
