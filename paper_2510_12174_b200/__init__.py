@@ -13,4 +13,6 @@ from .rasterizer import (  # noqa: F401
     param_layout, prune, rasterize, rasterize_backward, set_deterministic, set_stage_timing, stage_timings,
 )
 
+from .dataset import DatasetFrame, SceneDataset, load_dataset  # noqa: F401,E402
+
 __version__ = "0.1.0"

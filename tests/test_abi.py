@@ -61,3 +61,14 @@ def test_python_errors_map_to_reference_exception_types():
         _lib.check(_lib.MSPLAT_ERR_LOGIC)
     with pytest.raises(RuntimeError):
         _lib.check(_lib.MSPLAT_ERR_RUNTIME)
+
+
+def test_dropin_exports_the_io_header():
+    """include/msplat_io.h (dataset / image / config I/O) is exported by the
+    C++ drop-in library."""
+    hdr = open(os.path.join(ROOT, "include", "msplat_io.h")).read()
+    syms = set(re.findall(r"MSPLAT_IO_API\s+[\w\s\*]+?\b(msplat_\w+)\s*\(", hdr))
+    assert "msplat_dataset_load" in syms and "msplat_image_read_png" in syms
+    lib = os.path.join(ROOT, "paper_2510_12174_b200", "libmsplat_dropin.so")
+    nm = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True).stdout
+    assert syms <= set(re.findall(r" T (msplat_\w+)", nm))
