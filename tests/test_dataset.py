@@ -4,9 +4,9 @@ and the training config (dataset.cpp:210-284), against the reference's own
 code compiled unmodified into oracle/_ref/libmsplat_ref_io.so (real libpng
 1.6.56 from Pillow's wheel, nlohmann/json 3.11.3).
 
-CPU only: decoding and parsing are host work in both implementations; the
-Python front end's device upload is checked with device="cpu" here and on
-the GPU in test_gpu_parity-style smoke below.
+Decoding and parsing are host work in both implementations, so these are CPU
+tests; the last one (gpu) takes the maps to cuda:0 and through frame_losses /
+frame_metrics.
 """
 import ctypes as ct
 import json
@@ -491,3 +491,31 @@ def test_python_load_dataset_to_tensors(tmp_path, libs):
     assert np.array_equal(ds.points, r["points"]) and np.array_equal(ds.point_colors, r["colors"])
     with pytest.raises(RuntimeError, match="cannot open"):
         D.load_dataset(tmp_path / "absent", device="cpu")
+
+
+@pytest.mark.gpu
+def test_dataset_ground_truth_on_device_feeds_losses(tmp_path, libs):
+    """load_dataset onto cuda:0: the maps equal the reference's, and a frame
+    rendered from the dataset's camera goes through frame_losses /
+    frame_metrics with that ground truth."""
+    import torch
+    import paper_2510_12174_b200 as M
+    from paper_2510_12174_b200 import scenes
+    ref, _ = libs
+    rng = np.random.default_rng(12)
+    make_dataset(tmp_path / "g", rng, W=40, H=32, C=3, nframes=2, points=False)
+    r, _ = ref.dataset(tmp_path / "g")
+    ds = M.load_dataset(tmp_path / "g")
+    f = ds.frames[0]
+    assert f.truth.rgb.is_cuda and torch.equal(f.truth.rgb.cpu(), torch.from_numpy(r["frames"][0]["rgb"]))
+    assert torch.equal(f.truth.labels.cpu(), torch.from_numpy(r["frames"][0]["labels"]))
+    s = scenes.make_random_scene(200, 3, 1, seed=1)
+    scene = M.Scene.from_numpy(s, dtype=torch.float32)
+    # a camera looking at the random scene, with the dataset's intrinsics and size
+    view = M.make_camera(f.view.fx, f.view.fy, f.view.cx, f.view.cy, ds.width, ds.height, np.eye(3), np.zeros(3))
+    frame = M.rasterize(scene, view, M.RenderConfig(), M.ReplayState())
+    M.estimate_normals(frame.depth, frame.transmittance, view, M.NormalConfig(), frame.normals)
+    report, pix = M.frame_losses(frame, f.truth, view, M.NormalConfig())
+    assert np.isfinite(report.combined) and report.l1 > 0
+    met = M.frame_metrics(frame, f.truth)
+    assert met["psnr"] is not None and np.isfinite(met["psnr"])
