@@ -115,11 +115,10 @@ __device__ __forceinline__ Real seg_sum(Real v, const bool* same) {
 // ray-ellipsoid midpoint depth's adjoint into dmean (v[6..8]), drotation
 // (v[9..12]) and dscale (v[13..15]); dd = dL/ddepth(pixel) * w.
 template <typename Real>
-__device__ __forceinline__ void depth_chain_adjoint(const BackwardArgs<Real>& a, uint32_t g, int xL, int yL, Real dd,
-                                                    Real (&v)[16]) {
+__device__ __forceinline__ void depth_chain_adjoint(const BackwardArgs<Real>& a, uint32_t g, const PixelRay<Real>& ray,
+                                                    Real dd, Real (&v)[16]) {
     const Real sigma = Real(a.rp.sigma_scale);
     const BlendRec<Real>& br = a.brec[g];
-    const PixelRay<Real> ray = make_ray<Real>(a.cam, xL, yL);
     const HitEval<Real> h = intersect<Real>(br, ray, a.cam, a.raw, g);
     if (h.hit) {
         if constexpr (sizeof(Real) == 4) {
@@ -240,7 +239,7 @@ __device__ __forceinline__ void flush_pairs(const BackwardArgs<Real>& a, const Q
         }
         // Depth chain (rasterizer_backward.cpp:205-218).
         const Real dd = dDw[L] * w;
-        if (dd != Real(0)) depth_chain_adjoint<Real>(a, g, xL, yL, dd, v);
+        if (dd != Real(0)) depth_chain_adjoint<Real>(a, g, make_ray<Real>(a.cam, xL, yL), dd, v);
     }
     // Deterministic mode: this (instance, warp) owns a private slot; plain
     // read-modify-write in program order, reduced later in a fixed order.
@@ -276,7 +275,8 @@ __device__ __forceinline__ void flush_pairs(const BackwardArgs<Real>& a, const Q
 // ({gid, pixel lane, v0 = G dalpha, dd = dD w}): dopacity = v0, dmean2d / dconic
 // from dpower = opacity v0 (= alpha dalpha; 0 when alpha was clamped), the
 // depth chain from dd; segmented by Gaussian, one vector reduction per row.
-__device__ __forceinline__ void flush_records(const BackwardArgs<float>& a, const uint4* rec, int n, int bx, int by) {
+__device__ __forceinline__ void flush_records(const BackwardArgs<float>& a, const uint4* rec, int n, int bx, int by,
+                                              const float4* rays, float zoff) {
     const int lane = threadIdx.x & 31;
     const bool act = lane < n;
     const uint4 r = act ? rec[lane] : make_uint4(0xffffffffu - lane, 0u, 0u, 0u);  // padding: unique keys
@@ -309,7 +309,7 @@ __device__ __forceinline__ void flush_records(const BackwardArgs<float>& a, cons
             v[4] = dpower * (-0.5f * dx * dy);
             v[5] = dpower * (-0.5f * dy * dy);
         }
-        if (dd != 0.f) depth_chain_adjoint<float>(a, g, xL, yL, dd, v);
+        if (dd != 0.f) depth_chain_adjoint<float>(a, g, cached_ray(rays[L], zoff, xL, yL), dd, v);
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = seg_sum<float>(v[i], same);
@@ -764,6 +764,8 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
 // so that neither carries the other's registers; 5 blocks/SM (48 registers,
 // spills hit the large L1 this kernel leaves) hides its gather latency best.
 __global__ void __launch_bounds__(256, 5) backward_pairs_kernel(const __grid_constant__ BackwardArgs<float> a, int nseg) {
+    __shared__ float4 rays[8][32];  // the segment's pixel rays (cached_ray)
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int seg = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
     if (seg >= nseg) return;
     const uint32_t n = a.pair_n[seg];
@@ -771,9 +773,12 @@ __global__ void __launch_bounds__(256, 5) backward_pairs_kernel(const __grid_con
     const int tile = seg >> 3, w = seg & 7;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     const int bx = tx * kTile + (w & 1) * 8, by = ty * kTile + (w >> 1) * 4;
+    const PixelRay<float> r = make_ray<float>(a.cam, bx + (lane & 7), by + (lane >> 3));
+    rays[wib][lane] = ray_cache_entry(r);
+    __syncwarp();
     const uint4* const rec = a.pr + a.pair_off[seg];
     for (uint32_t k0 = 0; k0 < n; k0 += 32)
-        flush_records(a, rec + k0, int(n - k0 < 32 ? n - k0 : 32), bx, by);
+        flush_records(a, rec + k0, int(n - k0 < 32 ? n - k0 : 32), bx, by, rays[wib], r.zoff);
 }
 
 template <typename Real>

@@ -48,6 +48,25 @@ __device__ __forceinline__ PixelRay<Real> make_ray(const Cam& c, int x, int y) {
     return r;
 }
 
+// FP32 blends keep the 32 rays of a warp's 8x4 pixel block in shared memory
+// ({d, dz} per pixel plus the camera's zoff), computed once by make_ray, so a
+// pair's ray costs one 16-byte load instead of the camera conversions,
+// divisions and normalisation.  Values are make_ray's bit for bit (o is not
+// used by the FP32 intersect / midpoint_depth).
+__device__ __forceinline__ float4 ray_cache_entry(const PixelRay<float>& r) { return make_float4(r.d[0], r.d[1], r.d[2], r.dz); }
+__device__ __forceinline__ PixelRay<float> cached_ray(const float4 c, float zoff, int x, int y) {
+    PixelRay<float> r;
+    r.px = float(x) + 0.5f;
+    r.py = float(y) + 0.5f;
+    r.d[0] = c.x;
+    r.d[1] = c.y;
+    r.d[2] = c.z;
+    r.dz = c.w;
+    r.o[0] = r.o[1] = r.o[2] = 0.f;
+    r.zoff = zoff;
+    return r;
+}
+
 template <typename Real>
 struct AlphaEval {
     Real alpha, gauss, dx, dy;

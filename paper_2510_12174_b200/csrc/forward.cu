@@ -38,6 +38,8 @@ __host__ __device__ inline int sem_pitch(int C) { return C | 1; }  // odd pitch:
 template <typename Real>
 struct FwdWarpSmem {
     AlphaRec<Real> rec[32];
+    float4 ray[32];  // FP32: the block's pixel rays (cached_ray)
+    float zoff;
     uint32_t gid[32];
     uint32_t q_lane[kQueue];
     uint32_t q_gid[kQueue];
@@ -132,7 +134,11 @@ __device__ __forceinline__ void flush_depth(const ForwardArgs<Real>& a, FwdWarpS
         const uint32_t g = ws->q_gid[lane];
         const BlendRec<Real>& br = a.brec[g];
         const int xL = bx + (L & 7), yL = by + (L >> 3);
-        const PixelRay<Real> ray = make_ray<Real>(a.cam, xL, yL);
+        PixelRay<Real> ray;
+        if constexpr (sizeof(Real) == 4)
+            ray = cached_ray(ws->ray[L], ws->zoff, xL, yL);
+        else
+            ray = make_ray<Real>(a.cam, xL, yL);
         const HitEval<Real> h = intersect<Real>(br, ray, a.cam, a.raw, g);
         const Real d = !h.hit ? br.zc
                               : (h.depth_fp64 >= Real(0) ? h.depth_fp64 : midpoint_depth<Real>(a.cam, ray, h.t_mid));
@@ -176,6 +182,11 @@ __global__ void __launch_bounds__(kThreads, 2) forward_kernel(const __grid_const
     const int bx = tx * kTile + (warp & 1) * 8, by = ty * kTile + (warp >> 1) * 4;
     const int x = bx + (lane & 7), y = by + (lane >> 3);
     const bool inside = x < a.W && y < a.H;
+    if constexpr (kTC) {
+        const PixelRay<Real> r = make_ray<Real>(a.cam, x, y);
+        ws->ray[lane] = ray_cache_entry(r);
+        if (lane == 0) ws->zoff = r.zoff;
+    }
     const Real pxf = Real(x) + Real(0.5), pyf = Real(y) + Real(0.5);
     const Real rx0 = Real(bx) + Real(0.5), rx1 = rx0 + Real(7);
     const Real ry0 = Real(by) + Real(0.5), ry1 = ry0 + Real(3);
