@@ -27,6 +27,10 @@
 #include "kernels.h"
 #include "radix_sort.cuh"
 
+#ifndef K9_UNROLL
+#define K9_UNROLL 4
+#endif
+
 namespace msplat_cuda {
 
 namespace {
@@ -526,6 +530,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const __grid_cons
 // the same phase-B flush.
 namespace {
 
+constexpr int kK9Unroll = K9_UNROLL;
 constexpr int kSub = 8;         // events per sub-batch (mma N)
 constexpr int kTilePitch = 36;  // FS / W tiles [kSub][36]: conflict-free fragment stores and row reads
 
@@ -691,6 +696,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
                     FSs[(2 * t4 + (i & 1)) * kTilePitch + mt * 16 + 8 * (i >> 1) + g4] = d1[mt][i];
             __syncwarp();
             // (c) the reference's sequential recursion, event by event.
+#pragma unroll kK9Unroll
             for (int e = 0; e < ns; ++e) {
                 const unsigned fmask = ws->emask[s0 + e];
                 AlphaEval<float> ae;
