@@ -285,14 +285,16 @@ __device__ __forceinline__ void flush_records(const BackwardArgs<float>& a, cons
     const bool act = lane < n;
     const uint4 r = act ? rec[lane] : make_uint4(0xffffffffu - lane, 0u, 0u, 0u);  // padding: unique keys
     const uint32_t g = r.x;
-    bool same[5];
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-        const uint32_t o = __shfl_down_sync(0xffffffffu, g, 1 << k);
-        same[k] = (lane + (1 << k) < 32) && o == g;
-    }
+    // Runs of equal ids are contiguous (an event's pairs): lane's run ends at
+    // the next run start, and the segmented sum needs only ceil(log2(longest
+    // run)) shuffle steps.
     const uint32_t g_prev = __shfl_up_sync(0xffffffffu, g, 1);
-    const bool head = act && (lane == 0 || g_prev != g);
+    const bool brk = lane == 0 || g_prev != g;
+    const unsigned starts = __ballot_sync(0xffffffffu, brk);
+    const bool head = act && brk;
+    const unsigned later = lane == 31 ? 0u : (starts >> (lane + 1)) << (lane + 1);
+    const int run_end = later ? __ffs(later) - 1 : 32;
+    const unsigned longest = __reduce_max_sync(0xffffffffu, brk ? unsigned(run_end - lane) : 0u);
     float v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = 0.f;
@@ -316,7 +318,15 @@ __device__ __forceinline__ void flush_records(const BackwardArgs<float>& a, cons
         if (dd != 0.f) depth_chain_adjoint<float>(a, g, cached_ray(rays[L], zoff, xL, yL), dd, v);
     }
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = seg_sum<float>(v[i], same);
+    for (int k = 0; k < 5; ++k) {
+        if ((1u << k) >= longest) break;
+        const bool in_run = lane + (1 << k) < run_end;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const float o = __shfl_down_sync(0xffffffffu, v[i], 1 << k);
+            if (in_run) v[i] += o;
+        }
+    }
     if (head) {
         float* const row = a.acc16 + size_t(g) * 16;
 #pragma unroll
