@@ -567,35 +567,39 @@ size_t backward_tc_smem_bytes(int C) {
 
 }  // namespace
 
-// Stages F rows [rgb, k | sem] of n events into rows of pitch sp: one 16-byte
-// copy of (rgb, k) (BlendRec offset 80, 16-byte aligned) plus the semantic row
-// in 8-byte pieces when C is even (4-byte otherwise); lanes stride over all
-// pieces of all n rows, so one pass issues every copy.
-__device__ __forceinline__ void stage_rows_tc(float* Fb, int sp, const BlendRec<float>* brec, const float* semantics,
+// Stages F rows [rgb, k | sem] of n (<= kSub) events into rows of pitch sp:
+// one 16-byte copy of (rgb, k) per row from the AlphaRec (offset 48, the line
+// the sub-batch's records come from) and the semantic row in 8-byte pieces
+// when C is even (4-byte otherwise).  A lane owns a fixed piece column and
+// walks the rows, so the loop carries no index arithmetic.
+__device__ __forceinline__ void stage_rows_tc(float* Fb, int sp, const AlphaRec<float>* arec, const float* semantics,
                                               int C, const uint32_t* gid, int n, int lane) {
-    // Piece q = e * per + j of the batch; lanes advance by 32 pieces without a
-    // division per step.
-    const bool even = (C & 1) == 0;
-    const int per = 1 + (even ? C / 2 : C);
-    int e = lane / per, j = lane - e * per;
-    for (int q = lane; q < n * per; q += 32) {
-        const uint32_t g = gid[e];
-        if (j == 0) {
-            const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + e * sp));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(&brec[g].rgb[0]) : "memory");
-        } else if (even) {
-            const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + e * sp + 4 + 2 * (j - 1)));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(semantics + size_t(g) * C + 2 * (j - 1))
-                         : "memory");
-        } else {
-            const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + e * sp + 4 + (j - 1)));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(semantics + size_t(g) * C + (j - 1))
-                         : "memory");
+    if (lane < n) {
+        const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + lane * sp));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(&arec[gid[lane]].rgb[0]) : "memory");
+    }
+    const unsigned base = unsigned(__cvta_generic_to_shared(Fb + 4));
+    if ((C & 1) == 0) {
+        for (int j = lane; j < C / 2; j += 32) {
+            const float* const src = semantics + 2 * j;
+#pragma unroll
+            for (int e = 0; e < kSub; ++e) {
+                if (e >= n) break;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(base + unsigned(4 * (e * sp + 2 * j))),
+                             "l"(src + size_t(gid[e]) * C)
+                             : "memory");
+            }
         }
-        j += 32;
-        while (j >= per) {
-            j -= per;
-            ++e;
+    } else {
+        for (int j = lane; j < C; j += 32) {
+            const float* const src = semantics + j;
+#pragma unroll
+            for (int e = 0; e < kSub; ++e) {
+                if (e >= n) break;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(base + unsigned(4 * (e * sp + j))),
+                             "l"(src + size_t(gid[e]) * C)
+                             : "memory");
+            }
         }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -683,7 +687,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
         for (int s0 = 0; s0 < nb; s0 += kSub) {
             const int ns = nb - s0 < kSub ? nb - s0 : kSub;
             // (a) F rows (cp.async) and alpha records of the sub-batch.
-            stage_rows_tc(Fb, sp, a.brec, a.semantics, C, ws->gid + s0, ns, lane);
+            stage_rows_tc(Fb, sp, a.arec, a.semantics, C, ws->gid + s0, ns, lane);
             if (lane < ns) ws->rec[lane] = a.arec[ws->gid[s0 + lane]];
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncwarp();
