@@ -323,10 +323,13 @@ __device__ __forceinline__ void stage_F_wait_prev() {
 // ---- warp-level tensor-core helpers (mma.sync m16n8k8 TF32, FP32 accumulate)
 // with a hi/lo operand split: a.b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi, i.e.
 // FP32-level accuracy for the blend contractions.
+// hi = x truncated to TF32 (one AND), lo = x - hi exactly (<= 13 significant
+// bits, which the tensor core truncates to TF32): |a b - (a_hi b_hi + a_hi b_lo
+// + a_lo b_hi)| <= ~2^-20 |a b|.  (cvt.rna.tf32 lowers to a compare, an add
+// and a mask; this split is two instructions.)
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
-    const float r = x - __uint_as_float(hi);
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+    hi = __float_as_uint(x) & 0xffffe000u;
+    lo = __float_as_uint(x - __uint_as_float(hi));
 }
 
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
