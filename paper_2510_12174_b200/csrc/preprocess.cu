@@ -16,6 +16,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <type_traits>
+
 namespace msplat_cuda {
 
 constexpr int kPreThreads = 256;
@@ -74,6 +76,44 @@ __device__ __forceinline__ void sh_basis(int deg, T x, T y, T z, T* b) {
     }
 }
 
+// Copies count contiguous values to dst (when given) and reports whether any
+// of those this thread touched is non-finite: 16-byte vectors, four in flight
+// per thread, when src is 16-byte aligned (block offsets are; the tensor base
+// normally is), scalars otherwise and for the tail.
+template <typename Real>
+__device__ __forceinline__ bool stage_and_scan(const Real* __restrict__ src, Real* dst, int count) {
+    constexpr int W = 16 / int(sizeof(Real));
+    constexpr uint64_t kExp = sizeof(Real) == 4 ? 0x7f800000ull : 0x7ff0000000000000ull;
+    using Bits = std::conditional_t<sizeof(Real) == 4, uint32_t, uint64_t>;
+    bool bad = false;
+    int done = 0;
+    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        const int nv = count / W;
+        const uint4* s = reinterpret_cast<const uint4*>(src);
+        uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll 4
+        for (int v = threadIdx.x; v < nv; v += kPreThreads) {
+            const uint4 x = __ldg(s + v);
+            if (dst) d[v] = x;
+            if constexpr (sizeof(Real) == 4) {
+                bad |= (x.x & 0x7f800000u) == 0x7f800000u || (x.y & 0x7f800000u) == 0x7f800000u ||
+                       (x.z & 0x7f800000u) == 0x7f800000u || (x.w & 0x7f800000u) == 0x7f800000u;
+            } else {
+                bad |= (x.y & 0x7ff00000u) == 0x7ff00000u || (x.w & 0x7ff00000u) == 0x7ff00000u;
+            }
+        }
+        done = nv * W;
+    }
+    for (int e = done + int(threadIdx.x); e < count; e += kPreThreads) {
+        const Real v = src[e];
+        if (dst) dst[e] = v;
+        Bits b;
+        memcpy(&b, &v, sizeof(b));
+        bad |= (uint64_t(b) & kExp) == kExp;
+    }
+    return bad;
+}
+
 template <typename Real>
 __device__ __forceinline__ bool finite_params(const PreprocessArgs<Real>& a, int64_t i) {
     bool ok = true;
@@ -100,25 +140,28 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(const __grid_co
     {
         const int rs = 3 * a.K;
         bad_s[threadIdx.x] = 0;
-        __syncthreads();
-        // (element -> row index by a running quotient: no integer division per element)
-        const Real* src = a.sh + base * rs;
-        for (int e = threadIdx.x, row = threadIdx.x / rs, rem = threadIdx.x % rs; e < cnt * rs;
-             e += kPreThreads, rem += kPreThreads % rs, row += kPreThreads / rs) {
-            if (rem >= rs) { rem -= rs; ++row; }
-            const Real v = src[e];
-            sh_s[e] = v;
-            if (!isfinite(v)) bad_s[row] = 1;
-        }
-        if (a.C > 0) {
-            const Real* sem = a.semantics + base * a.C;
-            for (int e = threadIdx.x, row = threadIdx.x / a.C, rem = threadIdx.x % a.C; e < cnt * a.C;
-                 e += kPreThreads, rem += kPreThreads % a.C, row += kPreThreads / a.C) {
-                if (rem >= a.C) { rem -= a.C; ++row; }
-                if (!isfinite(sem[e])) bad_s[row] = 1;
+        // Fast path: 16-byte vector copies / scans with a block-wide "any
+        // non-finite" vote; the rows are only identified when the vote fires.
+        bool bad = stage_and_scan<Real>(a.sh + base * rs, sh_s, cnt * rs);
+        if (a.C > 0) bad |= stage_and_scan<Real>(a.semantics + base * a.C, nullptr, cnt * a.C);
+        if (__syncthreads_or(bad)) {
+            // (element -> row index by a running quotient: no integer division per element)
+            const Real* src = a.sh + base * rs;
+            for (int e = threadIdx.x, row = threadIdx.x / rs, rem = threadIdx.x % rs; e < cnt * rs;
+                 e += kPreThreads, rem += kPreThreads % rs, row += kPreThreads / rs) {
+                if (rem >= rs) { rem -= rs; ++row; }
+                if (!isfinite(src[e])) bad_s[row] = 1;
             }
+            if (a.C > 0) {
+                const Real* sem = a.semantics + base * a.C;
+                for (int e = threadIdx.x, row = threadIdx.x / a.C, rem = threadIdx.x % a.C; e < cnt * a.C;
+                     e += kPreThreads, rem += kPreThreads % a.C, row += kPreThreads / a.C) {
+                    if (rem >= a.C) { rem -= a.C; ++row; }
+                    if (!isfinite(sem[e])) bad_s[row] = 1;
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();
     }
     const int64_t i = base + threadIdx.x;
     if (i >= a.n) return;

@@ -276,6 +276,16 @@ def test_non_finite_and_zero_quaternion_primitives_raise():
         gpu_forward(s, scenes.simple_camera(), {}, "float32")
     with pytest.raises(ValueError, match="sh_degree"):
         M.Scene.from_numpy(dict(scenes.make_random_scene(3, 1, 1), sh_degree=4))._abi()
+    # SH and semantic rows (scanned block-wide by K1): the first bad primitive
+    # is reported, also past the first 256-Gaussian block and at a row tail
+    for dtype in ("float32", "float64"):
+        for field, idx, val in (("sh", (300, 2, 8), np.inf), ("semantics", (517, 4), np.nan),
+                                ("sh", (0, 0, 0), -np.inf), ("semantics", (599, 0), np.inf)):
+            s = scenes.make_random_scene(600, 5, 2, seed=2)
+            s[field] = np.array(s[field])
+            s[field][idx] = val
+            with pytest.raises(ValueError, match=f"primitive {idx[0]}"):
+                gpu_forward(s, scenes.simple_camera(), {}, dtype)
 
 
 def test_adam_and_prune_match_oracle(port):
