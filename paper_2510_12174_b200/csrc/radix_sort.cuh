@@ -24,9 +24,9 @@ constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortItems = 16;
 constexpr int kSortTileItems = kSortThreads * kSortItems;  // 4096 keys per CTA
 
-constexpr int kScanThreads = 512;
-constexpr int kScanItems = 8;
-constexpr int kScanTile = kScanThreads * kScanItems;  // 4096 elements per CTA
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;  // 1024 elements per CTA: >= 1 CTA per SM for the histogram scans
 
 // --------------------------------------------------------------- block scan
 template <typename T>
@@ -140,11 +140,16 @@ __global__ void __launch_bounds__(kSortThreads) radix_upsweep_kernel(
     __syncthreads();
     const int64_t n = d_n ? *d_n : n_host;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll 4
+    uint32_t dig[kSortItems];  // all loads in flight before the first match
+#pragma unroll
     for (int r = 0; r < kSortItems; ++r) {
         const int64_t i = sort_item_index(blockIdx.x, warp, r, lane);
-        const bool ok = i < n;
-        const uint32_t d = ok ? digit_of<Key, BITS>(keys[i], shift) : 0xffffffffu;
+        dig[r] = i < n ? digit_of<Key, BITS>(keys[i], shift) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int r = 0; r < kSortItems; ++r) {
+        const uint32_t d = dig[r];
+        const bool ok = d != 0xffffffffu;
         const unsigned peers = __match_any_sync(0xffffffffu, d);
         const int leader = __ffs(peers) - 1;
         if (ok && lane == leader) atomicAdd(&h[d], __popc(peers));
