@@ -1,5 +1,6 @@
 // C ABI (include/msplat_b200.h): context / replay lifetime, device buffer
 // management, precision dispatch and the error contract.  No kernels here.
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -170,7 +171,7 @@ struct msplat_replay {
         count_sorted, offset_sorted, inst_tile, inst_tile_alt, inst_gauss, inst_gauss_alt, tile_range,
         d_inst_count, d_inst_total32, hist, hist_scanned, scan_tiles, terminus, weight_sums, saved_means,
         saved_k, cap_center, cap_conic, cap_depth, cap_radius, cap_rgb, visible_count, ev_list, ev_count, ev_npairs,
-        pair_off, pair_n, pair_scan, pair_total, pair_rec;
+        pair_off, pair_n, pair_scan, pair_total, pair_rec, wq_order;
     int64_t pair_cap = 0;  // pair-record capacity of the FP32 split backward
     uint32_t* sorted_gauss = nullptr;
 
@@ -180,12 +181,22 @@ struct msplat_replay {
                           &inst_gauss, &inst_gauss_alt, &tile_range, &d_inst_count, &d_inst_total32, &hist,
                           &hist_scanned, &scan_tiles, &terminus, &weight_sums, &saved_means, &saved_k,
                           &cap_center, &cap_conic, &cap_depth, &cap_radius, &cap_rgb, &visible_count, &ev_list,
-                          &ev_count, &ev_npairs, &pair_off, &pair_n, &pair_scan, &pair_total, &pair_rec})
+                          &ev_count, &ev_npairs, &pair_off, &pair_n, &pair_scan, &pair_total, &pair_rec, &wq_order})
             b->release();
     }
 };
 
 namespace {
+
+// FP32 backward over a longest-first segment order (default); the environment
+// variable MSPLAT_STATIC_SCHEDULE=1 restores tile order (A/B timing).
+bool dynamic_schedule() {
+    static const bool on = [] {
+        const char* e = std::getenv("MSPLAT_STATIC_SCHEDULE");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
 
 // CameraView::finalize (core/src/camera.cpp:8-21).
 msplat_status make_cam(const msplat_camera* c, Cam& o) {
@@ -323,6 +334,7 @@ msplat_status size_replay(msplat_replay* r, int dtype, int64_t n, int C, int deg
     CUDA_TRY(r->ev_list.ensure(ic * 8 * sizeof(uint2)));  // 8 warps x (position, mask) per instance
     CUDA_TRY(r->ev_count.ensure(size_t(tiles) * 8 * 4));
     CUDA_TRY(r->ev_npairs.ensure(size_t(tiles) * 8 * 4));
+    CUDA_TRY(r->wq_order.ensure(size_t(tiles) * 8 * 4));
     CUDA_TRY(r->inst_gauss.ensure(ic * 4));
     CUDA_TRY(r->inst_gauss_alt.ensure(ic * 4));
     CUDA_TRY(r->tile_range.ensure(size_t(tiles) * 8));
@@ -627,6 +639,10 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
         af.pair_n = rw->pair_n.as<uint32_t>();
         af.pr = rw->pair_rec.as<uint4>();
         af.pair_cap = rw->pair_cap;
+        if (dynamic_schedule()) {
+            launch_work_order(nullptr, r->ev_count.as<uint32_t>(), int(nseg), rw->wq_order.as<uint32_t>(), st);
+            af.work_order = rw->wq_order.as<uint32_t>();
+        }
     }
     ctx->timer.begin(MSPLAT_STAGE_BACKWARD, st);
     launch_backward_blend<Real>(a, r->tiles_x * r->tiles_y, st);

@@ -108,6 +108,13 @@ struct ForwardArgs {
 template <typename Real>
 void launch_forward(const ForwardArgs<Real>& a, int ntiles, cudaStream_t s);
 
+// Longest-first order of the nseg = 8 * tiles (tile, warp) segments for the
+// FP32 backward: cost = seg_cost[i] (the forward's event counts) or, when
+// seg_cost is null, the tile's list length.  Coarse counting sort (1024 cost
+// buckets, arbitrary order inside a bucket: scheduling only, results do not
+// depend on it).
+void launch_work_order(const uint2* tile_range, const uint32_t* seg_cost, int nseg, uint32_t* order, cudaStream_t s);
+
 // K12: frame losses + seed assembly (core/src/trainer.cpp:171-264, losses.cpp).
 template <typename Real>
 struct LossArgs {
@@ -226,6 +233,11 @@ struct BackwardArgs {
     // 20 + C values [opac, dmean2, dconic3, pos3, rot4, scale3, dcolor3, k, sem C].
     Real* partial;
     int V;
+    // Segment schedule of the FP32 split backward (optional): warp w of CTA b
+    // replays segment work_order[8 b + w] = tile * 8 + block (longest first,
+    // launch_work_order), and phase B takes segments in the same order.  Null:
+    // warp w of CTA b replays block w of tile b.
+    const uint32_t* work_order;
     DeviceError* err;
 };
 template <typename Real>
