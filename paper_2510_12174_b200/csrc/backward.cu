@@ -12,8 +12,8 @@ namespace msplat_cuda {
 // SH colour adjoint (sh.cpp:45-73, 86-99) for a compile-time degree: dsh +=
 // g (x) basis, and the view-direction gradient through the basis Jacobian.
 template <typename Real, int DEG>
-__device__ __forceinline__ void sh_adjoint(const ProjBackwardArgs<Real>& a, int64_t i, Real dx, Real dy, Real dz,
-                                           const Real* g3, Real* ddir) {
+__device__ __forceinline__ void sh_adjoint(const Real* sh, Real* g_sh, Real dx, Real dy, Real dz, const Real* g3,
+                                           Real* ddir) {
     constexpr int K = (DEG + 1) * (DEG + 1);
     Real b[K], Jb[K][3];
     const Real C0 = Real(0.28209479177387814), C1 = Real(0.4886025119029199);
@@ -53,17 +53,18 @@ __device__ __forceinline__ void sh_adjoint(const ProjBackwardArgs<Real>& a, int6
     }
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        const Real shg = a.sh[(i * 3 + 0) * K + j] * g3[0] + a.sh[(i * 3 + 1) * K + j] * g3[1] +
-                         a.sh[(i * 3 + 2) * K + j] * g3[2];
+        const Real shg = sh[0 * K + j] * g3[0] + sh[1 * K + j] * g3[1] + sh[2 * K + j] * g3[2];
         for (int k = 0; k < 3; ++k) ddir[k] += Jb[j][k] * shg;
-        for (int ch = 0; ch < 3; ++ch) a.g_sh[(i * 3 + ch) * K + j] += g3[ch] * b[j];
+        for (int ch = 0; ch < 3; ++ch) g_sh[ch * K + j] += g3[ch] * b[j];
     }
 }
 
+// Per-Gaussian part of K10; sh / g_sh point at the Gaussian's staged rows.
+// Returns whether the Gaussian's small gradients (position, rotation, scale,
+// opacity, k) are finite.
 template <typename Real>
-__global__ void __launch_bounds__(256) projection_backward_kernel(const __grid_constant__ ProjBackwardArgs<Real> a) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= a.n) return;
+__device__ __forceinline__ bool projection_backward_one(const ProjBackwardArgs<Real>& a, int64_t i, const Real* sh,
+                                                        Real* g_sh) {
     const Cam& c = a.cam;
     // Activation (scene.cpp:42-60) in the kernel precision.
     Real q[4];
@@ -182,10 +183,10 @@ __global__ void __launch_bounds__(256) projection_backward_kernel(const __grid_c
                     if (cl & (1 << ch)) g3[ch] = 0;
                 Real ddir[3] = {0, 0, 0};
                 switch (a.deg) {  // compile-time K: basis and Jacobian stay in registers
-                    case 0: sh_adjoint<Real, 0>(a, i, dx, dy, dz, g3, ddir); break;
-                    case 1: sh_adjoint<Real, 1>(a, i, dx, dy, dz, g3, ddir); break;
-                    case 2: sh_adjoint<Real, 2>(a, i, dx, dy, dz, g3, ddir); break;
-                    default: sh_adjoint<Real, 3>(a, i, dx, dy, dz, g3, ddir); break;
+                    case 0: sh_adjoint<Real, 0>(sh, g_sh, dx, dy, dz, g3, ddir); break;
+                    case 1: sh_adjoint<Real, 1>(sh, g_sh, dx, dy, dz, g3, ddir); break;
+                    case 2: sh_adjoint<Real, 2>(sh, g_sh, dx, dy, dz, g3, ddir); break;
+                    default: sh_adjoint<Real, 3>(sh, g_sh, dx, dy, dz, g3, ddir); break;
                 }
                 const Real dirv[3] = {dx, dy, dz};
                 const Real dd = dx * ddir[0] + dy * ddir[1] + dz * ddir[2];
@@ -212,10 +213,57 @@ __global__ void __launch_bounds__(256) projection_backward_kernel(const __grid_c
     }
     a.g_opac[i] = go;
     ok &= isfinite(go) && isfinite(a.g_k[i]);
-    for (int j = 0; j < 3 * a.K; ++j) ok &= isfinite(a.g_sh[i * 3 * a.K + j]);
-    for (int j = 0; j < a.C; ++j) ok &= isfinite(a.g_sem[i * a.C + j]);
-    if (!ok) raise_error(a.err, kErrNonFiniteGrad, 0, i);
+    return ok;
 }
+
+// One thread per Gaussian.  The wide rows (SH and its gradient, 3K values;
+// the semantic gradient, C values) are moved block-wide: the block's rows are
+// one contiguous range, staged through shared memory (SH, SH gradient) or
+// scanned in place (semantic gradient finiteness) with coalesced accesses,
+// instead of each thread striding through its own 108- / 200-byte row.
+constexpr int kK10Threads = 128;
+
+template <typename Real>
+size_t k10_smem_bytes(int K) { return size_t(2) * kK10Threads * 3 * K * sizeof(Real); }
+
+template <typename Real>
+__global__ void __launch_bounds__(kK10Threads) projection_backward_kernel(const __grid_constant__ ProjBackwardArgs<Real> a) {
+    extern __shared__ __align__(16) unsigned char k10_smem[];
+    const int RK = 3 * a.K;
+    Real* const s_sh = reinterpret_cast<Real*>(k10_smem);
+    Real* const s_gsh = s_sh + kK10Threads * RK;
+    const int64_t i0 = int64_t(blockIdx.x) * kK10Threads;
+    const int nb = int(a.n - i0 < kK10Threads ? a.n - i0 : kK10Threads);
+    {
+        const Real* __restrict__ src = a.sh + size_t(i0) * RK;
+        const Real* __restrict__ gsrc = a.g_sh + size_t(i0) * RK;
+        for (int e = threadIdx.x; e < nb * RK; e += kK10Threads) {
+            s_sh[e] = src[e];
+            s_gsh[e] = gsrc[e];
+        }
+    }
+    __syncthreads();
+    const int64_t i = i0 + threadIdx.x;
+    bool ok = true;
+    if (i < a.n) ok = projection_backward_one<Real>(a, i, s_sh + threadIdx.x * RK, s_gsh + threadIdx.x * RK);
+    if (!ok) raise_error(a.err, kErrNonFiniteGrad, 0, i);
+    __syncthreads();
+    // write the SH gradient back; finiteness of the SH and semantic rows
+    int bad = -1;
+    {
+        Real* __restrict__ dst = a.g_sh + size_t(i0) * RK;
+        for (int e = threadIdx.x; e < nb * RK; e += kK10Threads) {
+            const Real v = s_gsh[e];
+            dst[e] = v;
+            if (!isfinite(v) && bad < 0) bad = e / RK;
+        }
+        const Real* __restrict__ gsem = a.g_sem + size_t(i0) * a.C;
+        for (int e = threadIdx.x; e < nb * a.C; e += kK10Threads)
+            if (!isfinite(gsem[e]) && bad < 0) bad = e / a.C;
+    }
+    if (bad >= 0) raise_error(a.err, kErrNonFiniteGrad, 0, i0 + bad);
+}
+
 
 template <typename Real>
 __global__ void chain_kernel(int64_t n, const Real* __restrict__ quats, const Real* __restrict__ log_scales,
@@ -250,7 +298,13 @@ __global__ void check_replay_kernel(int64_t n, const Real* __restrict__ means, c
 template <typename Real>
 void launch_projection_backward(const ProjBackwardArgs<Real>& a, cudaStream_t s) {
     if (a.n == 0) return;
-    projection_backward_kernel<Real><<<unsigned((a.n + 255) / 256), 256, 0, s>>>(a);
+    const size_t smem = k10_smem_bytes<Real>(a.K);
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+        cudaFuncSetAttribute(projection_backward_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        configured = true;
+    }
+    projection_backward_kernel<Real><<<unsigned((a.n + kK10Threads - 1) / kK10Threads), kK10Threads, smem, s>>>(a);
     count_launches(1);
 }
 
