@@ -343,7 +343,7 @@ msplat_status size_replay(msplat_replay* r, int dtype, int64_t n, int C, int deg
     CUDA_TRY(r->visible_count.ensure(8));
     const size_t hist = binning_scratch_elems(int64_t(nn), r->inst_cap);
     CUDA_TRY(r->hist.ensure(hist * 4));
-    CUDA_TRY(r->hist_scanned.ensure(hist * 4));
+    CUDA_TRY(r->hist_scanned.ensure((hist + 512) * 4));  // + the radix digit totals
     const size_t scan_tiles = (std::max(hist, nn) + kScanTile - 1) / kScanTile + 1;
     CUDA_TRY(r->scan_tiles.ensure(scan_tiles * 4));
     CUDA_TRY(r->terminus.ensure(size_t(W) * H * 4));

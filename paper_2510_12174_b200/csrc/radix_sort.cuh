@@ -5,9 +5,12 @@
 //
 // Radix pass = 3 launches:
 //   upsweep   : per-tile digit histogram, warp-aggregated with __match_any_sync
-//   scan      : exclusive scan of the digit-major [RADIX][tiles] histogram
-//   downsweep : stable rank (per-warp match_any multisplit, warps in order)
-//               and scatter to  offset[digit][tile] + warp prefix + lane rank.
+//   rowscan   : per digit, exclusive scan along the tiles (one warp per digit)
+//               and the digit total
+//   downsweep : digit bases (block scan of the RADIX totals, redundantly per
+//               CTA), stable rank (per-warp match_any multisplit, warps in
+//               order) and scatter to base[digit] + row prefix[digit][tile] +
+//               warp prefix + lane rank.
 // Stability: items are processed in global index order (tile-major, then
 // warp-major, then item-row, then lane), which is what makes the composition
 // of passes an exact (key, original index) order -- the tie-break the
@@ -158,18 +161,59 @@ __global__ void __launch_bounds__(kSortThreads) radix_upsweep_kernel(
     for (int d = threadIdx.x; d < RADIX; d += kSortThreads) hist[int64_t(d) * ntiles + blockIdx.x] = h[d];
 }
 
+// Per digit (one warp each): exclusive scan of hist[d][0 .. ntiles) into
+// out[d][.] and the row total into totals[d].  A lane scans a contiguous
+// chunk of the row (loads in flight together), then the warp scans the chunk sums.
+template <int RADIX>
+__global__ void __launch_bounds__(256) radix_rowscan_kernel(const uint32_t* __restrict__ hist, int ntiles,
+                                                           uint32_t* __restrict__ out, uint32_t* __restrict__ totals) {
+    const int d = int((blockIdx.x * 256u + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (d >= RADIX) return;
+    const uint32_t* __restrict__ row = hist + int64_t(d) * ntiles;
+    uint32_t* __restrict__ orow = out + int64_t(d) * ntiles;
+    const int per = (ntiles + 31) >> 5, t0 = lane * per, t1 = t0 + per < ntiles ? t0 + per : ntiles;
+    uint32_t s = 0;
+#pragma unroll 8
+    for (int t = t0; t < t1; ++t) s += row[t];
+    const uint32_t inc = warp_inclusive_scan(s);
+    uint32_t run = inc - s;
+#pragma unroll 8
+    for (int t = t0; t < t1; ++t) {
+        const uint32_t v = row[t];
+        orow[t] = run;
+        run += v;
+    }
+    if (lane == 31) totals[d] = inc;
+}
+
 template <typename Key, int BITS>
 __global__ void __launch_bounds__(kSortThreads) radix_downsweep_kernel(
     const Key* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, Key* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, const int64_t* __restrict__ d_n, int64_t n_host, int shift,
-    const uint32_t* __restrict__ offsets /* scanned [RADIX][ntiles] */, int ntiles) {
+    const uint32_t* __restrict__ offsets /* row-scanned [RADIX][ntiles] */, const uint32_t* __restrict__ totals,
+    int ntiles) {
     constexpr int RADIX = 1 << BITS;
+    static_assert(RADIX % kSortThreads == 0, "digits per thread");
+    constexpr int PER = RADIX / kSortThreads;
     __shared__ uint32_t wh[kSortWarps][RADIX];
     __shared__ uint32_t base[RADIX];
-    for (int d = threadIdx.x; d < RADIX; d += kSortThreads) {
+    {  // digit bases: exclusive scan of the totals (thread t owns digits [t PER, t PER + PER))
+        uint32_t tv[PER], sum = 0;
 #pragma unroll
-        for (int w = 0; w < kSortWarps; ++w) wh[w][d] = 0;
-        base[d] = offsets[int64_t(d) * ntiles + blockIdx.x];
+        for (int j = 0; j < PER; ++j) {
+            tv[j] = totals[threadIdx.x * PER + j];
+            sum += tv[j];
+        }
+        uint32_t all;
+        uint32_t ex = block_exclusive_scan<uint32_t, kSortThreads>(sum, all);
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int d = threadIdx.x * PER + j;
+            base[d] = ex + offsets[int64_t(d) * ntiles + blockIdx.x];
+            ex += tv[j];
+#pragma unroll
+            for (int w = 0; w < kSortWarps; ++w) wh[w][d] = 0;
+        }
     }
     __syncthreads();
     const int64_t n = d_n ? *d_n : n_host;
@@ -229,8 +273,9 @@ __global__ void __launch_bounds__(kSortThreads) radix_downsweep_kernel(
     }
 }
 
-// Host-side driver.  Scratch requirements (elements): hist/offsets
-// RADIX * tiles(cap) uint32, scan tile sums ceil(RADIX*tiles/kScanTile) uint32.
+// Host-side driver.  Scratch requirements (elements): hist RADIX * tiles(cap)
+// uint32, hist_scanned RADIX * tiles(cap) + RADIX uint32 (row prefixes, then
+// the digit totals).
 struct SortScratch {
     uint32_t* hist = nullptr;
     uint32_t* hist_scanned = nullptr;
@@ -270,11 +315,11 @@ inline bool radix_sort_pairs(Key* keys_a, uint32_t* vals_a, Key* keys_b, uint32_
         radix_upsweep_kernel<Key, BITS><<<ntiles, kSortThreads, 0, s>>>(kin, d_n, n_cap, shift,
                                                                        sc.hist, ntiles);
         count_launches(1);
-        device_exclusive_scan<uint32_t>(sc.hist, sc.hist_scanned, nullptr, int64_t(RADIX) * ntiles,
-                                        sc.scan_tiles, nullptr, s);
+        uint32_t* const totals = sc.hist_scanned + int64_t(RADIX) * ntiles;
+        radix_rowscan_kernel<RADIX><<<(RADIX * 32 + 255) / 256, 256, 0, s>>>(sc.hist, ntiles, sc.hist_scanned, totals);
         radix_downsweep_kernel<Key, BITS><<<ntiles, kSortThreads, 0, s>>>(
-            kin, vin, kout, vout, d_n, n_cap, shift, sc.hist_scanned, ntiles);
-        count_launches(1);
+            kin, vin, kout, vout, d_n, n_cap, shift, sc.hist_scanned, totals, ntiles);
+        count_launches(2);
         in_b = !in_b;
     }
     return in_b;
