@@ -639,12 +639,12 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
         af.pair_n = rw->pair_n.as<uint32_t>();
         af.pr = rw->pair_rec.as<uint4>();
         af.pair_cap = rw->pair_cap;
-        if (dynamic_schedule()) {
-            launch_work_order(nullptr, r->ev_count.as<uint32_t>(), int(nseg), rw->wq_order.as<uint32_t>(), st);
-            af.work_order = rw->wq_order.as<uint32_t>();
-        }
+        if (dynamic_schedule()) af.work_order = rw->wq_order.as<uint32_t>();
     }
     ctx->timer.begin(MSPLAT_STAGE_BACKWARD, st);
+    if (sizeof(Real) == 4 && !ctx->deterministic && dynamic_schedule())
+        launch_work_order(nullptr, r->ev_count.as<uint32_t>(), r->tiles_x * r->tiles_y * 8, r->wq_order.as<uint32_t>(),
+                          st);
     launch_backward_blend<Real>(a, r->tiles_x * r->tiles_y, st);
     if (ctx->deterministic)
         launch_deterministic_reduce<Real>(a, det, r->d_inst_count.as<int64_t>(), det_count, st);
