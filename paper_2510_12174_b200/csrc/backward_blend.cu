@@ -843,7 +843,14 @@ __global__ void __launch_bounds__(kOrderThreads) work_order_kernel(const uint2* 
     auto bucket = [m](uint32_t c) {
         return m == 0 ? 0u : uint32_t(kOrderBuckets - 1) - uint32_t(uint64_t(c) * (kOrderBuckets - 1) / m);
     };
-    for (int i = tid; i < nseg; i += kOrderThreads) atomicAdd(&hist[bucket(seg_cost(tile_range, cost, i))], 1u);
+    // Warp-aggregated shared atomics: many segments share a bucket (empty
+    // segments all land in the last one), and same-address atomics serialise.
+    for (int i0 = 0; i0 < nseg; i0 += kOrderThreads) {
+        const int i = i0 + tid;
+        const uint32_t b = i < nseg ? bucket(seg_cost(tile_range, cost, i)) : 0xffffffffu;
+        const unsigned peers = __match_any_sync(0xffffffffu, b);
+        if (b != 0xffffffffu && lane == __ffs(peers) - 1) atomicAdd(&hist[b], __popc(peers));
+    }
     __syncthreads();
     // exclusive scan of the 1024 bucket counts (thread = bucket)
     const uint32_t h = hist[tid];
@@ -866,8 +873,16 @@ __global__ void __launch_bounds__(kOrderThreads) work_order_kernel(const uint2* 
     __syncthreads();
     hist[tid] = x - h + (wid > 0 ? wsum[wid - 1] : 0u);
     __syncthreads();
-    for (int i = tid; i < nseg; i += kOrderThreads)
-        order[atomicAdd(&hist[bucket(seg_cost(tile_range, cost, i))], 1u)] = uint32_t(i);
+    for (int i0 = 0; i0 < nseg; i0 += kOrderThreads) {
+        const int i = i0 + tid;
+        const uint32_t b = i < nseg ? bucket(seg_cost(tile_range, cost, i)) : 0xffffffffu;
+        const unsigned peers = __match_any_sync(0xffffffffu, b);
+        const int leader = __ffs(peers) - 1;
+        uint32_t pos = 0;
+        if (b != 0xffffffffu && lane == leader) pos = atomicAdd(&hist[b], __popc(peers));
+        pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(peers & ((1u << lane) - 1u));
+        if (b != 0xffffffffu) order[pos] = uint32_t(i);
+    }
 }
 
 }  // namespace
