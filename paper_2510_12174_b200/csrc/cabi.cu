@@ -171,7 +171,7 @@ struct msplat_replay {
         count_sorted, offset_sorted, inst_tile, inst_tile_alt, inst_gauss, inst_gauss_alt, tile_range,
         d_inst_count, d_inst_total32, hist, hist_scanned, scan_tiles, terminus, weight_sums, saved_means,
         saved_k, cap_center, cap_conic, cap_depth, cap_radius, cap_rgb, visible_count, ev_list, ev_count, ev_npairs,
-        pair_off, pair_n, pair_scan, pair_total, pair_rec, wq_order;
+        pair_off, pair_n, pair_scan, pair_total, pair_rec, wq_order, wq_scratch;
     int64_t pair_cap = 0;  // pair-record capacity of the FP32 split backward
     uint32_t* sorted_gauss = nullptr;
 
@@ -181,7 +181,8 @@ struct msplat_replay {
                           &inst_gauss, &inst_gauss_alt, &tile_range, &d_inst_count, &d_inst_total32, &hist,
                           &hist_scanned, &scan_tiles, &terminus, &weight_sums, &saved_means, &saved_k,
                           &cap_center, &cap_conic, &cap_depth, &cap_radius, &cap_rgb, &visible_count, &ev_list,
-                          &ev_count, &ev_npairs, &pair_off, &pair_n, &pair_scan, &pair_total, &pair_rec, &wq_order})
+                          &ev_count, &ev_npairs, &pair_off, &pair_n, &pair_scan, &pair_total, &pair_rec, &wq_order,
+                          &wq_scratch})
             b->release();
     }
 };
@@ -335,6 +336,7 @@ msplat_status size_replay(msplat_replay* r, int dtype, int64_t n, int C, int deg
     CUDA_TRY(r->ev_count.ensure(size_t(tiles) * 8 * 4));
     CUDA_TRY(r->ev_npairs.ensure(size_t(tiles) * 8 * 4));
     CUDA_TRY(r->wq_order.ensure(size_t(tiles) * 8 * 4));
+    CUDA_TRY(r->wq_scratch.ensure(2048 * 4));
     CUDA_TRY(r->inst_gauss.ensure(ic * 4));
     CUDA_TRY(r->inst_gauss_alt.ensure(ic * 4));
     CUDA_TRY(r->tile_range.ensure(size_t(tiles) * 8));
@@ -643,8 +645,8 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
     }
     ctx->timer.begin(MSPLAT_STAGE_BACKWARD, st);
     if (sizeof(Real) == 4 && !ctx->deterministic && dynamic_schedule())
-        launch_work_order(nullptr, r->ev_count.as<uint32_t>(), r->tiles_x * r->tiles_y * 8, r->wq_order.as<uint32_t>(),
-                          st);
+        launch_work_order(r->ev_count.as<uint32_t>(), r->tiles_x * r->tiles_y * 8, r->wq_order.as<uint32_t>(),
+                          r->wq_scratch.as<uint32_t>(), st);
     launch_backward_blend<Real>(a, r->tiles_x * r->tiles_y, st);
     if (ctx->deterministic)
         launch_deterministic_reduce<Real>(a, det, r->d_inst_count.as<int64_t>(), det_count, st);

@@ -109,11 +109,11 @@ template <typename Real>
 void launch_forward(const ForwardArgs<Real>& a, int ntiles, cudaStream_t s);
 
 // Longest-first order of the nseg = 8 * tiles (tile, warp) segments for the
-// FP32 backward: cost = seg_cost[i] (the forward's event counts) or, when
-// seg_cost is null, the tile's list length.  Coarse counting sort (1024 cost
-// buckets, arbitrary order inside a bucket: scheduling only, results do not
-// depend on it).
-void launch_work_order(const uint2* tile_range, const uint32_t* seg_cost, int nseg, uint32_t* order, cudaStream_t s);
+// FP32 backward, cost = seg_cost[i] (the forward's per-warp event counts):
+// a two-kernel counting sort into 1024 buckets (count, clamped), arbitrary
+// order inside a bucket (scheduling only: results do not depend on it).
+// scratch: 2048 uint32 (bucket sizes and cursors, zeroed here).
+void launch_work_order(const uint32_t* seg_cost, int nseg, uint32_t* order, uint32_t* scratch, cudaStream_t s);
 
 // K12: frame losses + seed assembly (core/src/trainer.cpp:171-264, losses.cpp).
 template <typename Real>
