@@ -38,6 +38,7 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--views", type=int, default=8, help="views per rank per step")
+    p.add_argument("--lanes", type=int, default=2, help="context lanes (concurrent streams) per rank")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--n", type=int, default=1_000_000)
     p.add_argument("--width", type=int, default=1200)
@@ -245,7 +246,8 @@ def workload_config(args, world, graph):
             "n_gaussians": args.n, "width": args.width, "height": args.height, "num_classes": args.classes,
             "sh_degree": args.sh_degree, "views_per_rank": args.views, "parallelism": f"view-sharded dp{world}",
             "l2": "inputs larger than L2 (scene 356 MB + 189 MB of pixel gradients per view)",
-            "cuda_graph": bool(graph)}
+            "cuda_graph": bool(graph), "lanes": args.lanes,
+            "stage_timing": "per-stage CUDA-event brackets from a single-lane replay of the same step"}
 
 
 # ---------------------------------------------------------------------- ours
@@ -299,7 +301,13 @@ def run_ours(args, rank, world, local_rank):
     replay = M.ReplayState(device=local_rank)
 
     from paper_2510_12174_b200.distributed import ViewShardedStep
-    sharded = ViewShardedStep(scene, flat, gflat, grads, opt, tc, rc, nc, cams, pixs, frame, replay, world)
+    sharded = ViewShardedStep(scene, flat, gflat, grads, opt, tc, rc, nc, cams, pixs, frame, replay, world,
+                              lanes=args.lanes)
+
+    # Single-lane twin sharing lane 0's frame / replay / gradients: its graph
+    # carries the per-stage event brackets (stage times of concurrent lanes
+    # would include each other's interference).
+    single = ViewShardedStep(scene, flat, gflat, grads, opt, tc, rc, nc, cams, pixs, frame, replay, world, lanes=1)
 
     def step(pix_list):
         sharded(pix_list)
@@ -312,23 +320,28 @@ def run_ours(args, rank, world, local_rank):
     counters = replay.counters()
     Pc, Pb, Pf = pair_counters(frame, replay, rc.early_stop_transmittance)
 
-    graph = None
+    def capture(fn, timing):
+        g = torch.cuda.CUDAGraph()
+        s_cap = torch.cuda.Stream(dev)
+        s_cap.wait_stream(stream)
+        R.set_stage_timing(timing, local_rank)
+        try:
+            with torch.cuda.graph(g, stream=s_cap):
+                fn(pixs)
+        finally:
+            R.set_stage_timing(False, local_rank)
+        torch.cuda.synchronize(dev)
+        return g
+
+    graph = stage_graph = None
     if not args.no_graph:
         try:
-            g = torch.cuda.CUDAGraph()
-            s_cap = torch.cuda.Stream(dev)
-            s_cap.wait_stream(stream)
-            R.set_stage_timing(True, local_rank)
-            with torch.cuda.graph(g, stream=s_cap):
-                step(pixs)
-            R.set_stage_timing(False, local_rank)
-            torch.cuda.synchronize(dev)
-            graph = g
+            graph = capture(step, False)
+            stage_graph = capture(single, True)
         except Exception as e:  # noqa: BLE001
-            R.set_stage_timing(False, local_rank)
             if rank == 0:
                 print(f"# cuda graph capture failed ({e}); timing eager launches", file=sys.stderr)
-            graph = None
+            graph = stage_graph = None
             torch.cuda.synchronize(dev)
     if graph is None:
         R.set_stage_timing(True, local_rank)
@@ -351,6 +364,9 @@ def run_ours(args, rank, world, local_rank):
     clk = clocks.stop()
     ms = t0.elapsed_time(t1)
     launches = R.kernel_launches() - launches0  # 0 under graph replay (no host launches)
+    if stage_graph is not None:  # per-stage brackets from a single-lane replay, after the timed region
+        stage_graph.replay()
+        torch.cuda.synchronize(dev)
     stage = R.stage_timings(local_rank)
     R.set_stage_timing(False, local_rank)
     R.check_device_errors(local_rank)

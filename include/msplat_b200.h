@@ -270,6 +270,14 @@ MSPLAT_API msplat_status msplat_adam_step(msplat_context* ctx, int dtype, int64_
                                int sh_degree, void* params, const void* grads, void* m, void* v,
                                int64_t step, const double lr[7]);
 
+/* dst += src over count packed values (device pointers, stream-ordered).  The
+ * gradient sum of a training step whose views were rendered on several
+ * context lanes (train() accumulates every view into one Gradients,
+ * core/src/trainer.cpp:295-309; here each lane accumulates its own views and
+ * the lane buffers are summed before chain/all-reduce/Adam). */
+MSPLAT_API msplat_status msplat_accumulate(msplat_context* ctx, int dtype, int64_t count, void* dst,
+                                           const void* src);
+
 /* prune() keep mask (core/src/trainer.cpp:135-147): keep[i] = !(|k-1| > T)
  * (or !(|k-1| < T) with keep_small).  Synchronizing; returns the kept count
  * in *kept and MSPLAT_ERR_RUNTIME if every Gaussian would be removed. */

@@ -8,7 +8,7 @@ hand-written sm_100a kernels behind the C ABI in include/msplat_b200.h.
 from . import _lib  # noqa: F401
 from .rasterizer import (  # noqa: F401
     CameraView, GradientBuffer, GroundTruth, LogicError, LossReport, MultimodalFrame, NormalConfig, OptimizerState,
-    PixelGradients, RenderConfig, ReplayState, Scene, TileBins, TrainConfig, adam_step, bin_and_sort,
+    PixelGradients, RenderConfig, ReplayState, Scene, TileBins, TrainConfig, accumulate_packed, adam_step, bin_and_sort,
     chain_activations, estimate_normals, frame_losses, frame_metrics, fwd_bwd, load_scene_ply, pack_scene, save_scene_ply, make_camera, make_lookat_camera, normals_backward,
     param_layout, prune, rasterize, rasterize_backward, set_deterministic, set_stage_timing, stage_timings,
 )

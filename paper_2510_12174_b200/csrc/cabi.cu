@@ -1020,6 +1020,19 @@ msplat_status msplat_adam_step(msplat_context* ctx, int dtype, int64_t n, int C,
     return MSPLAT_OK;
 }
 
+msplat_status msplat_accumulate(msplat_context* ctx, int dtype, int64_t count, void* dst, const void* src) {
+    if (!ctx || (count > 0 && (!dst || !src))) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "accumulate: null argument");
+    if (count < 0) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "accumulate: negative count");
+    if (dtype != MSPLAT_F32 && dtype != MSPLAT_F64)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "accumulate: dtype must be MSPLAT_F32 or MSPLAT_F64");
+    if (dtype == MSPLAT_F64)
+        launch_accumulate<double>(count, static_cast<double*>(dst), static_cast<const double*>(src), ctx->stream);
+    else
+        launch_accumulate<float>(count, static_cast<float*>(dst), static_cast<const float*>(src), ctx->stream);
+    CUDA_TRY(cudaGetLastError());
+    return MSPLAT_OK;
+}
+
 msplat_status msplat_context_set_timing(msplat_context* ctx, int enable) {
     if (!ctx) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null context");
     ctx->timer.enabled = enable != 0;

@@ -284,6 +284,9 @@ template <typename Real>
 void launch_adam(int64_t total, const int64_t* seg_starts /*host, 8*/, const double* lr /*7*/,
                  Real* params, const Real* grads, Real* m, Real* v, double bc1, double bc2,
                  cudaStream_t s);
+// dst += src over total packed values (multi-lane gradient sums).
+template <typename Real>
+void launch_accumulate(int64_t total, Real* dst, const Real* src, cudaStream_t s);
 template <typename Real>
 void launch_prune_mask(int64_t n, const Real* k, double threshold, int keep_small, uint8_t* keep,
                        unsigned long long* kept, cudaStream_t s);

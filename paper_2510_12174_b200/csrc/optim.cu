@@ -6,6 +6,7 @@
 //   prune mask (core/src/trainer.cpp:135-147): keep = !(|k-1| > T)
 //              (or !(|k-1| < T) with prune_keep_small).
 #include <algorithm>
+#include <cstdint>
 #include <type_traits>
 
 #include "common.cuh"
@@ -121,5 +122,42 @@ template void launch_prune_mask<float>(int64_t, const float*, double, int, uint8
                                        cudaStream_t);
 template void launch_prune_mask<double>(int64_t, const double*, double, int, uint8_t*, unsigned long long*,
                                         cudaStream_t);
+
+// dst += src over a packed buffer (the per-lane gradient sums of a multi-lane
+// training step): grid-stride 16-byte vectors, scalar tail.
+template <typename Real>
+__global__ void __launch_bounds__(256) accumulate_kernel(int64_t total, Real* __restrict__ dst,
+                                                         const Real* __restrict__ src, bool aligned) {
+    constexpr int VEC = 16 / sizeof(Real);
+    using V = typename std::conditional<sizeof(Real) == 4, float4, double2>::type;
+    const int64_t nvec = aligned ? total / VEC : 0;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    const int64_t t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (int64_t i = t0; i < nvec; i += stride) {
+        V d = reinterpret_cast<const V*>(dst)[i];
+        const V a = reinterpret_cast<const V*>(src)[i];
+        Real* dd = reinterpret_cast<Real*>(&d);
+        const Real* aa = reinterpret_cast<const Real*>(&a);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) dd[j] += aa[j];
+        reinterpret_cast<V*>(dst)[i] = d;
+    }
+    for (int64_t e = nvec * VEC + t0; e < total; e += stride) dst[e] += src[e];
+}
+
+template <typename Real>
+void launch_accumulate(int64_t total, Real* dst, const Real* src, cudaStream_t s) {
+    if (total <= 0) return;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const bool aligned = (reinterpret_cast<uintptr_t>(dst) % 16 == 0) && (reinterpret_cast<uintptr_t>(src) % 16 == 0);
+    const int64_t need = (total + 256 * 4 - 1) / (256 * 4);
+    const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sms) * 8)));
+    accumulate_kernel<Real><<<blocks, 256, 0, s>>>(total, dst, src, aligned);
+    count_launches(1);
+}
+template void launch_accumulate<float>(int64_t, float*, const float*, cudaStream_t);
+template void launch_accumulate<double>(int64_t, double*, const double*, cudaStream_t);
 
 }  // namespace msplat_cuda

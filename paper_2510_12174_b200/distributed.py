@@ -43,25 +43,69 @@ def reduce_gradients(flat: torch.Tensor, world: int | None = None) -> torch.Tens
     return flat
 
 
+def lane_views(num_views: int, lanes: int) -> list[list[int]]:
+    """Contiguous blocks of this rank's view indices, one per context lane."""
+    if lanes < 1:
+        raise ValueError("lane_views: lanes must be >= 1")
+    return [list(range(num_views * k // lanes, num_views * (k + 1) // lanes)) for k in range(lanes)]
+
+
 class ViewShardedStep:
     """One training step of `views` on this rank: fused fwd+bwd per view with
     gradient accumulation, chain once, all-reduce, Adam.  All tensors live on
     the rank's GPU; the call is asynchronous and CUDA-graph capturable once the
-    replay buffers are sized (first call)."""
+    replay buffers are sized (first call).
+
+    lanes > 1 splits the rank's views over that many context lanes, each with
+    its own stream, replay, frame and packed gradient buffer (lane 0 uses
+    `packed_grads`): the lanes' renders overlap on the GPU (one lane's
+    latency-bound preprocess / binning / kernel tails run beside another's
+    blend kernels), and their buffers are summed (msplat_accumulate) before
+    chain / all-reduce / Adam.  Same gradients up to float summation order."""
 
     def __init__(self, scene, packed_params, packed_grads, grads, opt, train_cfg, render_cfg, normal_cfg,
-                 cameras, pixel_grads, frame, replay, world: int = 1):
+                 cameras, pixel_grads, frame, replay, world: int = 1, lanes: int = 1):
+        from . import rasterizer as R
         self.scene, self.flat, self.gflat, self.grads = scene, packed_params, packed_grads, grads
         self.opt, self.tc, self.rc, self.nc = opt, train_cfg, render_cfg, normal_cfg
         self.cameras, self.pixel_grads, self.frame, self.replay = cameras, pixel_grads, frame, replay
         self.world = world
+        self.lanes = max(1, min(int(lanes), len(cameras)))
+        self.blocks = lane_views(len(cameras), self.lanes)
+        self.lane_state = [(frame, replay, grads, packed_grads)]
+        dev = packed_grads.device
+        for k in range(1, self.lanes):
+            g = torch.zeros_like(packed_grads)
+            self.lane_state.append((R.MultimodalFrame.empty(frame.width, frame.height, frame.num_classes,
+                                                            frame.color.dtype, dev),
+                                    R.ReplayState(device=dev.index, lane=k),
+                                    R.GradientBuffer.from_packed(g, scene.size(), scene.num_classes,
+                                                                 scene.sh_degree), g))
+        self.streams = [None] + [torch.cuda.Stream(dev) for _ in range(1, self.lanes)] if dev.type == "cuda" else []
 
     def __call__(self, pixel_grads=None):
         from . import rasterizer as R
         pix = self.pixel_grads if pixel_grads is None else pixel_grads
-        for j, cam in enumerate(self.cameras):
-            R.fwd_bwd(self.scene, cam, self.rc, self.nc, self.frame, pix[j], self.grads, self.replay,
-                      chain=False, accumulate=j > 0)
+        if self.lanes == 1:
+            for j, cam in enumerate(self.cameras):
+                R.fwd_bwd(self.scene, cam, self.rc, self.nc, self.frame, pix[j], self.grads, self.replay,
+                          chain=False, accumulate=j > 0)
+        else:
+            main = torch.cuda.current_stream(self.gflat.device)
+            for st in self.streams[1:]:
+                st.wait_stream(main)
+            for i in range(max(len(b) for b in self.blocks)):  # interleaved issue: lanes advance together
+                for k, views in enumerate(self.blocks):
+                    if i >= len(views):
+                        continue
+                    frame, replay, grads, _ = self.lane_state[k]
+                    with torch.cuda.stream(main if k == 0 else self.streams[k]):
+                        R.fwd_bwd(self.scene, self.cameras[views[i]], self.rc, self.nc, frame, pix[views[i]], grads,
+                                  replay, chain=False, accumulate=i > 0)
+            for st in self.streams[1:]:
+                main.wait_stream(st)
+            for k in range(1, self.lanes):
+                R.accumulate_packed(self.gflat, self.lane_state[k][3])
         self.grads.raw_space = False
         R.chain_activations(self.grads, self.scene)
         reduce_gradients(self.gflat, self.world)

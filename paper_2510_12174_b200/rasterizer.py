@@ -322,8 +322,10 @@ def param_layout(n: int, C: int, deg: int):
 
 # ---------------------------------------------------------------- context
 class _Context:
-    """One msplat_context per device; follows torch's current stream."""
-    _per_device: dict[int, "_Context"] = {}
+    """One msplat_context per (device, lane); follows torch's current stream.
+    Lanes are independent contexts (own scratch and error word) so that
+    renders on different streams of one device can run concurrently."""
+    _per_device: dict[tuple, "_Context"] = {}
 
     def __init__(self, device: int):
         self.device = device
@@ -333,11 +335,11 @@ class _Context:
         self.h = h
 
     @classmethod
-    def get(cls, device=None) -> "_Context":
+    def get(cls, device=None, lane: int = 0) -> "_Context":
         dev = torch.cuda.current_device() if device is None else int(device)
-        c = cls._per_device.get(dev)
+        c = cls._per_device.get((dev, lane))
         if c is None:
-            c = cls._per_device[dev] = _Context(dev)
+            c = cls._per_device[(dev, lane)] = _Context(dev)
         check(_lib.lib().msplat_context_set_stream(c.h, ct.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
         return c
 
@@ -347,8 +349,9 @@ class ReplayState:
 
     capture: 1 keeps FP64 splats (for parity checks), 2 records weight_sums."""
 
-    def __init__(self, capture: int = 0, device=None):
-        self._ctx = _Context.get(device)
+    def __init__(self, capture: int = 0, device=None, lane: int = 0):
+        self._ctx = _Context.get(device, lane)
+        self.lane = lane
         h = ct.c_void_p()
         check(_lib.lib().msplat_replay_create(self._ctx.h, ct.byref(h)))
         self.h = h
@@ -407,7 +410,7 @@ def rasterize(scene: Scene, view: CameraView, cfg: RenderConfig | None = None,
     """rasterize (rasterizer.cpp:87-205).  frame.normals stays zero until
     estimate_normals, exactly like the reference (rasterizer.cpp:101)."""
     cfg = cfg or RenderConfig()
-    ctx = _Context.get(scene.means.device.index)
+    ctx = _Context.get(scene.means.device.index, replay.lane if replay is not None else 0)
     frame = MultimodalFrame.empty(view.width, view.height, scene.num_classes, scene.dtype,
                                   scene.means.device)
     frame.transmittance.fill_(1.0)
@@ -563,7 +566,7 @@ def save_scene_ply(path: str, scene: Scene) -> None:
 def rasterize_backward(scene: Scene, view: CameraView, frame: MultimodalFrame, replay: ReplayState,
                        pix: PixelGradients) -> GradientBuffer:
     """rasterize_backward (rasterizer_backward.cpp:127-264); activated space."""
-    ctx = _Context.get(scene.means.device.index)
+    ctx = _Context.get(scene.means.device.index, replay.lane)
     grads = GradientBuffer.zeros_like_scene(scene)
     for t in (pix.dcolor, pix.ddepth, pix.dsemantics, pix.dkmap):
         if t.dtype != scene.dtype or not t.is_contiguous():
@@ -596,8 +599,10 @@ def fwd_bwd(scene: Scene, view: CameraView, cfg: RenderConfig, ncfg: NormalConfi
             chain: bool = True, accumulate: bool = False) -> None:
     """The fused training-step unit (msplat_fwd_bwd): rasterize, estimate_normals,
     normals_backward merged into ddepth, rasterize_backward, chain_activations.
-    Asynchronous on torch's current stream once the replay is sized."""
-    ctx = _Context.get(scene.means.device.index)
+    Asynchronous on torch's current stream once the replay is sized.  Runs on
+    the replay's context lane (ReplayState(lane=k)): renders of different lanes
+    may be issued on different streams concurrently."""
+    ctx = _Context.get(scene.means.device.index, replay.lane)
     check(_lib.lib().msplat_fwd_bwd(ctx.h, ct.byref(scene._abi()), ct.byref(view._abi()),
                                     ct.byref(cfg._abi()), ct.byref(ncfg._abi()), ct.byref(frame._abi()),
                                     ct.byref(pix._abi()), ct.byref(grads._abi()), int(chain),
@@ -709,6 +714,17 @@ def adam_step(scene: Scene, grads: GradientBuffer, state: OptimizerState, cfg: T
                                       state.v.data_ptr(), state.step, lr))
     if packed_params is None:
         unpack_into_scene(p, scene)
+
+
+def accumulate_packed(dst: torch.Tensor, src: torch.Tensor) -> None:
+    """dst += src (msplat_accumulate) on two packed buffers of one device, on
+    torch's current stream: sums per-lane gradient buffers of a multi-lane step."""
+    if dst.shape != src.shape or dst.dtype != src.dtype or dst.device != src.device:
+        raise ValueError("accumulate: buffers differ in shape, dtype or device")
+    if not (dst.is_contiguous() and src.is_contiguous()):
+        raise ValueError("accumulate: buffers must be contiguous")
+    ctx = _Context.get(dst.device.index)
+    check(_lib.lib().msplat_accumulate(ctx.h, _dtype_code(dst.dtype), dst.numel(), dst.data_ptr(), src.data_ptr()))
 
 
 def prune(scene: Scene, state: OptimizerState, cfg: TrainConfig) -> int:

@@ -56,6 +56,19 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
+def test_lane_views_partitions_a_ranks_views():
+    from paper_2510_12174_b200.distributed import lane_views
+    assert lane_views(8, 2) == [[0, 1, 2, 3], [4, 5, 6, 7]]
+    assert lane_views(5, 2) == [[0, 1], [2, 3, 4]]
+    assert lane_views(3, 1) == [[0, 1, 2]]
+    for V in range(1, 12):
+        for L in range(1, 5):
+            parts = lane_views(V, L)
+            assert sum(parts, []) == list(range(V)) and len(parts) == L
+    with pytest.raises(ValueError):
+        lane_views(4, 0)
+
+
 def test_shard_views_partitions_all_views():
     from paper_2510_12174_b200.distributed import shard_views
     for total in (1, 7, 8, 64):

@@ -223,6 +223,61 @@ def test_multiview_accumulation_is_sum_of_views(port):
         assert rel_l2_err(g[k], total[k]) < 1e-8, k
 
 
+@pytest.mark.parametrize("graph", [False, True])
+def test_multilane_step_gradients_equal_sum_of_views(port, graph):
+    """The view-sharded step with its views split over two context lanes on two
+    streams (ViewShardedStep(lanes=2): separate replays / frames / gradient
+    buffers, summed by msplat_accumulate) gives the oracle's summed, chained
+    gradients; also when the step is captured into a CUDA graph."""
+    import torch
+    import paper_2510_12174_b200 as M
+    from paper_2510_12174_b200.distributed import ViewShardedStep
+    V, W, H, C = 4, 96, 64, 4
+    s = scenes.make_room_scene(20000, C, 1, seed=3, views=tuple(range(V)), width=W, height=H, f=70.0)
+    scene = M.Scene.from_numpy(s, dtype=torch.float64)
+    n = scene.size()
+    off = M.param_layout(n, C, 1)
+    flat = M.pack_scene(scene)
+    gflat = torch.zeros(off[-1], dtype=torch.float64, device="cuda")
+    grads = M.GradientBuffer.from_packed(gflat, n, C, 1)
+    cams, pixs, total = [], [], None
+    for v in range(V):
+        cam = scenes.view_camera(v, W, H, 70.0)
+        cams.append(M.make_camera(cam["fx"], cam["fy"], cam["cx"], cam["cy"], W, H, cam["R_c2w"], cam["t_c2w"]))
+        pix = scenes.pixel_grads(W, H, C, seed=10 + v, scale=1.0)
+        pixs.append(torch_pix(pix, torch.float64))
+        _, gv, _ = port.fwd_bwd(s, cam, hwc_pix(pix), {})
+        total = dict(gv) if total is None else {k: total[k] + gv[k] for k in total}
+    frame = M.MultimodalFrame.empty(W, H, C, torch.float64, "cuda")
+    step = ViewShardedStep(scene, flat, gflat, grads, M.OptimizerState(torch.zeros_like(flat), torch.zeros_like(flat), 0),
+                           M.TrainConfig(), M.RenderConfig(), M.NormalConfig(), cams, pixs, frame, M.ReplayState(),
+                           lanes=2)
+    assert step.lanes == 2 and step.blocks == [[0, 1], [2, 3]]
+    # the step's Adam would move the scene: read the gradients in its place
+    import paper_2510_12174_b200.rasterizer as R
+    seen = {}
+
+    def keep(scene_, grads_, *a, **k):
+        seen["g"] = gflat.clone()
+    R_adam = R.adam_step
+    R.adam_step = keep
+    try:
+        step()  # sizes the replays (eager)
+        if graph:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream()
+            cap.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.graph(g, stream=cap):
+                step()
+            g.replay()
+        torch.cuda.synchronize()
+    finally:
+        R.adam_step = R_adam
+    from paper_2510_12174_b200.distributed import pack_grad_dict
+    assert rel_l2_err(seen["g"].cpu().numpy(), pack_grad_dict(total)) < 1e-8
+
+
 def test_bin_and_sort_reference_kat():
     """tests/test_rasterizer.cpp:35-88 on the device binning path."""
     import paper_2510_12174_b200 as M
