@@ -496,49 +496,61 @@ def run_train_step(args, dev, scene, flat, opt, tc, rc, nc, cams, iters=8, warm=
 
 def run_e2e(args, rank, world, dev, scene, grads, gflat, flat, opt, tc, rc, nc, cams, frame, replay, pixs,
             step_fn=None):
-    """Same step through the public API with HOST inputs: every view's pixel
-    gradients are copied from pinned host memory (on a copy stream, double
-    buffered so the next view's upload overlaps this view's kernels), and the
-    step's result (|grad|_1 of the reduced gradient) is read back."""
+    """Same step through the public API with HOST inputs: every step copies
+    each view's pixel gradients from pinned host memory (on a copy stream, in
+    the lanes' issue order; each view's render waits only for its own upload,
+    so uploads overlap the renders) and reads the step's result (|grad|_1 of
+    the reduced gradient) back to the host.  The step (uploads included) is a
+    CUDA graph of public-API calls (ViewShardedStep is capturable); wall-clock
+    timed around replay + read-back."""
     import torch
     import torch.distributed as dist
 
     import paper_2510_12174_b200 as M
+    from paper_2510_12174_b200.distributed import ViewShardedStep
 
     V = len(cams)
-    host = [[t.cpu().pin_memory() for t in (p.dcolor, p.ddepth, p.dsemantics, p.dkmap, p.dnormals)] for p in pixs]
-    slots = [M.PixelGradients(*(torch.empty_like(t) for t in (p.dcolor, p.ddepth, p.dsemantics, p.dkmap,
-                                                               p.dnormals))) for p in pixs[:2]]
+    fields = ("dcolor", "ddepth", "dsemantics", "dkmap", "dnormals")
+    host = [[getattr(p, f).cpu().pin_memory() for f in fields] for p in pixs]
+    dpix = [M.PixelGradients(*(torch.empty_like(getattr(p, f)) for f in fields)) for p in pixs]
     h2d = sum(t.numel() * t.element_size() for t in host[0]) * V
-    comp = torch.cuda.current_stream(dev)
+    step = ViewShardedStep(scene, flat, gflat, grads, opt, tc, rc, nc, cams, dpix, frame, replay, world,
+                           lanes=args.lanes)
     copy = torch.cuda.Stream(dev)
-    done_ev = [torch.cuda.Event(), torch.cuda.Event()]
-    ready_ev = [torch.cuda.Event(), torch.cuda.Event()]
+    ready = [torch.cuda.Event() for _ in range(V)]
 
-    def upload(j, slot):
-        copy.wait_event(done_ev[slot])
+    def body():
+        main = torch.cuda.current_stream(dev)
+        copy.wait_stream(main)
         with torch.cuda.stream(copy):
-            for dst, src in zip((slots[slot].dcolor, slots[slot].ddepth, slots[slot].dsemantics,
-                                 slots[slot].dkmap, slots[slot].dnormals), host[j]):
-                dst.copy_(src, non_blocking=True)
-        ready_ev[slot].record(copy)
+            for j in step.issue_order():
+                for f, src in zip(fields, host[j]):
+                    getattr(dpix[j], f).copy_(src, non_blocking=True)
+                ready[j].record(copy)
+        step(dpix, before_view=lambda j: torch.cuda.current_stream(dev).wait_event(ready[j]))
+        main.wait_stream(copy)
+
+    body()  # sizes the lanes' replays (eager)
+    torch.cuda.synchronize(dev)
+    graph = None
+    if not args.no_graph and world == 1:
+        try:
+            graph = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(dev)
+            cap.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.graph(graph, stream=cap):
+                body()
+            torch.cuda.synchronize(dev)
+        except Exception as e:  # noqa: BLE001
+            print(f"# e2e graph capture failed ({e}); eager", file=sys.stderr)
+            graph = None
+            torch.cuda.synchronize(dev)
 
     def e2e_step():
-        for ev in done_ev:
-            ev.record(comp)
-        upload(0, 0)
-        for j in range(V):
-            slot = j & 1
-            if j + 1 < V:
-                upload(j + 1, (j + 1) & 1)
-            comp.wait_event(ready_ev[slot])
-            M.fwd_bwd(scene, cams[j], rc, nc, frame, slots[slot], grads, replay, chain=False, accumulate=j > 0)
-            done_ev[slot].record(comp)
-        grads.raw_space = False
-        M.chain_activations(grads, scene)
-        if world > 1:
-            dist.all_reduce(gflat)
-        M.adam_step(scene, grads, opt, tc, packed_params=flat, packed_grads=gflat)
+        if graph is not None:
+            graph.replay()
+        else:
+            body()
         return float(gflat.abs().sum().item())  # device -> host read of the step's result
 
     for _ in range(max(1, min(args.warmup, 2))):
@@ -557,8 +569,10 @@ def run_e2e(args, rank, world, dev, scene, grads, gflat, flat, opt, tc, rc, nc, 
         dt = float(tt.item())
     return {"value": world * V * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": 4,
-            "note": "public Python API (msplat_fwd_bwd via ctypes), pinned-host pixel gradients uploaded per "
-                    "view on a copy stream overlapped with compute, eager launches, |grad|_1 read back"}
+            "note": f"public Python API (ViewShardedStep over msplat_fwd_bwd, {args.lanes} lanes); every step "
+                    "uploads all views' pixel gradients from pinned host memory on a copy stream (each render "
+                    "waits for its own view's upload) and reads |grad|_1 back; step captured as a CUDA graph "
+                    f"({'yes' if graph is not None else 'no, eager'}); wall clock"}
 
 
 def main():

@@ -83,11 +83,19 @@ class ViewShardedStep:
                                                                  scene.sh_degree), g))
         self.streams = [None] + [torch.cuda.Stream(dev) for _ in range(1, self.lanes)] if dev.type == "cuda" else []
 
-    def __call__(self, pixel_grads=None):
+    def issue_order(self) -> list[int]:
+        """Views in the order __call__ issues them (lanes interleaved)."""
+        return [b[i] for i in range(max(len(b) for b in self.blocks)) for b in self.blocks if i < len(b)]
+
+    def __call__(self, pixel_grads=None, before_view=None):
+        """before_view(j), when given, runs on view j's stream right before its
+        render is issued (e.g. to wait for that view's upload)."""
         from . import rasterizer as R
         pix = self.pixel_grads if pixel_grads is None else pixel_grads
         if self.lanes == 1:
             for j, cam in enumerate(self.cameras):
+                if before_view is not None:
+                    before_view(j)
                 R.fwd_bwd(self.scene, cam, self.rc, self.nc, self.frame, pix[j], self.grads, self.replay,
                           chain=False, accumulate=j > 0)
         else:
@@ -100,6 +108,8 @@ class ViewShardedStep:
                         continue
                     frame, replay, grads, _ = self.lane_state[k]
                     with torch.cuda.stream(main if k == 0 else self.streams[k]):
+                        if before_view is not None:
+                            before_view(views[i])
                         R.fwd_bwd(self.scene, self.cameras[views[i]], self.rc, self.nc, frame, pix[views[i]], grads,
                                   replay, chain=False, accumulate=i > 0)
             for st in self.streams[1:]:
