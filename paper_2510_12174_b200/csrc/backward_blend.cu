@@ -541,6 +541,9 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const __grid_cons
 namespace {
 
 constexpr int kK9Unroll = K9_UNROLL;
+#ifndef K9_RED2
+#define K9_RED2 1  // semantic GEMM2 outputs as 8-byte vector reductions (pairs from the g4^1 lane): 2.495 ms vs 2.509
+#endif
 #ifndef K9_PIPE
 #define K9_PIPE 1  // chunk ids one chunk ahead, F rows prefetched to L2 and records to L1 at chunk start: 2.55 ms vs 2.58
 #endif
@@ -795,6 +798,26 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
                     const float af[4] = {A0[0], A0[8], A0[4 * sp], A0[4 * sp + 8]};
                     mma_3xtf32(d2, af, bf);
                 }
+#if K9_RED2
+                if (mt > 0 && (C & 1) == 0) {
+                    // Semantic channels only: pair up channels (c, c + 1) of one event
+                    // with the neighbour lane (g4 ^ 1) and issue 8-byte vector reductions.
+                    const bool odd = g4 & 1;
+                    const int e = 2 * t4 + (odd ? 1 : 0);
+                    float* const semE = odd ? sem1 : sem0;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const float mine0 = d2[2 * h], mine1 = d2[2 * h + 1];
+                        const float recv = __shfl_xor_sync(0xffffffffu, odd ? mine0 : mine1, 4);
+                        const int c = mt * 16 + (g4 & ~1) + 8 * h;  // even channel of the pair
+                        const float lo = odd ? recv : mine0, hi = odd ? mine1 : recv;
+                        if (c < S && e < ns && (lo != 0.f || hi != 0.f))
+                            asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(semE + c), "f"(lo), "f"(hi)
+                                         : "memory");
+                    }
+                    continue;
+                }
+#endif
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int ch = mt * 16 + g4 + 8 * (i >> 1), e = 2 * t4 + (i & 1);
