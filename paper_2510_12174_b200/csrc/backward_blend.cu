@@ -28,7 +28,7 @@
 #include "radix_sort.cuh"
 
 #ifndef K9_UNROLL
-#define K9_UNROLL 4
+#define K9_UNROLL 8  // full sub-batch: 2.483 ms vs 2.494 at 4, 2.51 at 2
 #endif
 
 namespace msplat_cuda {
