@@ -541,6 +541,9 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const __grid_cons
 namespace {
 
 constexpr int kK9Unroll = K9_UNROLL;
+#ifndef K9B_MINB
+#define K9B_MINB 5  // phase-B CTAs per SM
+#endif
 #ifndef K9_RED2
 #define K9_RED2 1  // semantic GEMM2 outputs as 8-byte vector reductions (pairs from the g4^1 lane): 2.495 ms vs 2.509
 #endif
@@ -840,7 +843,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
 // reduced per Gaussian inside the warp into the acc16 rows.  Split from phase A
 // so that neither carries the other's registers; 5 blocks/SM (48 registers,
 // spills hit the large L1 this kernel leaves) hides its gather latency best.
-__global__ void __launch_bounds__(256, 5) backward_pairs_kernel(const __grid_constant__ BackwardArgs<float> a, int nseg) {
+__global__ void __launch_bounds__(256, K9B_MINB) backward_pairs_kernel(const __grid_constant__ BackwardArgs<float> a, int nseg) {
     __shared__ float4 rays[8][32];  // the segment's pixel rays (cached_ray)
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int item = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
