@@ -376,3 +376,24 @@ def test_adam_and_prune_match_oracle(port):
         assert removed == int((~mask_ref).sum())
         assert sc.size() == int(mask_ref.sum())
         assert np.all(sc.k.cpu().numpy() == 0.9)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+@pytest.mark.parametrize("count,offset", [(1, 0), (7, 0), (4096 + 3, 0), (1000, 1)])
+def test_accumulate_packed(dtype, count, offset):
+    """msplat_accumulate (dst += src) on vector and scalar-tail paths, aligned
+    and misaligned views, against the host sum."""
+    import torch
+    import paper_2510_12174_b200 as M
+    dt = getattr(torch, dtype)
+    g = torch.Generator().manual_seed(count)
+    a = torch.randn(count + offset, generator=g, dtype=torch.float64)
+    b = torch.randn(count + offset, generator=g, dtype=torch.float64)
+    dst = a.to(dt).cuda()[offset:]
+    src = b.to(dt).cuda()[offset:]
+    want = (a.to(dt)[offset:] + b.to(dt)[offset:]).numpy()
+    M.accumulate_packed(dst, src)
+    torch.cuda.synchronize()
+    assert np.array_equal(dst.cpu().numpy(), want)
+    with pytest.raises(ValueError):
+        M.accumulate_packed(dst, src[:-1] if count > 1 else src.double() if dtype == "float32" else src.float())
