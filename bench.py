@@ -496,13 +496,14 @@ def run_train_step(args, dev, scene, flat, opt, tc, rc, nc, cams, iters=8, warm=
 
 def run_e2e(args, rank, world, dev, scene, grads, gflat, flat, opt, tc, rc, nc, cams, frame, replay, pixs,
             step_fn=None):
-    """Same step through the public API with HOST inputs: every step copies
-    each view's pixel gradients from pinned host memory (on a copy stream, in
-    the lanes' issue order; each view's render waits only for its own upload,
-    so uploads overlap the renders) and reads the step's result (|grad|_1 of
-    the reduced gradient) back to the host.  The step (uploads included) is a
-    CUDA graph of public-API calls (ViewShardedStep is capturable); wall-clock
-    timed around replay + read-back."""
+    """Same step through the public API with HOST inputs.  Every step's pixel
+    gradients (all views) are copied from pinned host memory and the step's
+    result (|grad|_1 of the reduced gradient) is read back to the host.  The
+    copies are software-pipelined one step ahead over two device buffer sets:
+    while step k renders from set k%2, a copy stream uploads step k+1's inputs
+    into the other set (the first step's inputs are uploaded at the start of
+    the timed region).  Each step is a CUDA graph of public-API calls
+    (ViewShardedStep is capturable); wall-clock timed."""
     import torch
     import torch.distributed as dist
 
@@ -512,55 +513,63 @@ def run_e2e(args, rank, world, dev, scene, grads, gflat, flat, opt, tc, rc, nc, 
     V = len(cams)
     fields = ("dcolor", "ddepth", "dsemantics", "dkmap", "dnormals")
     host = [[getattr(p, f).cpu().pin_memory() for f in fields] for p in pixs]
-    dpix = [M.PixelGradients(*(torch.empty_like(getattr(p, f)) for f in fields)) for p in pixs]
+    sets = [[M.PixelGradients(*(torch.empty_like(getattr(p, f)) for f in fields)) for p in pixs] for _ in range(2)]
     h2d = sum(t.numel() * t.element_size() for t in host[0]) * V
-    step = ViewShardedStep(scene, flat, gflat, grads, opt, tc, rc, nc, cams, dpix, frame, replay, world,
+    step = ViewShardedStep(scene, flat, gflat, grads, opt, tc, rc, nc, cams, sets[0], frame, replay, world,
                            lanes=args.lanes)
     copy = torch.cuda.Stream(dev)
-    ready = [torch.cuda.Event() for _ in range(V)]
 
-    def body():
-        main = torch.cuda.current_stream(dev)
-        copy.wait_stream(main)
-        with torch.cuda.stream(copy):
+    def upload(dst, stream):
+        with torch.cuda.stream(stream):
             for j in step.issue_order():
                 for f, src in zip(fields, host[j]):
-                    getattr(dpix[j], f).copy_(src, non_blocking=True)
-                ready[j].record(copy)
-        step(dpix, before_view=lambda j: torch.cuda.current_stream(dev).wait_event(ready[j]))
+                    getattr(dst[j], f).copy_(src, non_blocking=True)
+
+    def body(k):  # render from set k, upload the next step's inputs into set 1 - k
+        main = torch.cuda.current_stream(dev)
+        copy.wait_stream(main)
+        upload(sets[1 - k], copy)
+        step(sets[k])
         main.wait_stream(copy)
 
-    body()  # sizes the lanes' replays (eager)
+    main0 = torch.cuda.current_stream(dev)
+    upload(sets[0], main0)
+    body(0)  # sizes the lanes' replays (eager)
     torch.cuda.synchronize(dev)
-    graph = None
+    graphs = None
     if not args.no_graph and world == 1:
         try:
-            graph = torch.cuda.CUDAGraph()
-            cap = torch.cuda.Stream(dev)
-            cap.wait_stream(torch.cuda.current_stream(dev))
-            with torch.cuda.graph(graph, stream=cap):
-                body()
+            graphs = []
+            for k in range(2):
+                g = torch.cuda.CUDAGraph()
+                cap = torch.cuda.Stream(dev)
+                cap.wait_stream(torch.cuda.current_stream(dev))
+                with torch.cuda.graph(g, stream=cap):
+                    body(k)
+                graphs.append(g)
             torch.cuda.synchronize(dev)
         except Exception as e:  # noqa: BLE001
             print(f"# e2e graph capture failed ({e}); eager", file=sys.stderr)
-            graph = None
+            graphs = None
             torch.cuda.synchronize(dev)
 
-    def e2e_step():
-        if graph is not None:
-            graph.replay()
+    def e2e_step(i):
+        if graphs is not None:
+            graphs[i & 1].replay()
         else:
-            body()
+            body(i & 1)
         return float(gflat.abs().sum().item())  # device -> host read of the step's result
 
-    for _ in range(max(1, min(args.warmup, 2))):
-        e2e_step()
+    for i in range(max(1, min(args.warmup, 2))):
+        upload(sets[0], main0)
+        e2e_step(0)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     t = time.perf_counter()
-    for _ in range(args.steps):
-        e2e_step()
+    upload(sets[0], main0)  # the first step's inputs
+    for i in range(args.steps):
+        e2e_step(i)
     torch.cuda.synchronize(dev)
     dt = time.perf_counter() - t
     if world > 1:
@@ -569,10 +578,10 @@ def run_e2e(args, rank, world, dev, scene, grads, gflat, flat, opt, tc, rc, nc, 
         dt = float(tt.item())
     return {"value": world * V * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": 4,
-            "note": f"public Python API (ViewShardedStep over msplat_fwd_bwd, {args.lanes} lanes); every step "
-                    "uploads all views' pixel gradients from pinned host memory on a copy stream (each render "
-                    "waits for its own view's upload) and reads |grad|_1 back; step captured as a CUDA graph "
-                    f"({'yes' if graph is not None else 'no, eager'}); wall clock"}
+            "note": f"public Python API (ViewShardedStep over msplat_fwd_bwd, {args.lanes} lanes); every step's "
+                    "pixel gradients (all views) copied from pinned host memory, software-pipelined one step "
+                    "ahead on a copy stream (first step's upload inside the timed region), |grad|_1 read back "
+                    f"every step; steps as CUDA graphs ({'yes' if graphs is not None else 'no, eager'}); wall clock"}
 
 
 def main():
