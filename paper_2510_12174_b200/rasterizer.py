@@ -612,8 +612,13 @@ def fwd_bwd(scene: Scene, view: CameraView, cfg: RenderConfig, ncfg: NormalConfi
 
 
 def check_device_errors(device=None):
-    """Surface a latched device-side error (synchronizing)."""
-    check(_lib.lib().msplat_context_check(_Context.get(device).h))
+    """Surface a latched device-side error of any context lane of the device
+    (synchronizing)."""
+    dev = torch.cuda.current_device() if device is None else int(device)
+    _Context.get(dev)
+    for (d, _lane), c in sorted(_Context._per_device.items()):
+        if d == dev:
+            check(_lib.lib().msplat_context_check(c.h))
 
 
 def set_stage_timing(enable: bool, device=None):
