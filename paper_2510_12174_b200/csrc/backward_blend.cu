@@ -544,6 +544,9 @@ constexpr int kK9Unroll = K9_UNROLL;
 #ifndef K9B_MINB
 #define K9B_MINB 5  // phase-B CTAs per SM
 #endif
+#ifndef K9_RED2_MT0
+#define K9_RED2_MT0 1  // also the semantic pairs of channel tile 0 (colour / k stay scalar): 2.486 ms vs 2.494
+#endif
 #ifndef K9_RED2
 #define K9_RED2 1  // semantic GEMM2 outputs as 8-byte vector reductions (pairs from the g4^1 lane): 2.495 ms vs 2.509
 #endif
@@ -802,7 +805,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
                     mma_3xtf32(d2, af, bf);
                 }
 #if K9_RED2
-                if (mt > 0 && (C & 1) == 0) {
+                if ((mt > 0 || K9_RED2_MT0) && (C & 1) == 0) {
                     // Semantic channels only: pair up channels (c, c + 1) of one event
                     // with the neighbour lane (g4 ^ 1) and issue 8-byte vector reductions.
                     const bool odd = g4 & 1;
@@ -814,9 +817,21 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
                         const float recv = __shfl_xor_sync(0xffffffffu, odd ? mine0 : mine1, 4);
                         const int c = mt * 16 + (g4 & ~1) + 8 * h;  // even channel of the pair
                         const float lo = odd ? recv : mine0, hi = odd ? mine1 : recv;
-                        if (c < S && e < ns && (lo != 0.f || hi != 0.f))
-                            asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(semE + c), "f"(lo), "f"(hi)
-                                         : "memory");
+                        if (c >= 4) {
+                            if (c < S && e < ns && (lo != 0.f || hi != 0.f))
+                                asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(semE + c), "f"(lo),
+                                             "f"(hi)
+                                             : "memory");
+                        } else {  // colour / k channels (tile 0 only): this lane's own two values
+                            const int ch = mt * 16 + g4 + 8 * h;
+#pragma unroll
+                            for (int q = 0; q < 2; ++q) {
+                                const float v = d2[2 * h + q];
+                                const uint32_t gg = q ? ge1 : ge0;
+                                if (2 * t4 + q < ns && v != 0.f)
+                                    atomicAdd(ch < 3 ? a.acc_dcolor + size_t(gg) * 3 + ch : a.g_k + gg, v);
+                            }
+                        }
                     }
                     continue;
                 }
