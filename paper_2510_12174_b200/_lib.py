@@ -125,6 +125,8 @@ def _sig(lib):
         ("msplat_accumulate", ct.c_int, [_vp, ct.c_int, _i64, _vp, _vp]),
         ("msplat_prune_mask", ct.c_int, [_vp, ct.c_int, _i64, _vp, ct.c_double, ct.c_int, _vp,
                                          P(_i64)]),
+        ("msplat_prune_compact", ct.c_int, [_vp, ct.c_int, _i64, ct.c_int, ct.c_int, _vp, _i64, P(_vp), P(_vp),
+                                            ct.c_double]),
         ("msplat_replay_counters", ct.c_int, [_vp, P(MsplatCounters)]),
         ("msplat_replay_bins", ct.c_int, [_vp, P(_i64), P(ct.c_int32), _i64]),
         ("msplat_replay_splats", ct.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -302,11 +302,8 @@ template <typename Real>
 void launch_projection_backward(const ProjBackwardArgs<Real>& a, cudaStream_t s) {
     if (a.n == 0) return;
     const size_t smem = k10_smem_bytes<Real>(a.K);
-    static bool configured = false;  // per instantiation
-    if (!configured) {
-        cudaFuncSetAttribute(projection_backward_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        configured = true;
-    }
+    static std::atomic<unsigned long long> attr{0};  // per instantiation, per device
+    opt_in_smem(reinterpret_cast<const void*>(projection_backward_kernel<Real>), attr);
     projection_backward_kernel<Real><<<unsigned((a.n + kK10Threads - 1) / kK10Threads), kK10Threads, smem, s>>>(a);
     count_launches(1);
 }

@@ -582,16 +582,16 @@ size_t backward_tc_smem_bytes(int C) {
 // Stages F rows [rgb, k | sem] of n (<= kSub) events into rows of pitch sp:
 // one 16-byte copy of (rgb, k) per row from the AlphaRec (offset 48, the line
 // the sub-batch's records come from) and the semantic row in 8-byte pieces
-// when C is even (4-byte otherwise).  A lane owns a fixed piece column and
+// when C is even and the rows are 8-byte aligned (4-byte otherwise).  A lane owns a fixed piece column and
 // walks the rows, so the loop carries no index arithmetic.
 __device__ __forceinline__ void stage_rows_tc(float* Fb, int sp, const AlphaRec<float>* arec, const float* semantics,
-                                              int C, const uint32_t* gid, int n, int lane) {
+                                              int C, bool vec, const uint32_t* gid, int n, int lane) {
     if (lane < n) {
         const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + lane * sp));
         asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(&arec[gid[lane]].rgb[0]) : "memory");
     }
     const unsigned base = unsigned(__cvta_generic_to_shared(Fb + 4));
-    if ((C & 1) == 0) {
+    if (vec) {
         for (int j = lane; j < C / 2; j += 32) {
             const float* const src = semantics + 2 * j;
 #pragma unroll
@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
         for (int s0 = 0; s0 < nb; s0 += kSub) {
             const int ns = nb - s0 < kSub ? nb - s0 : kSub;
             // (a) F rows (cp.async) and alpha records of the sub-batch.
-            stage_rows_tc(Fb, sp, a.arec, a.semantics, C, ws->gid + s0, ns, lane);
+            stage_rows_tc(Fb, sp, a.arec, a.semantics, C, a.sem_vec != 0, ws->gid + s0, ns, lane);
             if (lane < ns) ws->rec[lane] = a.arec[ws->gid[s0 + lane]];
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncwarp();
@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
                     mma_3xtf32(d2, af, bf);
                 }
 #if K9_RED2
-                if ((mt > 0 || K9_RED2_MT0) && (C & 1) == 0) {
+                if ((mt > 0 || K9_RED2_MT0) && a.sem_vec) {
                     // Semantic channels only: pair up channels (c, c + 1) of one event
                     // with the neighbour lane (g4 ^ 1) and issue 8-byte vector reductions.
                     const bool odd = g4 & 1;
@@ -960,20 +960,14 @@ void launch_work_order(const uint32_t* seg_cost, int nseg, uint32_t* order, uint
 template <typename Real>
 void launch_backward_blend(const BackwardArgs<Real>& a, int ntiles, cudaStream_t s) {
     if (ntiles == 0) return;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(backward_kernel<Real, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(backward_kernel<Real, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        configured = true;
-    }
+    static std::atomic<unsigned long long> attr0{0}, attr1{0};  // per instantiation, per device
+    opt_in_smem(reinterpret_cast<const void*>(backward_kernel<Real, false>), attr0);
+    opt_in_smem(reinterpret_cast<const void*>(backward_kernel<Real, true>), attr1);
     if (a.partial) {
         backward_kernel<Real, true><<<ntiles, kThreads, backward_smem_bytes<Real>(a.C), s>>>(a);
     } else if constexpr (sizeof(Real) == 4) {
-        static bool tc_configured = false;
-        if (!tc_configured) {
-            cudaFuncSetAttribute(backward_kernel_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            tc_configured = true;
-        }
+        static std::atomic<unsigned long long> attr_tc{0};
+        opt_in_smem(reinterpret_cast<const void*>(backward_kernel_tc), attr_tc);
         backward_kernel_tc<<<ntiles, kThreads, backward_tc_smem_bytes(a.C), s>>>(a);
         backward_pairs_kernel<<<unsigned((ntiles * 8 + 7) / 8), 256, 0, s>>>(a, ntiles * 8);
         count_launches(1);

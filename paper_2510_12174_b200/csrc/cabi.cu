@@ -35,6 +35,25 @@ msplat_status set_error(msplat_status st, const std::string& msg) {
                              std::string("CUDA error: ") + cudaGetErrorString(e_) + " (" #expr ")"); \
     } while (0)
 
+// Makes a context's device current for the duration of an entry point and
+// restores the caller's device afterwards (dev < 0: no-op).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (dev < 0) return;
+        int cur = -1;
+        if (cudaGetDevice(&cur) != cudaSuccess) return;
+        if (cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+#define CTX_DEVICE_GUARD(c) DeviceGuard device_guard_((c) ? (c)->device : -1)
+#define REPLAY_DEVICE_GUARD(r) DeviceGuard device_guard_((r) && (r)->ctx ? (r)->ctx->device : -1)
+
 // Grow-only device allocation.
 struct DevBuf {
     void* p = nullptr;
@@ -642,6 +661,8 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
         af.pr = rw->pair_rec.as<uint4>();
         af.pair_cap = rw->pair_cap;
         if (dynamic_schedule()) af.work_order = rw->wq_order.as<uint32_t>();
+        af.sem_vec = (C % 2 == 0) && (reinterpret_cast<uintptr_t>(s->semantics) % 8 == 0) &&
+                     (reinterpret_cast<uintptr_t>(g->dsemantics) % 8 == 0);
     }
     ctx->timer.begin(MSPLAT_STAGE_BACKWARD, st);
     if (sizeof(Real) == 4 && !ctx->deterministic && dynamic_schedule())
@@ -755,7 +776,10 @@ int msplat_abi_version(void) { return MSPLAT_ABI_VERSION; }
 msplat_status msplat_context_create(int device, void* cuda_stream, msplat_context** out) {
     if (!out) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null output");
     *out = nullptr;
-    CUDA_TRY(cudaSetDevice(device));
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "context: no such device");
+    DeviceGuard device_guard_(device);  // the caller's current device is restored on return
     auto* ctx = new msplat_context();
     ctx->device = device;
     if (cuda_stream) {
@@ -777,12 +801,13 @@ msplat_status msplat_context_create(int device, void* cuda_stream, msplat_contex
 }
 
 void msplat_context_destroy(msplat_context* ctx) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx) return;
     cudaStreamSynchronize(ctx->stream);
     for (DevBuf* b : {&ctx->acc_dcolor, &ctx->acc16, &ctx->loss_acc, &ctx->loss_report, &ctx->metric_acc, &ctx->metric_hist, &ctx->ssim_maps, &ctx->ssim_grad, &ctx->loss_dN, &ctx->init_pts,
                        &ctx->init_cols, &ctx->init_logs, &ctx->cmp_k32, &ctx->cmp_idx, &ctx->cmp_tiles, &ctx->cmp_total,
-                       &ctx->ddepth_total, &ctx->normal_dv,
-                      &ctx->kept})
+                       &ctx->ddepth_total, &ctx->normal_dv, &ctx->kept, &ctx->det_partial, &ctx->det_keys,
+                       &ctx->det_keys_alt, &ctx->det_vals, &ctx->det_vals_alt, &ctx->det_range})
         b->release();
     cudaFree(ctx->d_err);
     cudaFreeHost(ctx->h_err);
@@ -792,6 +817,7 @@ void msplat_context_destroy(msplat_context* ctx) {
 }
 
 msplat_status msplat_context_set_stream(msplat_context* ctx, void* cuda_stream) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null context");
     if (ctx->own_stream) {
         cudaStreamSynchronize(ctx->stream);
@@ -803,12 +829,14 @@ msplat_status msplat_context_set_stream(msplat_context* ctx, void* cuda_stream) 
 }
 
 msplat_status msplat_context_check(msplat_context* ctx) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null context");
     CUDA_TRY(cudaGetLastError());
     return drain_device_error(ctx, 0);
 }
 
 msplat_status msplat_replay_create(msplat_context* ctx, msplat_replay** out) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx || !out) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null argument");
     *out = new msplat_replay();
     (*out)->ctx = ctx;
@@ -816,6 +844,7 @@ msplat_status msplat_replay_create(msplat_context* ctx, msplat_replay** out) {
 }
 
 void msplat_replay_destroy(msplat_replay* r) {
+    REPLAY_DEVICE_GUARD(r);
     if (!r) return;
     cudaStreamSynchronize(r->ctx->stream);
     r->release_all();
@@ -823,6 +852,7 @@ void msplat_replay_destroy(msplat_replay* r) {
 }
 
 msplat_status msplat_replay_set_capture(msplat_replay* r, int flags) {
+    REPLAY_DEVICE_GUARD(r);
     if (!r) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null replay");
     r->capture = flags;
     return MSPLAT_OK;
@@ -866,11 +896,13 @@ static msplat_status rasterize_entry(msplat_context* ctx, const msplat_scene* s,
 
 msplat_status msplat_rasterize(msplat_context* ctx, const msplat_scene* s, const msplat_camera* cam,
                                const msplat_render_config* cfg, const msplat_frame* f, msplat_replay* replay) {
+    CTX_DEVICE_GUARD(ctx);
     return rasterize_entry(ctx, s, cam, cfg, f, replay, true);
 }
 
 msplat_status msplat_estimate_normals(msplat_context* ctx, int dtype, const void* depth, const void* T,
                                       const msplat_camera* cam, const msplat_normal_config* ncfg, void* normals) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx || !depth || !T || !normals) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "estimate_normals: null argument");
     msplat_status st = check_ncfg(ncfg);
     if (st != MSPLAT_OK) return st;
@@ -894,6 +926,7 @@ msplat_status msplat_estimate_normals(msplat_context* ctx, int dtype, const void
 msplat_status msplat_normals_backward(msplat_context* ctx, int dtype, const void* dN, const void* depth, const void* T,
                                       const msplat_camera* cam, const msplat_normal_config* ncfg, double seed,
                                       void* dD) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx || !dN || !depth || !T || !dD)
         return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "normals_backward: gradient shape mismatch");
     msplat_status st = check_ncfg(ncfg);
@@ -942,6 +975,7 @@ static msplat_status backward_checks(const msplat_scene* s, const msplat_camera*
 msplat_status msplat_rasterize_backward(msplat_context* ctx, const msplat_scene* s, const msplat_camera* cam,
                                         const msplat_frame* f, const msplat_replay* r, const msplat_pixel_grads* pix,
                                         msplat_grads* g) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null context");
     msplat_status st = backward_checks(s, cam, f, r, pix, g);
     if (st != MSPLAT_OK) return st;
@@ -952,6 +986,7 @@ msplat_status msplat_rasterize_backward(msplat_context* ctx, const msplat_scene*
 }
 
 msplat_status msplat_chain_activations(msplat_context* ctx, const msplat_scene* s, msplat_grads* g) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx || !g) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "chain_activations: null argument");
     msplat_status st = check_scene(s);
     if (st != MSPLAT_OK) return st;
@@ -971,6 +1006,7 @@ msplat_status msplat_fwd_bwd(msplat_context* ctx, const msplat_scene* s, const m
                              const msplat_render_config* cfg, const msplat_normal_config* ncfg, const msplat_frame* f,
                              const msplat_pixel_grads* pix, msplat_grads* g, int chain, int accumulate,
                              msplat_replay* r) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx || !r || !f || !f->depth || !f->transmittance)
         return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "fwd_bwd: null argument (replay, depth and T required)");
     msplat_status st = check_ncfg(ncfg);
@@ -1002,6 +1038,7 @@ msplat_status msplat_fwd_bwd(msplat_context* ctx, const msplat_scene* s, const m
 
 msplat_status msplat_adam_step(msplat_context* ctx, int dtype, int64_t n, int C, int deg, void* params,
                                const void* grads, void* m, void* v, int64_t step, const double lr[7]) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx || !params || !grads || !m || !v || !lr) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "adam_step: null argument");
     if (step < 1) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "adam_step: step must be >= 1");
     int64_t off[8];
@@ -1021,6 +1058,7 @@ msplat_status msplat_adam_step(msplat_context* ctx, int dtype, int64_t n, int C,
 }
 
 msplat_status msplat_accumulate(msplat_context* ctx, int dtype, int64_t count, void* dst, const void* src) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx || (count > 0 && (!dst || !src))) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "accumulate: null argument");
     if (count < 0) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "accumulate: negative count");
     if (dtype != MSPLAT_F32 && dtype != MSPLAT_F64)
@@ -1034,6 +1072,7 @@ msplat_status msplat_accumulate(msplat_context* ctx, int dtype, int64_t count, v
 }
 
 msplat_status msplat_context_set_timing(msplat_context* ctx, int enable) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null context");
     ctx->timer.enabled = enable != 0;
     return MSPLAT_OK;
@@ -1043,6 +1082,7 @@ msplat_status msplat_frame_losses(msplat_context* ctx, int dtype, int num_classe
                                   const msplat_normal_config* ncfg, const msplat_frame* frame,
                                   const msplat_ground_truth* gt, const double lambdas[6], msplat_pixel_grads* out,
                                   msplat_loss_report* host_report) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx || !frame || !gt || !lambdas || !out) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "frame_losses: null argument");
     if (dtype != MSPLAT_F32 && dtype != MSPLAT_F64)
         return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "frame_losses: dtype must be MSPLAT_F32 or MSPLAT_F64");
@@ -1087,6 +1127,7 @@ msplat_status msplat_frame_losses(msplat_context* ctx, int dtype, int num_classe
 }
 
 const double* msplat_loss_report_device(msplat_context* ctx) {
+    CTX_DEVICE_GUARD(ctx);
     return ctx ? static_cast<const double*>(ctx->loss_report.p) : nullptr;
 }
 
@@ -1095,6 +1136,7 @@ msplat_status msplat_frame_metrics(msplat_context* ctx, int dtype, int width, in
                                    const uint8_t* depth_mask, const void* normals, const void* gt_normal,
                                    const uint8_t* normal_mask, const void* semantics, const uint8_t* gt_labels,
                                    const uint8_t* label_mask, msplat_metric_report* out) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx || !out) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "frame_metrics: null argument");
     if (width < 1 || height < 1 || num_classes < 0)
         return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "frame_metrics: bad frame size");
@@ -1207,6 +1249,7 @@ msplat_status msplat_ply_scene_info(const char* path, int64_t* n, int* num_class
 }
 
 msplat_status msplat_load_scene_ply(msplat_context* ctx, const char* path, int dtype, void* params) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx || !path || !params) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "load_scene_ply: null argument");
     if (dtype == MSPLAT_F64) return io_status(ply_load_scene<double>(path, static_cast<double*>(params), ctx->stream, ctx->d_err));
     if (dtype == MSPLAT_F32) return io_status(ply_load_scene<float>(path, static_cast<float*>(params), ctx->stream, ctx->d_err));
@@ -1215,6 +1258,7 @@ msplat_status msplat_load_scene_ply(msplat_context* ctx, const char* path, int d
 
 msplat_status msplat_save_scene_ply(msplat_context* ctx, const char* path, int dtype, int64_t n, int num_classes,
                                     int sh_degree, const void* params) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx || !path || (n > 0 && !params)) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "save_scene_ply: null argument");
     if (sh_degree < 0 || sh_degree > 3) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "Scene: sh_degree must be in [0,3]");
     if (num_classes < 0) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "Scene: num_classes must be >= 0");
@@ -1227,6 +1271,7 @@ msplat_status msplat_save_scene_ply(msplat_context* ctx, const char* path, int d
 
 msplat_status msplat_init_scene(msplat_context* ctx, int dtype, int64_t n, const double* points, const double* colors,
                                 int num_classes, int sh_degree, double k_reset, void* params) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx || !params) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "init_scene: null argument");
     if (n <= 0 || !points) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "init_scene: empty point list");
     if (!colors) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "init_scene: point/color count mismatch");
@@ -1254,6 +1299,7 @@ msplat_status msplat_init_scene(msplat_context* ctx, int dtype, int64_t n, const
 msplat_status msplat_prune_compact(msplat_context* ctx, int dtype, int64_t n, int num_classes, int sh_degree,
                                    const uint8_t* keep, int64_t kept, const void* const in[3], void* const out[3],
                                    double k_reset) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx || !keep || !in || !out || !in[0] || !out[0])
         return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "prune: null argument");
     if (kept <= 0) return set_error(MSPLAT_ERR_RUNTIME, "prune: every gaussian would be removed");
@@ -1284,6 +1330,7 @@ msplat_status msplat_prune_compact(msplat_context* ctx, int dtype, int64_t n, in
 }
 
 msplat_status msplat_context_set_deterministic(msplat_context* ctx, int enable) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null context");
     ctx->deterministic = enable != 0;
     return MSPLAT_OK;
@@ -1291,6 +1338,7 @@ msplat_status msplat_context_set_deterministic(msplat_context* ctx, int enable) 
 
 msplat_status msplat_context_timings(msplat_context* ctx, double ms[MSPLAT_STAGE_COUNT],
                                      int64_t calls[MSPLAT_STAGE_COUNT]) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx || !ms) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "null argument");
     ctx->timer.collect(ms, calls);
     CUDA_TRY(cudaGetLastError());
@@ -1301,6 +1349,7 @@ int64_t msplat_kernel_launches(void) { return int64_t(g_launches.load()); }
 
 msplat_status msplat_prune_mask(msplat_context* ctx, int dtype, int64_t n, const void* k, double threshold,
                                 int keep_small, uint8_t* keep, int64_t* kept) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx || !k || !keep) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "prune: null argument");
     CUDA_TRY(ctx->kept.ensure(8));
     CUDA_TRY(cudaMemsetAsync(ctx->kept.p, 0, 8, ctx->stream));
@@ -1324,6 +1373,7 @@ msplat_status msplat_prune_mask(msplat_context* ctx, int dtype, int64_t n, const
 }
 
 msplat_status msplat_replay_counters(msplat_replay* r, msplat_counters* out) {
+    REPLAY_DEVICE_GUARD(r);
     if (!r || !out || !r->valid) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "replay: no forward recorded");
     cudaStream_t st = r->ctx->stream;
     const int64_t tiles = int64_t(r->tiles_x) * r->tiles_y;
@@ -1345,6 +1395,7 @@ msplat_status msplat_replay_counters(msplat_replay* r, msplat_counters* out) {
 }
 
 msplat_status msplat_replay_bins(msplat_replay* r, int64_t* tile_offsets, int32_t* values, int64_t capacity) {
+    REPLAY_DEVICE_GUARD(r);
     if (!r || !r->valid) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "replay: no forward recorded");
     cudaStream_t st = r->ctx->stream;
     const int64_t tiles = int64_t(r->tiles_x) * r->tiles_y;
@@ -1369,6 +1420,7 @@ msplat_status msplat_replay_bins(msplat_replay* r, int64_t* tile_offsets, int32_
 
 msplat_status msplat_replay_splats(msplat_replay* r, uint8_t* visible, double* center, double* conic,
                                    double* sort_depth, double* radius, double* rgb, uint8_t* clamped) {
+    REPLAY_DEVICE_GUARD(r);
     if (!r || !r->valid) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "replay: no forward recorded");
     if (!(r->capture & 1) && (center || conic || sort_depth || radius || rgb))
         return set_error(MSPLAT_ERR_LOGIC, "replay: splat capture was not enabled (msplat_replay_set_capture)");
@@ -1391,6 +1443,7 @@ msplat_status msplat_replay_splats(msplat_replay* r, uint8_t* visible, double* c
 }
 
 msplat_status msplat_replay_terminus(msplat_replay* r, int32_t* terminus) {
+    REPLAY_DEVICE_GUARD(r);
     if (!r || !r->valid || !terminus) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "replay: no forward recorded");
     CUDA_TRY(cudaStreamSynchronize(r->ctx->stream));
     CUDA_TRY(cudaMemcpy(terminus, r->terminus.p, size_t(r->W) * r->H * 4, cudaMemcpyDeviceToHost));
@@ -1398,6 +1451,7 @@ msplat_status msplat_replay_terminus(msplat_replay* r, int32_t* terminus) {
 }
 
 msplat_status msplat_replay_weight_sums(msplat_replay* r, double* ws) {
+    REPLAY_DEVICE_GUARD(r);
     if (!r || !r->valid || !ws) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "replay: no forward recorded");
     if (!(r->capture & 2)) return set_error(MSPLAT_ERR_LOGIC, "replay: weight-sum capture was not enabled");
     CUDA_TRY(cudaStreamSynchronize(r->ctx->stream));
@@ -1416,6 +1470,7 @@ msplat_status msplat_replay_weight_sums(msplat_replay* r, double* ws) {
 msplat_status msplat_bin_and_sort_host(msplat_context* ctx, int64_t n, const uint8_t* visible, const double* center,
                                        const double* radius, const double* sort_depth, int width, int height,
                                        int64_t* tile_offsets, int32_t* values, int64_t capacity, int64_t* count) {
+    CTX_DEVICE_GUARD(ctx);
     if (!ctx || (n > 0 && (!visible || !center || !radius || !sort_depth)) || width < 1 || height < 1)
         return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "bin_and_sort: bad argument");
     msplat_replay r;

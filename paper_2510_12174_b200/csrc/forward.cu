@@ -400,11 +400,8 @@ template <typename Real>
 void launch_forward(const ForwardArgs<Real>& a, int ntiles, cudaStream_t s) {
     if (ntiles == 0) return;
     const size_t smem = forward_smem_bytes<Real>(a.C);
-    static bool configured = false;  // per instantiation
-    if (!configured) {
-        cudaFuncSetAttribute(forward_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        configured = true;
-    }
+    static std::atomic<unsigned long long> attr{0};  // per instantiation, per device
+    opt_in_smem(reinterpret_cast<const void*>(forward_kernel<Real>), attr);
     forward_kernel<Real><<<ntiles, kThreads, smem, s>>>(a);
     count_launches(1);
 }

@@ -3,6 +3,8 @@
 // optim.cu) and the C-ABI layer (cabi.cu).
 #pragma once
 
+#include <atomic>
+
 #include <string>
 
 #include <cuda_runtime.h>
@@ -16,6 +18,20 @@ namespace msplat_cuda {
 // Process-wide kernel launch counter (msplat_kernel_launches); every launch
 // site calls count_launches with the number of kernels it enqueued.
 void count_launches(int n);
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize belongs to the device context:
+// opt a kernel in once per (kernel, device id), thread-safely.  `done` is the
+// kernel's bitmask of configured devices (a function-local static).
+inline cudaError_t opt_in_smem(const void* fn, std::atomic<unsigned long long>& done, int bytes = 227 * 1024) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
 
 template <typename Real>
 struct PreprocessArgs {
@@ -238,6 +254,9 @@ struct BackwardArgs {
     // launch_work_order), and phase B takes segments in the same order.  Null:
     // warp w of CTA b replays block w of tile b.
     const uint32_t* work_order;
+    // FP32: semantic rows may be moved in 8-byte pieces (C even and both the
+    // scene's and the gradient buffer's semantic arrays 8-byte aligned).
+    int sem_vec;
     DeviceError* err;
 };
 template <typename Real>

@@ -384,11 +384,8 @@ void launch_preprocess(const PreprocessArgs<Real>& a, cudaStream_t s) {
     if (a.n == 0) return;
     const int64_t blocks = (a.n + kPreThreads - 1) / kPreThreads;
     const size_t smem = sizeof(Real) * size_t(kPreThreads) * 3 * a.K + kPreThreads;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(preprocess_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = true;
-    }
+    static std::atomic<unsigned long long> attr{0};  // per instantiation, per device
+    opt_in_smem(reinterpret_cast<const void*>(preprocess_kernel<Real>), attr, 200 * 1024);
     preprocess_kernel<Real><<<unsigned(blocks), kPreThreads, smem, s>>>(a);
     count_launches(1);
 }

@@ -326,6 +326,9 @@ class _Context:
     Lanes are independent contexts (own scratch and error word) so that
     renders on different streams of one device can run concurrently."""
     _per_device: dict[tuple, "_Context"] = {}
+    # Per-device settings every lane follows (also lanes created later):
+    # {device: {"deterministic": bool, "timing": bool}}
+    _settings: dict[int, dict] = {}
 
     def __init__(self, device: int):
         self.device = device
@@ -333,6 +336,11 @@ class _Context:
         check(_lib.lib().msplat_context_create(device, ct.c_void_p(torch.cuda.current_stream(device).cuda_stream),
                                                ct.byref(h)))
         self.h = h
+        st = self._settings.get(device, {})
+        if st.get("deterministic"):
+            check(_lib.lib().msplat_context_set_deterministic(h, 1))
+        if st.get("timing"):
+            check(_lib.lib().msplat_context_set_timing(h, 1))
 
     @classmethod
     def get(cls, device=None, lane: int = 0) -> "_Context":
@@ -342,6 +350,17 @@ class _Context:
             c = cls._per_device[(dev, lane)] = _Context(dev)
         check(_lib.lib().msplat_context_set_stream(c.h, ct.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
         return c
+
+    @classmethod
+    def apply(cls, device, key: str, value: bool, fn) -> None:
+        """Set a per-device flag on every existing lane and remember it for
+        lanes created later."""
+        dev = torch.cuda.current_device() if device is None else int(device)
+        cls.get(dev)
+        cls._settings.setdefault(dev, {})[key] = bool(value)
+        for (d, _lane), c in sorted(cls._per_device.items()):
+            if d == dev:
+                check(fn(c.h, int(value)))
 
 
 class ReplayState:
@@ -622,23 +641,35 @@ def check_device_errors(device=None):
 
 
 def set_stage_timing(enable: bool, device=None):
-    """Bracket every stage with CUDA events on the launching stream."""
-    check(_lib.lib().msplat_context_set_timing(_Context.get(device).h, int(enable)))
+    """Bracket every stage with CUDA events on the launching stream (every
+    context lane of the device)."""
+    _Context.apply(device, "timing", enable, _lib.lib().msplat_context_set_timing)
 
 
 def set_deterministic(enable: bool, device=None):
     """Bitwise-reproducible backward (TrainConfig::deterministic,
     msplat/trainer.hpp:48-63): per-(instance, warp) partial slots reduced in a
-    fixed order instead of float atomics.  Synchronizing, not graph-capturable."""
-    check(_lib.lib().msplat_context_set_deterministic(_Context.get(device).h, int(enable)))
+    fixed order instead of float atomics.  Applies to every context lane of
+    the device, including lanes created later."""
+    _Context.apply(device, "deterministic", enable, _lib.lib().msplat_context_set_deterministic)
 
 
 def stage_timings(device=None) -> dict:
-    """{stage: (device ms summed since the last call, launches of the stage)}; synchronizing."""
-    ms = (ct.c_double * 8)()
-    calls = (ct.c_int64 * 8)()
-    check(_lib.lib().msplat_context_timings(_Context.get(device).h, ms, calls))
-    return {name: (ms[i], int(calls[i])) for i, name in enumerate(_lib.STAGES)}
+    """{stage: (device ms summed since the last call, launches of the stage)},
+    summed over every context lane of the device; synchronizing."""
+    dev = torch.cuda.current_device() if device is None else int(device)
+    _Context.get(dev)
+    tot = {name: [0.0, 0] for name in _lib.STAGES}
+    for (d, _lane), c in sorted(_Context._per_device.items()):
+        if d != dev:
+            continue
+        ms = (ct.c_double * 8)()
+        calls = (ct.c_int64 * 8)()
+        check(_lib.lib().msplat_context_timings(c.h, ms, calls))
+        for i, name in enumerate(_lib.STAGES):
+            tot[name][0] += ms[i]
+            tot[name][1] += int(calls[i])
+    return {name: (v[0], v[1]) for name, v in tot.items()}
 
 
 def kernel_launches() -> int:
@@ -733,30 +764,39 @@ def accumulate_packed(dst: torch.Tensor, src: torch.Tensor) -> None:
 
 
 def prune(scene: Scene, state: OptimizerState, cfg: TrainConfig) -> int:
-    """prune (trainer.cpp:135-169): device mask, stable compaction of params and
-    moments, k reset.  Returns the number removed."""
+    """prune (trainer.cpp:135-169): device mask (msplat_prune_mask), then one
+    stable device compaction of the packed parameters and both Adam moments
+    with the k reset (msplat_prune_compact, trainer.cpp:150-168).  The scene's
+    tensors become views of the compacted packed buffer.  Returns the number
+    removed."""
     n = scene.size()
-    keep = torch.empty(n, dtype=torch.uint8, device=scene.means.device)
+    dev = scene.means.device
+    keep = torch.empty(n, dtype=torch.uint8, device=dev)
     kept = ct.c_int64()
-    ctx = _Context.get(scene.means.device.index)
-    check(_lib.lib().msplat_prune_mask(ctx.h, _dtype_code(scene.dtype), n, scene.k.data_ptr(),
-                                       float(cfg.prune_threshold), int(cfg.prune_keep_small),
-                                       keep.data_ptr(), ct.byref(kept)))
-    idx = keep.bool().nonzero().squeeze(1)
-    off = param_layout(n, scene.num_classes, scene.sh_degree)
-    m_views = [state.m[off[i]:off[i + 1]] for i in range(7)]
-    v_views = [state.v[off[i]:off[i + 1]] for i in range(7)]
-    fields = ["means", "quats", "log_scales", "opacity_logits", "k", "sh", "semantics"]
-    new_m, new_v = [], []
-    for i, name in enumerate(fields):
-        t = getattr(scene, name)
-        setattr(scene, name, t.index_select(0, idx).contiguous())
-        new_m.append(m_views[i].view(n, -1).index_select(0, idx).reshape(-1))
-        new_v.append(v_views[i].view(n, -1).index_select(0, idx).reshape(-1))
-    state.m = torch.cat(new_m)
-    state.v = torch.cat(new_v)
-    scene.k.fill_(cfg.k_reset)
-    return n - int(kept.value)
+    ctx = _Context.get(dev.index)
+    code = _dtype_code(scene.dtype)
+    check(_lib.lib().msplat_prune_mask(ctx.h, code, n, scene.k.data_ptr(), float(cfg.prune_threshold),
+                                       int(cfg.prune_keep_small), keep.data_ptr(), ct.byref(kept)))
+    k = int(kept.value)
+    C, deg = scene.num_classes, scene.sh_degree
+    P_in = param_layout(n, C, deg)[-1]
+    P_out = param_layout(k, C, deg)[-1]
+    params = pack_scene(scene)
+    if state.m.numel() != P_in or state.v.numel() != P_in:
+        raise ValueError("prune: optimizer state does not match the scene")
+    out = [torch.empty(P_out, dtype=scene.dtype, device=dev) for _ in range(3)]
+    ins = (ct.c_void_p * 3)(params.data_ptr(), state.m.data_ptr(), state.v.data_ptr())
+    outs = (ct.c_void_p * 3)(*(t.data_ptr() for t in out))
+    check(_lib.lib().msplat_prune_compact(ctx.h, code, n, C, deg, keep.data_ptr(), k, ins, outs,
+                                          float(cfg.k_reset)))
+    off = param_layout(k, C, deg)
+    shapes = {"means": (k, 3), "quats": (k, 4), "log_scales": (k, 3), "opacity_logits": (k,), "k": (k,),
+              "sh": tuple(scene.sh.shape[1:]), "semantics": (k, C)}
+    for i, name in enumerate(("means", "quats", "log_scales", "opacity_logits", "k", "sh", "semantics")):
+        shp = shapes[name] if name != "sh" else (k, *shapes["sh"])
+        setattr(scene, name, out[0][off[i]:off[i + 1]].view(shp))
+    state.m, state.v = out[1], out[2]
+    return n - k
 
 
 # --------------------------------------------------------------- binning
