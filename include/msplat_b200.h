@@ -270,6 +270,16 @@ MSPLAT_API msplat_status msplat_adam_step(msplat_context* ctx, int dtype, int64_
                                int sh_degree, void* params, const void* grads, void* m, void* v,
                                int64_t step, const double lr[7]);
 
+/* adam_step restricted to the packed elements [begin, begin + count) -- one
+ * rank's shard of a sharded optimizer step (reduce-scatter -> Adam on the
+ * shard -> all-gather; the reference's adam_step, core/src/trainer.cpp:98-133,
+ * is elementwise, so the shards together equal one full step bit for bit).
+ * params/grads/m/v address element `begin`; the learning rate of each element
+ * follows its global index.  count < 0 means "to the end". */
+MSPLAT_API msplat_status msplat_adam_step_range(msplat_context* ctx, int dtype, int64_t n, int num_classes,
+                                     int sh_degree, int64_t begin, int64_t count, void* params,
+                                     const void* grads, void* m, void* v, int64_t step, const double lr[7]);
+
 /* dst += src over count packed values (device pointers, stream-ordered).  The
  * gradient sum of a training step whose views were rendered on several
  * context lanes (train() accumulates every view into one Gradients,

@@ -122,6 +122,8 @@ def _sig(lib):
                                       P(MsplatGrads), ct.c_int, ct.c_int, _vp]),
         ("msplat_adam_step", ct.c_int, [_vp, ct.c_int, _i64, ct.c_int, ct.c_int, _vp, _vp, _vp, _vp,
                                         _i64, P(ct.c_double)]),
+        ("msplat_adam_step_range", ct.c_int, [_vp, ct.c_int, _i64, ct.c_int, ct.c_int, _i64, _i64, _vp, _vp,
+                                              _vp, _vp, _i64, P(ct.c_double)]),
         ("msplat_accumulate", ct.c_int, [_vp, ct.c_int, _i64, _vp, _vp]),
         ("msplat_prune_mask", ct.c_int, [_vp, ct.c_int, _i64, _vp, ct.c_double, ct.c_int, _vp,
                                          P(_i64)]),

@@ -1036,25 +1036,44 @@ msplat_status msplat_fwd_bwd(msplat_context* ctx, const msplat_scene* s, const m
     return st;
 }
 
-msplat_status msplat_adam_step(msplat_context* ctx, int dtype, int64_t n, int C, int deg, void* params,
-                               const void* grads, void* m, void* v, int64_t step, const double lr[7]) {
-    CTX_DEVICE_GUARD(ctx);
-    if (!ctx || !params || !grads || !m || !v || !lr) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "adam_step: null argument");
-    if (step < 1) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, "adam_step: step must be >= 1");
+static msplat_status adam_range_impl(msplat_context* ctx, int dtype, int64_t n, int C, int deg, int64_t begin,
+                                     int64_t count, void* params, const void* grads, void* m, void* v,
+                                     int64_t step, const double lr[7], const char* who) {
+    if (!ctx || !params || !grads || !m || !v || !lr)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, std::string(who) + ": null argument");
+    if (step < 1) return set_error(MSPLAT_ERR_INVALID_ARGUMENT, std::string(who) + ": step must be >= 1");
+    if (dtype != MSPLAT_F32 && dtype != MSPLAT_F64)
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, std::string(who) + ": dtype must be MSPLAT_F32 or MSPLAT_F64");
     int64_t off[8];
     msplat_status st = msplat_param_layout(n, C, deg, off);
     if (st != MSPLAT_OK) return st;
+    if (count < 0) count = off[7] - begin;
+    if (begin < 0 || begin > off[7] || count < 0 || begin + count > off[7])
+        return set_error(MSPLAT_ERR_INVALID_ARGUMENT, std::string(who) + ": range outside the packed buffer");
     const double bc1 = 1 - std::pow(0.9, double(step)), bc2 = 1 - std::pow(0.999, double(step));
     ctx->timer.begin(MSPLAT_STAGE_OPTIM, ctx->stream);
     if (dtype == MSPLAT_F64)
-        launch_adam<double>(off[7], off, lr, static_cast<double*>(params), static_cast<const double*>(grads),
+        launch_adam<double>(begin, count, off, lr, static_cast<double*>(params), static_cast<const double*>(grads),
                             static_cast<double*>(m), static_cast<double*>(v), bc1, bc2, ctx->stream);
     else
-        launch_adam<float>(off[7], off, lr, static_cast<float*>(params), static_cast<const float*>(grads),
+        launch_adam<float>(begin, count, off, lr, static_cast<float*>(params), static_cast<const float*>(grads),
                            static_cast<float*>(m), static_cast<float*>(v), bc1, bc2, ctx->stream);
     ctx->timer.end(ctx->stream);
     CUDA_TRY(cudaGetLastError());
     return MSPLAT_OK;
+}
+
+msplat_status msplat_adam_step(msplat_context* ctx, int dtype, int64_t n, int C, int deg, void* params,
+                               const void* grads, void* m, void* v, int64_t step, const double lr[7]) {
+    CTX_DEVICE_GUARD(ctx);
+    return adam_range_impl(ctx, dtype, n, C, deg, 0, -1, params, grads, m, v, step, lr, "adam_step");
+}
+
+msplat_status msplat_adam_step_range(msplat_context* ctx, int dtype, int64_t n, int C, int deg, int64_t begin,
+                                     int64_t count, void* params, const void* grads, void* m, void* v,
+                                     int64_t step, const double lr[7]) {
+    CTX_DEVICE_GUARD(ctx);
+    return adam_range_impl(ctx, dtype, n, C, deg, begin, count, params, grads, m, v, step, lr, "adam_step_range");
 }
 
 msplat_status msplat_accumulate(msplat_context* ctx, int dtype, int64_t count, void* dst, const void* src) {

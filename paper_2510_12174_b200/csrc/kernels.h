@@ -299,8 +299,10 @@ void launch_check_replay(int64_t n, const Real* means, const Real* k, const Real
                          const Real* saved_k, DeviceError* err, cudaStream_t s);
 
 // Optimizer (K11).
+// Elements [base, base + total) of the packed buffer; the pointers address
+// element `base` (a shard of a sharded optimizer step, or base = 0 for all).
 template <typename Real>
-void launch_adam(int64_t total, const int64_t* seg_starts /*host, 8*/, const double* lr /*7*/,
+void launch_adam(int64_t base, int64_t total, const int64_t* seg_starts /*host, 8*/, const double* lr /*7*/,
                  Real* params, const Real* grads, Real* m, Real* v, double bc1, double bc2,
                  cudaStream_t s);
 // dst += src over total packed values (multi-lane gradient sums).

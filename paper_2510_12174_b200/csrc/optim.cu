@@ -92,11 +92,11 @@ __global__ void prune_mask_kernel(int64_t n, const Real* __restrict__ k, double 
 }  // namespace
 
 template <typename Real>
-void launch_adam(int64_t total, const int64_t* seg_starts, const double* lr, Real* params, const Real* grads,
-                 Real* m, Real* v, double bc1, double bc2, cudaStream_t s) {
+void launch_adam(int64_t base, int64_t total, const int64_t* seg_starts, const double* lr, Real* params,
+                 const Real* grads, Real* m, Real* v, double bc1, double bc2, cudaStream_t s) {
     if (total == 0) return;
-    AdamSegments seg;
-    for (int i = 0; i < 8; ++i) seg.start[i] = seg_starts[i];
+    AdamSegments seg;  // segment starts relative to the first element handled
+    for (int i = 0; i < 8; ++i) seg.start[i] = seg_starts[i] - base;
     for (int i = 0; i < 7; ++i) seg.lr[i] = lr[i];
     const bool aligned = ((reinterpret_cast<uintptr_t>(params) | reinterpret_cast<uintptr_t>(grads) |
                            reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 15u) == 0;
@@ -114,10 +114,10 @@ void launch_prune_mask(int64_t n, const Real* k, double threshold, int keep_smal
     count_launches(1);
 }
 
-template void launch_adam<float>(int64_t, const int64_t*, const double*, float*, const float*, float*, float*,
-                                 double, double, cudaStream_t);
-template void launch_adam<double>(int64_t, const int64_t*, const double*, double*, const double*, double*,
-                                  double*, double, double, cudaStream_t);
+template void launch_adam<float>(int64_t, int64_t, const int64_t*, const double*, float*, const float*, float*,
+                                 float*, double, double, cudaStream_t);
+template void launch_adam<double>(int64_t, int64_t, const int64_t*, const double*, double*, const double*,
+                                  double*, double*, double, double, cudaStream_t);
 template void launch_prune_mask<float>(int64_t, const float*, double, int, uint8_t*, unsigned long long*,
                                        cudaStream_t);
 template void launch_prune_mask<double>(int64_t, const double*, double, int, uint8_t*, unsigned long long*,

@@ -425,14 +425,23 @@ class ReplayState:
 
 # ------------------------------------------------------------- hot path API
 def rasterize(scene: Scene, view: CameraView, cfg: RenderConfig | None = None,
-              replay: ReplayState | None = None) -> MultimodalFrame:
+              replay: ReplayState | None = None, out: MultimodalFrame | None = None) -> MultimodalFrame:
     """rasterize (rasterizer.cpp:87-205).  frame.normals stays zero until
-    estimate_normals, exactly like the reference (rasterizer.cpp:101)."""
+    estimate_normals, exactly like the reference (rasterizer.cpp:101).  `out`
+    reuses a caller-owned frame of the view's size (every channel is
+    overwritten; no allocation, so the call is CUDA-graph capturable once the
+    replay is sized)."""
     cfg = cfg or RenderConfig()
     ctx = _Context.get(scene.means.device.index, replay.lane if replay is not None else 0)
-    frame = MultimodalFrame.empty(view.width, view.height, scene.num_classes, scene.dtype,
-                                  scene.means.device)
-    frame.transmittance.fill_(1.0)
+    if out is None:
+        frame = MultimodalFrame.empty(view.width, view.height, scene.num_classes, scene.dtype,
+                                      scene.means.device)
+        frame.transmittance.fill_(1.0)
+    else:
+        if (out.width, out.height, out.num_classes) != (view.width, view.height, scene.num_classes) or \
+                out.color.dtype != scene.dtype:
+            raise ValueError("rasterize: output frame does not match the view / scene")
+        frame = out
     check(_lib.lib().msplat_rasterize(ctx.h, ct.byref(scene._abi()), ct.byref(view._abi()),
                                       ct.byref(cfg._abi()), ct.byref(frame._abi()),
                                       replay.h if replay is not None else None))
@@ -443,11 +452,12 @@ def rasterize(scene: Scene, view: CameraView, cfg: RenderConfig | None = None,
 
 
 def estimate_normals(depth: torch.Tensor, transmittance: torch.Tensor, view: CameraView,
-                     ncfg: NormalConfig, normals: torch.Tensor) -> None:
-    """estimate_normals (normals.cpp:28-101): writes unit normals [3, H, W]."""
+                     ncfg: NormalConfig, normals: torch.Tensor, lane: int = 0) -> None:
+    """estimate_normals (normals.cpp:28-101): writes unit normals [3, H, W]
+    (on context lane `lane`, torch's current stream)."""
     if depth.shape != (view.height, view.width) or transmittance.shape != depth.shape:
         raise ValueError("backproject: depth map does not match the view")
-    ctx = _Context.get(depth.device.index)
+    ctx = _Context.get(depth.device.index, lane)
     check(_lib.lib().msplat_estimate_normals(ctx.h, _dtype_code(depth.dtype), depth.data_ptr(),
                                              transmittance.data_ptr(), ct.byref(view._abi()),
                                              ct.byref(ncfg._abi()), normals.data_ptr()))
@@ -750,6 +760,30 @@ def adam_step(scene: Scene, grads: GradientBuffer, state: OptimizerState, cfg: T
                                       state.v.data_ptr(), state.step, lr))
     if packed_params is None:
         unpack_into_scene(p, scene)
+
+
+def adam_step_range(scene: Scene, grads: GradientBuffer, state: OptimizerState, cfg: TrainConfig,
+                    packed_params: torch.Tensor, packed_grads: torch.Tensor, begin: int, count: int) -> None:
+    """adam_step (trainer.cpp:98-133) on the packed elements [begin, begin+count)
+    only (msplat_adam_step_range): one rank's shard of a sharded optimizer step.
+    state.step is used as is (the caller advances it once per step); the packed
+    buffers and state.m / state.v are full length (n*P, or padded beyond)."""
+    if not grads.raw_space:
+        raise LogicError("adam_step: gradients not chained to raw parameters")
+    total = param_layout(scene.size(), scene.num_classes, scene.sh_degree)[-1]
+    if begin < 0 or count < 0 or begin + count > total:
+        raise ValueError("adam_step_range: range outside the packed buffer")
+    if min(packed_params.numel(), packed_grads.numel(), state.m.numel(), state.v.numel()) < total:
+        raise ValueError("adam_step_range: packed buffers shorter than n*P")
+    if state.step < 1:
+        raise ValueError("adam_step_range: state.step must be >= 1")
+    ctx = _Context.get(scene.means.device.index)
+    lr = (ct.c_double * 7)(*cfg.lrs_packed())
+    es = packed_params.element_size()
+    check(_lib.lib().msplat_adam_step_range(
+        ctx.h, _dtype_code(scene.dtype), scene.size(), scene.num_classes, scene.sh_degree, int(begin), int(count),
+        packed_params.data_ptr() + begin * es, packed_grads.data_ptr() + begin * es,
+        state.m.data_ptr() + begin * es, state.v.data_ptr() + begin * es, state.step, lr))
 
 
 def accumulate_packed(dst: torch.Tensor, src: torch.Tensor) -> None:

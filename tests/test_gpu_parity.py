@@ -251,31 +251,58 @@ def test_multilane_step_gradients_equal_sum_of_views(port, graph):
     frame = M.MultimodalFrame.empty(W, H, C, torch.float64, "cuda")
     step = ViewShardedStep(scene, flat, gflat, grads, M.OptimizerState(torch.zeros_like(flat), torch.zeros_like(flat), 0),
                            M.TrainConfig(), M.RenderConfig(), M.NormalConfig(), cams, pixs, frame, M.ReplayState(),
-                           lanes=2)
+                           lanes=2, optimizer=False)  # no Adam: the packed buffer keeps the chained gradients
     assert step.lanes == 2 and step.blocks == [[0, 1], [2, 3]]
-    # the step's Adam would move the scene: read the gradients in its place
-    import paper_2510_12174_b200.rasterizer as R
     seen = {}
-
-    def keep(scene_, grads_, *a, **k):
-        seen["g"] = gflat.clone()
-    R_adam = R.adam_step
-    R.adam_step = keep
-    try:
-        step()  # sizes the replays (eager)
-        if graph:
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            cap = torch.cuda.Stream()
-            cap.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.graph(g, stream=cap):
-                step()
-            g.replay()
+    step()  # sizes the replays (eager)
+    if graph:
         torch.cuda.synchronize()
-    finally:
-        R.adam_step = R_adam
+        gflat.zero_()
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(g, stream=cap):
+            step()
+        g.replay()
+    torch.cuda.synchronize()
+    seen["g"] = gflat.clone()
     from paper_2510_12174_b200.distributed import pack_grad_dict
     assert rel_l2_err(seen["g"].cpu().numpy(), pack_grad_dict(total)) < 1e-8
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_sharded_adam_ranges_equal_one_full_step(dtype):
+    """msplat_adam_step_range over the shards of a sharded optimizer step (the
+    ranks' [begin, begin+count) ranges, distributed.shard_range, and ranges
+    that start off the 16-byte vector grid) leaves exactly the bits of one
+    full adam_step (trainer.cpp:98-133) -- params and both moments."""
+    import torch
+    import paper_2510_12174_b200 as M
+    from paper_2510_12174_b200.distributed import shard_range
+    dt = torch.float64 if dtype == "float64" else torch.float32
+    n, C, deg = 3001, 5, 2
+    s = scenes.make_random_scene(n, num_classes=C, sh_degree=deg, seed=11)
+    scene = M.Scene.from_numpy(s, dtype=dt)
+    total = M.param_layout(n, C, deg)[-1]
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    g = torch.randn(total, generator=gen, device="cuda", dtype=dt)
+    m0 = torch.randn(total, generator=gen, device="cuda", dtype=dt) * 0.1
+    v0 = torch.rand(total, generator=gen, device="cuda", dtype=dt) * 0.01
+    grads = M.GradientBuffer.from_packed(g.clone(), n, C, deg)
+    grads.raw_space = True
+    tc = M.TrainConfig()
+    p_full = M.pack_scene(scene)
+    st_full = M.OptimizerState(m0.clone(), v0.clone(), 4)
+    M.adam_step(scene, grads, st_full, tc, packed_params=p_full, packed_grads=g)  # step 5
+    for ranges in ([shard_range(total, r, 3) for r in range(3)], [(0, 7), (7, 1234), (1241, total - 1241)]):
+        p = M.pack_scene(scene)
+        st = M.OptimizerState(m0.clone(), v0.clone(), 5)
+        for b, c in ranges:
+            M.rasterizer.adam_step_range(scene, grads, st, tc, p, g, b, c)
+        torch.cuda.synchronize()
+        assert torch.equal(p, p_full) and torch.equal(st.m, st_full.m) and torch.equal(st.v, st_full.v)
+    with pytest.raises(ValueError):
+        M.rasterizer.adam_step_range(scene, grads, st, tc, p, g, total - 3, 4)
 
 
 def test_bin_and_sort_reference_kat():
