@@ -455,8 +455,7 @@ def run_ours(args, rank, world, local_rank):
     reps, clk = _time_steps(run, args.steps, max(1, args.repeats), dev, world, clocks_for=True)
     launches = R.kernel_launches() - launches0  # 0 under graph replay (no host launches)
     if stage_graph is not None:  # per-stage brackets from a single-lane replay, after the timed region
-        R.stage_timings(local_rank)  # drop the brackets of earlier replays
-        stage_graph.replay()
+        stage_graph.replay()  # its event-record nodes are the only brackets held
         torch.cuda.synchronize(dev)
     stage = R.stage_timings(local_rank)
     R.set_stage_timing(False, local_rank)

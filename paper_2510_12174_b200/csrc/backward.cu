@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kK10Threads, K10_MINB) projection_backward_ker
     const int64_t i = i0 + threadIdx.x;
     bool ok = true;
     if (i < a.n) ok = projection_backward_one<Real>(a, i, s_sh + threadIdx.x * RK, s_gsh + threadIdx.x * RK);
-    if (!ok) raise_error(a.err, kErrNonFiniteGrad, 0, i);
+    if (!ok) raise_error_ordered(a.err, kErrNonFiniteGrad, i);
     __syncthreads();
     // write the SH gradient back; finiteness of the SH and semantic rows
     int bad = -1;
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kK10Threads, K10_MINB) projection_backward_ker
         for (int e = threadIdx.x; e < nb * a.C; e += kK10Threads)
             if (!isfinite(gsem[e]) && bad < 0) bad = e / a.C;
     }
-    if (bad >= 0) raise_error(a.err, kErrNonFiniteGrad, 0, i0 + bad);
+    if (bad >= 0) raise_error_ordered(a.err, kErrNonFiniteGrad, i0 + bad);
 }
 
 
@@ -295,7 +295,7 @@ __global__ void check_replay_kernel(int64_t n, const Real* __restrict__ means, c
     if (i >= n) return;
     bool same = k[i] == saved_k[i];
     for (int j = 0; j < 3; ++j) same &= means[3 * i + j] == saved_means[3 * i + j];
-    if (!same) raise_error(err, kErrSceneModified, 0, i);
+    if (!same) raise_error_ordered(err, kErrSceneModified, i);
 }
 
 template <typename Real>

@@ -252,9 +252,10 @@ __device__ __forceinline__ void flush_pairs(const BackwardArgs<Real>& a, const Q
     for (int i = 0; i < 16; ++i) v[i] = seg_sum<Real>(v[i], same);
     if (head) {
         if constexpr (DET) {
+            if (int64_t(inst) < a.pair_cap)  // else capacity exceeded (zero_det_slots raised it)
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-                if (v[i] != Real(0)) slot[i] += v[i];
+                for (int i = 0; i < 16; ++i)
+                    if (v[i] != Real(0)) slot[i] += v[i];
         } else {
             Real* const row = a.acc16 + size_t(g) * 16;
             if constexpr (sizeof(Real) == 4) {
@@ -480,10 +481,12 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const __grid_cons
                     acc1 += wr.w * warp_seed[wr.soff + c1];
                 }
                 if constexpr (DET) {  // fields 16 + ch: dcolor, dk, dsem
+                    // (beyond the slot capacity: zero_det_slots raised it; nothing is written)
+                    const bool in_cap = int64_t(list0 + ws->pos[slot]) < a.pair_cap;
                     Real* const ps = a.partial + (size_t(list0 + ws->pos[slot]) * 8 + warp) * a.V + 16;
-                    if (lane < S && acc0 != Real(0)) ps[lane] += acc0;
-                    if (lane + 32 < S && acc1 != Real(0)) ps[lane + 32] += acc1;
-                    for (int ch = lane + 64; ch < S; ch += 32) {
+                    if (in_cap && lane < S && acc0 != Real(0)) ps[lane] += acc0;
+                    if (in_cap && lane + 32 < S && acc1 != Real(0)) ps[lane + 32] += acc1;
+                    for (int ch = lane + 64; in_cap && ch < S; ch += 32) {
                         Real s = Real(0);
                         for (int e = qn; e < qn + npairs; ++e) s += Q.ws[e].w * warp_seed[Q.ws[e].soff + ch];
                         if (s != Real(0)) ps[ch] += s;
@@ -661,6 +664,19 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
     }
     // rasterize_backward.cpp:156-171: nothing to do without blends or seeds.
     if (!(inside && term > 0 && any)) term = 0;
+    // Non-finite seeds (an error path): check_finite (scene.cpp:97-106) then
+    // names the lowest primitive blending at such a pixel.  They are zeroed
+    // for the tensor-core products (0 * inf in another event's column would
+    // spread NaN to primitives that never touch the pixel) and every primitive
+    // the forward blended at such a pixel is reported (a pass over the event
+    // log, off the hot loop), so the named primitive is the reference's.
+    bool bad = !isfinite(dD);
+    for (int ch = 0; ch < S; ++ch) bad |= !isfinite(my_seed[ch]);
+    if (bad) {
+        for (int ch = 0; ch < sp; ++ch) my_seed[ch] = 0.f;
+        dD = 0.f;
+    }
+    const unsigned bad_mask = __ballot_sync(0xffffffffu, bad && term > 0);
     const size_t seg = size_t(seg_i);  // this warp's pair-record segment
     const unsigned act_mask = __ballot_sync(0xffffffffu, term > 0);
     if (act_mask == 0) {
@@ -682,6 +698,12 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
     const uint32_t nev = a.ev_count[seg];
     const uint2* const evl = a.ev_list + size_t(8) * list0 + size_t(wl) * (range.y - list0);
     const int mtiles2 = (S + 15) / 16;  // GEMM2 channel tiles
+    if (bad_mask) {  // error path only (warp-uniform)
+        for (int e = lane; e < int(nev); e += 32) {
+            const uint2 ev = evl[e];
+            if (ev.y & bad_mask) raise_error_ordered(a.err, kErrNonFiniteGrad, a.inst_gauss[list0 + ev.x]);
+        }
+    }
     int qn = 0;
     const int64_t pbase = a.pair_off[seg];
     const int64_t pcap = a.pair_cap - pbase;  // records this segment may hold
@@ -1024,6 +1046,19 @@ __global__ void det_reduce_kernel(const __grid_constant__ BackwardArgs<Real> a, 
     }
 }
 
+template <typename Real>
+__global__ void zero_det_slots_kernel(Real* __restrict__ partial, const int64_t* __restrict__ d_count, int64_t cap,
+                                      int per_item, DeviceError* err) {
+    const int64_t count = *d_count;
+    if (count > cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) raise_error(err, kErrPairOverflow, count, cap);
+        return;
+    }
+    const int64_t total = count * per_item;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x)
+        partial[i] = Real(0);
+}
+
 int bits_for_ids(int64_t v) {
     int b = 1;
     while ((int64_t(1) << b) < v) ++b;
@@ -1048,6 +1083,15 @@ void launch_deterministic_reduce(const BackwardArgs<Real>& a, const DetScratch& 
     det_reduce_kernel<Real><<<unsigned((a.n * 32 + 255) / 256), 256, 0, s>>>(a, d.gid_range, inst_of);
     count_launches(3);
 }
+
+template <typename Real>
+void launch_zero_det_slots(Real* partial, const int64_t* d_count, int64_t cap, int per_item, DeviceError* err,
+                           cudaStream_t s) {
+    zero_det_slots_kernel<Real><<<unsigned(device_sm_count() * 8), 256, 0, s>>>(partial, d_count, cap, per_item, err);
+    count_launches(1);
+}
+template void launch_zero_det_slots<float>(float*, const int64_t*, int64_t, int, DeviceError*, cudaStream_t);
+template void launch_zero_det_slots<double>(double*, const int64_t*, int64_t, int, DeviceError*, cudaStream_t);
 
 template void launch_deterministic_reduce<float>(const BackwardArgs<float>&, const DetScratch&, const int64_t*,
                                                  int64_t, cudaStream_t);

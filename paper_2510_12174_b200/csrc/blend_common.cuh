@@ -121,9 +121,9 @@ struct RawParams {
 // decisions match the FP64 oracle.  Not inlined: it runs for a tiny fraction
 // of blended pairs (grazing rays).
 template <typename Real>
-__device__ __noinline__ bool intersect_fp64(const Cam& c, const RawParams<Real>& rp, uint32_t g, Real px,
-                                            Real py, double* t_out, double* a_out, double* b_out,
-                                            double* ds_out, double* depth_out) {
+__device__ __forceinline__ bool intersect_fp64_impl(const Cam& c, const RawParams<Real>& rp, uint32_t g, Real px,
+                                                    Real py, double* t_out, double* a_out, double* b_out,
+                                                    double* ds_out, double* depth_out) {
     const double pd[3] = {(double(px) - c.cx) / c.fx, (double(py) - c.cy) / c.fy, 1.0};
     double d[3];
     for (int i = 0; i < 3; ++i) {
@@ -199,10 +199,25 @@ __device__ __noinline__ bool intersect_fp64(const Cam& c, const RawParams<Real>&
     return true;
 }
 
+template <typename Real>
+__device__ __noinline__ bool intersect_fp64(const Cam& c, const RawParams<Real>& rp, uint32_t g, Real px,
+                                            Real py, double* t_out, double* a_out, double* b_out,
+                                            double* ds_out, double* depth_out) {
+    return intersect_fp64_impl<Real>(c, rp, g, px, py, t_out, a_out, b_out, ds_out, depth_out);
+}
+
+// How the FP32 intersect re-decides a near-boundary pair in FP64.
+enum : int {
+    kFp64Undecided = 0,  // not at all: hit = false, depth_fp64 = -2 ("undecided"); the caller re-runs the pair
+    kFp64Call = 1,       // a call to the out-of-line intersect_fp64
+    kFp64Inline = 2,     // inlined (callers with many live registers: no call-site spills)
+};
+
 // intersect (core/src/geometry.cpp:37-64) with the per-view constant v_s and
 // |v_s|^2 - 1 precomputed by K1.  In FP32, a discriminant or t_mid within a
-// relative 1e-4 of zero is re-decided in FP64 (intersect_fp64).
-template <typename Real>
+// relative 1e-4 of zero is re-decided in FP64 (intersect_fp64), as kFp64
+// selects.
+template <typename Real, int kFp64 = kFp64Call>
 __device__ __forceinline__ HitEval<Real> intersect(const BlendRec<Real>& g, const PixelRay<Real>& r,
                                                    const Cam& cam, const RawParams<Real>& rp, uint32_t gid) {
     HitEval<Real> h;
@@ -245,8 +260,17 @@ __device__ __forceinline__ HitEval<Real> intersect(const BlendRec<Real>& g, cons
         // Decisions within FP32 noise of the boundary are re-taken in FP64 exactly
         // as the reference computes them (rare: grazing rays / camera on the shell).
         if (fabsf(disc4) <= Real(1e-4) * h.a || fabsf(vd) <= Real(1e-4) * sqrtf(h.a * (g.csq + Real(1)))) {
+            if constexpr (kFp64 == kFp64Undecided) {
+                h.depth_fp64 = Real(-2);
+                return h;
+            }
             double t, a, b, ds[3], dep;
-            if (!intersect_fp64<Real>(cam, rp, gid, r.px, r.py, &t, &a, &b, ds, &dep)) return h;
+            bool ok;
+            if constexpr (kFp64 == kFp64Inline)
+                ok = intersect_fp64_impl<Real>(cam, rp, gid, r.px, r.py, &t, &a, &b, ds, &dep);
+            else
+                ok = intersect_fp64<Real>(cam, rp, gid, r.px, r.py, &t, &a, &b, ds, &dep);
+            if (!ok) return h;
             h.hit = true;
             h.t_mid = Real(t);
             h.a = Real(a);

@@ -135,9 +135,13 @@ struct StageTimer {
             if (calls) calls[i] = 0;
         }
         for (const Mark& m : marks) {
-            cudaEventSynchronize(m.b);
+            // A bracket captured into a graph that was never replayed has no
+            // timestamps: skip it (and clear the non-sticky error it raises).
             float t = 0;
-            cudaEventElapsedTime(&t, m.a, m.b);
+            if (cudaEventSynchronize(m.b) != cudaSuccess || cudaEventElapsedTime(&t, m.a, m.b) != cudaSuccess) {
+                (void)cudaGetLastError();
+                continue;
+            }
             ms[m.stage] += t;
             if (calls) calls[m.stage] += 1;
         }
@@ -172,6 +176,7 @@ struct msplat_context {
     // deterministic backward (msplat_context_set_deterministic)
     int deterministic = 0;
     DevBuf det_partial, det_keys, det_keys_alt, det_vals, det_vals_alt, det_range;
+    int64_t det_cap = 0;  // instances the deterministic slots hold (grown by eager calls)
     StageTimer timer;
 };
 
@@ -190,7 +195,7 @@ struct msplat_replay {
         count_sorted, offset_sorted, inst_tile, inst_tile_alt, inst_gauss, inst_gauss_alt, tile_range,
         d_inst_count, d_inst_total32, hist, hist_scanned, scan_tiles, terminus, weight_sums, saved_means,
         saved_k, cap_center, cap_conic, cap_depth, cap_radius, cap_rgb, visible_count, ev_list, ev_count, ev_npairs,
-        pair_off, pair_n, pair_scan, pair_total, pair_rec, wq_order, wq_scratch;
+        pair_off, pair_n, pair_scan, pair_total, pair_rec, wq_order, wq_scratch, ev_w;
     int64_t pair_cap = 0;  // pair-record capacity of the FP32 split backward
     uint32_t* sorted_gauss = nullptr;
 
@@ -200,8 +205,8 @@ struct msplat_replay {
                           &inst_gauss, &inst_gauss_alt, &tile_range, &d_inst_count, &d_inst_total32, &hist,
                           &hist_scanned, &scan_tiles, &terminus, &weight_sums, &saved_means, &saved_k,
                           &cap_center, &cap_conic, &cap_depth, &cap_radius, &cap_rgb, &visible_count, &ev_list,
-                          &ev_count, &ev_npairs, &pair_off, &pair_n, &pair_scan, &pair_total, &pair_rec, &wq_order,
-                          &wq_scratch})
+                          &ev_count, &ev_npairs, &pair_off, &pair_n, &pair_scan, &pair_total, &pair_rec,
+                          &wq_order, &wq_scratch, &ev_w})
             b->release();
     }
 };
@@ -278,8 +283,9 @@ msplat_status check_scene(const msplat_scene* s) {
 msplat_status drain_device_error(msplat_context* ctx, int W) {
     CUDA_TRY(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(DeviceError), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    const DeviceError e = *ctx->h_err;
+    DeviceError e = *ctx->h_err;
     if (e.code == kErrNone) return MSPLAT_OK;
+    if (e.min_b != 0) e.b = static_cast<long long>(~e.min_b);  // raise_error_ordered: lowest primitive
     CUDA_TRY(cudaMemsetAsync(ctx->d_err, 0, sizeof(DeviceError), ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     char buf[256];
@@ -352,6 +358,7 @@ msplat_status size_replay(msplat_replay* r, int dtype, int64_t n, int C, int deg
     CUDA_TRY(r->inst_tile.ensure(ic * 4));
     CUDA_TRY(r->inst_tile_alt.ensure(ic * 4));
     CUDA_TRY(r->ev_list.ensure(ic * 8 * sizeof(uint2)));  // 8 warps x (position, mask) per instance
+
     CUDA_TRY(r->ev_count.ensure(size_t(tiles) * 8 * 4));
     CUDA_TRY(r->ev_npairs.ensure(size_t(tiles) * 8 * 4));
     CUDA_TRY(r->wq_order.ensure(size_t(tiles) * 8 * 4));
@@ -424,7 +431,16 @@ msplat_status binning_with_capacity(msplat_replay* r, bool sync) {
         CUDA_TRY(cudaMemcpyAsync(ctx->h_u64, b.d_inst_total32, 4, cudaMemcpyDeviceToHost, ctx->stream));
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         const int64_t need = int64_t(*reinterpret_cast<uint32_t*>(ctx->h_u64));
-        if (need <= r->inst_cap) return MSPLAT_OK;
+        if (need <= r->inst_cap) {
+            // split FP32 forward: <= 32 compacted blend weights per event-log
+            // entry (8 per instance), sized from this render's instances (a
+            // captured replay keeps the capacity; K6a checks it)
+            if (r->dtype != MSPLAT_F64 && forward_split_supported(r->C)) {
+                const size_t want = size_t(need + need / 4 + 1024) * 8 * 32 * sizeof(float);
+                if (r->ev_w.bytes < size_t(need) * 8 * 32 * sizeof(float)) CUDA_TRY(r->ev_w.ensure(want));
+            }
+            return MSPLAT_OK;
+        }
         // clear the latched overflow, grow, retry
         CUDA_TRY(cudaMemsetAsync(ctx->d_err, 0, sizeof(DeviceError), ctx->stream));
         r->inst_cap = need + need / 4 + 1024;
@@ -520,7 +536,19 @@ msplat_status rasterize_impl(msplat_context* ctx, const msplat_scene* s, const m
     a.ev_npairs = r->ev_npairs.as<uint32_t>();
     a.err = ctx->d_err;
     ctx->timer.begin(MSPLAT_STAGE_FORWARD, ctx->stream);
-    launch_forward<Real>(a, r->tiles_x * r->tiles_y, ctx->stream);
+    if constexpr (sizeof(Real) == 4) {
+        if (forward_split_supported(a.C) && r->ev_w.p) {
+            a.ev_w = r->ev_w.as<float>();
+            a.ev_w_cap = int64_t(r->ev_w.bytes / sizeof(float));
+            a.sem_vec = (a.C % 2 == 0) && (reinterpret_cast<uintptr_t>(s->semantics) % 8 == 0);
+            launch_forward_split(a, r->tiles_x * r->tiles_y, ctx->stream,
+                                 dynamic_schedule() ? r->wq_order.as<uint32_t>() : nullptr, r->wq_scratch.as<uint32_t>());
+        } else {
+            launch_forward<Real>(a, r->tiles_x * r->tiles_y, ctx->stream);
+        }
+    } else {
+        launch_forward<Real>(a, r->tiles_x * r->tiles_y, ctx->stream);
+    }
     ctx->timer.end(ctx->stream);
     CUDA_TRY(cudaGetLastError());
     r->valid = true;
@@ -610,20 +638,34 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
     int64_t det_count = 0;
     DetScratch det{};
     if (ctx->deterministic) {
-        // Synchronizing: the partial slots are sized by this render's instance count.
-        CUDA_TRY(cudaMemcpyAsync(ctx->h_u64, r->d_inst_count.p, 8, cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaStreamSynchronize(st));
-        det_count = int64_t(*ctx->h_u64);
-        const size_t dc = size_t(std::max<int64_t>(det_count, 1));
+        // The partial slots are sized by a CAPACITY of instances, grown whenever
+        // the stream is not being captured (one synchronizing read of the
+        // instance count), so the deterministic backward is graph-capturable;
+        // the kernels bound themselves by the device-side count.
         a.V = 20 + C;
-        CUDA_TRY(ctx->det_partial.ensure(dc * 8 * size_t(a.V) * R));
-        CUDA_TRY(cudaMemsetAsync(ctx->det_partial.p, 0, dc * 8 * size_t(a.V) * R, st));
-        CUDA_TRY(ctx->det_keys.ensure(dc * 4));
-        CUDA_TRY(ctx->det_keys_alt.ensure(dc * 4));
-        CUDA_TRY(ctx->det_vals.ensure(dc * 4));
-        CUDA_TRY(ctx->det_vals_alt.ensure(dc * 4));
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        CUDA_TRY(cudaStreamIsCapturing(st, &cs));
+        if (cs == cudaStreamCaptureStatusNone) {
+            CUDA_TRY(cudaMemcpyAsync(ctx->h_u64, r->d_inst_count.p, 8, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            const int64_t need = int64_t(*ctx->h_u64);
+            if (need > ctx->det_cap || size_t(ctx->det_cap) * 8 * size_t(a.V) * R > ctx->det_partial.bytes) {
+                const int64_t cap = std::max<int64_t>(need + need / 4 + 4096, ctx->det_cap);
+                CUDA_TRY(ctx->det_partial.ensure(size_t(cap) * 8 * size_t(a.V) * R));
+                CUDA_TRY(ctx->det_keys.ensure(size_t(cap) * 4));
+                CUDA_TRY(ctx->det_keys_alt.ensure(size_t(cap) * 4));
+                CUDA_TRY(ctx->det_vals.ensure(size_t(cap) * 4));
+                CUDA_TRY(ctx->det_vals_alt.ensure(size_t(cap) * 4));
+                ctx->det_cap = cap;
+            }
+        }
+        if (ctx->det_cap == 0)
+            return set_error(MSPLAT_ERR_RUNTIME, "rasterize_backward: deterministic capture before any eager call");
+        det_count = std::min<int64_t>(ctx->det_cap, r->inst_cap);
         CUDA_TRY(ctx->det_range.ensure(nn * 8));
         a.partial = ctx->det_partial.as<Real>();
+        a.pair_cap = ctx->det_cap;  // slot capacity (instances)
+        launch_zero_det_slots<Real>(a.partial, r->d_inst_count.as<int64_t>(), ctx->det_cap, 8 * a.V, ctx->d_err, st);
         // the replay's radix scratch is sized for inst_cap >= det_count items
         det = DetScratch{ctx->det_keys.as<uint32_t>(), ctx->det_keys_alt.as<uint32_t>(),
                          ctx->det_vals.as<uint32_t>(), ctx->det_vals_alt.as<uint32_t>(),

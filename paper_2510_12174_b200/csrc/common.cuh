@@ -35,6 +35,7 @@ struct DeviceError {
     int pad;
     long long a;
     long long b;
+    unsigned long long min_b;  // ~(lowest primitive) of an ordered error (raise_error_ordered), 0 = unset
 };
 
 __device__ __forceinline__ void raise_error(DeviceError* e, int code, long long a, long long b) {
@@ -42,6 +43,16 @@ __device__ __forceinline__ void raise_error(DeviceError* e, int code, long long 
         e->a = a;
         e->b = b;
     }
+}
+
+// Errors the reference raises from a sequential scan over primitives
+// (Scene::validate scene.cpp:22-40, activate :43-51, check_finite :97-106,
+// rasterize_backward's modification check rasterizer_backward.cpp:40-44)
+// report the LOWEST offending primitive, whichever thread faults first.
+__device__ __forceinline__ void raise_error_ordered(DeviceError* e, int code, long long b) {
+    const int old = atomicCAS(&e->code, 0, code);
+    if (old != 0 && old != code) return;
+    atomicMax(&e->min_b, ~static_cast<unsigned long long>(b));
 }
 
 // Camera with the derived world->cam pose, both in double (CameraView).

@@ -38,6 +38,9 @@ constexpr int kThreads = 256;
 #define K6_NEXT_PREFETCH 1  // next chunk ids one chunk ahead + L1 prefetch of their records: 2.05 ms vs 2.11
 #endif
 constexpr int kQueue = 64;
+#ifndef K6_SPLIT_MINB
+#define K6_SPLIT_MINB 3  // CTAs per SM of the semantics-free variant
+#endif
 
 __host__ __device__ inline int sem_pitch(int C) { return C | 1; }  // odd pitch: conflict-free rows
 
@@ -162,11 +165,15 @@ __device__ __forceinline__ void flush_depth(const ForwardArgs<Real>& a, FwdWarpS
 
 }  // namespace
 
-template <typename Real>
-__global__ void __launch_bounds__(kThreads, 2) forward_kernel(const __grid_constant__ ForwardArgs<Real> a) {
+// kSplit (FP32): semantics are left to the separate tensor-core pass
+// (forward_split.cu, K6b), which replays the event log with the blend weights
+// this kernel writes (one 32-float row per event); nothing semantic is live
+// here.
+template <typename Real, bool kSplit>
+__global__ void __launch_bounds__(kThreads, kSplit ? K6_SPLIT_MINB : 2) forward_kernel(const __grid_constant__ ForwardArgs<Real> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int C = a.C, pitch = sem_pitch(C);
+    const int C = kSplit ? 0 : a.C, pitch = sem_pitch(C);
     constexpr bool kTC = sizeof(Real) == 4;  // tensor-core semantic accumulation (FP32)
     FwdWarpSmem<Real>* ws = reinterpret_cast<FwdWarpSmem<Real>*>(smem_raw) + warp;
     unsigned char* const sem_base = reinterpret_cast<unsigned char*>(reinterpret_cast<FwdWarpSmem<Real>*>(smem_raw) + 8);
@@ -207,6 +214,7 @@ __global__ void __launch_bounds__(kThreads, 2) forward_kernel(const __grid_const
     int qn = 0;
     unsigned long long own = 0;  // queue entries owned by this pixel
     uint2* const evl = a.ev_list ? a.ev_list + size_t(8) * range.x + size_t(warp) * len : nullptr;
+    float* const wd = kSplit ? a.ev_w + (size_t(8) * range.x + size_t(warp) * len) * 32 : nullptr;
     uint32_t n_ev = 0, n_pairs = 0;
 
 #if K6_NEXT_PREFETCH
@@ -249,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, 2) forward_kernel(const __grid_const
             if (mask == 0) continue;
             if (evl) {  // the backward replays exactly these events
                 if (lane == 0) evl[n_ev] = make_uint2(uint32_t(c * 32 + slot), mask);
+                if constexpr (kSplit) wd[size_t(n_ev) * 32 + lane] = ae.pass ? ae.alpha * T : Real(0);
                 ++n_ev;
                 n_pairs += __popc(mask);
             }
@@ -401,8 +410,17 @@ void launch_forward(const ForwardArgs<Real>& a, int ntiles, cudaStream_t s) {
     if (ntiles == 0) return;
     const size_t smem = forward_smem_bytes<Real>(a.C);
     static std::atomic<unsigned long long> attr{0};  // per instantiation, per device
-    opt_in_smem(reinterpret_cast<const void*>(forward_kernel<Real>), attr);
-    forward_kernel<Real><<<ntiles, kThreads, smem, s>>>(a);
+    opt_in_smem(reinterpret_cast<const void*>(forward_kernel<Real, false>), attr);
+    forward_kernel<Real, false><<<ntiles, kThreads, smem, s>>>(a);
+    count_launches(1);
+}
+
+void launch_forward_blend_split(const ForwardArgs<float>& a, int ntiles, cudaStream_t s) {
+    if (ntiles == 0) return;
+    const size_t smem = forward_smem_bytes<float>(0);
+    static std::atomic<unsigned long long> attr{0};
+    opt_in_smem(reinterpret_cast<const void*>(forward_kernel<float, true>), attr);
+    forward_kernel<float, true><<<ntiles, kThreads, smem, s>>>(a);
     count_launches(1);
 }
 

@@ -33,6 +33,19 @@ inline cudaError_t opt_in_smem(const void* fn, std::atomic<unsigned long long>& 
     return e;
 }
 
+// SM count of the current device (cached per device id; persistent-grid sizing).
+inline int device_sm_count() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    int v = cache[dev & 63].load(std::memory_order_relaxed);
+    if (v == 0) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        cache[dev & 63].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+
 template <typename Real>
 struct PreprocessArgs {
     int64_t n;
@@ -119,10 +132,25 @@ struct ForwardArgs {
     uint2* ev_list;
     uint32_t* ev_count;
     uint32_t* ev_npairs;  // blended pairs per (tile, warp): the backward's pair-record segments
+    // FP32 split forward (forward_split.cu): per event one row of 32 blend
+    // weights (0 for lanes that did not blend), in the region [32 (8 range.x +
+    // warp len), + 32 len) -- the event log's region scaled by 32 -- and the
+    // optional longest-first segment order of its per-pair kernel.
+    float* ev_w;
+    int64_t ev_w_cap;  // floats
+    int sem_vec;       // semantic rows may be staged in 8-byte pieces (C even, 8-byte aligned)
+    const uint32_t* work_order;
     DeviceError* err;
 };
 template <typename Real>
 void launch_forward(const ForwardArgs<Real>& a, int ntiles, cudaStream_t s);
+// The fused blend without semantics (colour, k, depth, T, the event log and
+// the weight rows), for the split FP32 forward.
+void launch_forward_blend_split(const ForwardArgs<float>& a, int ntiles, cudaStream_t s);
+// The split FP32 forward (blend pass + tensor-core semantic pass) handles C <= 64.
+bool forward_split_supported(int C);
+void launch_forward_split(const ForwardArgs<float>& a, int ntiles, cudaStream_t s, const uint32_t* seg_order,
+                          uint32_t* order_scratch);
 
 // Longest-first order of the nseg = 8 * tiles (tile, warp) segments for the
 // FP32 backward, cost = seg_cost[i] (the forward's per-warp event counts):
@@ -270,6 +298,11 @@ struct DetScratch {
     uint2* gid_range;                             // [n]
     uint32_t *hist, *hist_scanned, *scan_tiles;   // radix-sort scratch for count items
 };
+// Zeroes the first (*d_count) x per_item slots of the deterministic partial
+// buffer (capacity cap items); raises kErrPairOverflow when *d_count > cap.
+template <typename Real>
+void launch_zero_det_slots(Real* partial, const int64_t* d_count, int64_t cap, int per_item, DeviceError* err,
+                           cudaStream_t s);
 template <typename Real>
 void launch_deterministic_reduce(const BackwardArgs<Real>& a, const DetScratch& d, const int64_t* d_count,
                                  int64_t count, cudaStream_t s);

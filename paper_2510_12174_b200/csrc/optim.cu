@@ -21,14 +21,23 @@ struct AdamSegments {
     double lr[7];
 };
 
+// Every operation is explicitly rounded (no FMA contraction), so the vector
+// loop, the scalar tail and any sharded sub-range give the same bits for an
+// element (sharded Adam == replicated Adam), and FP64 follows the reference's
+// -ffp-contract=off evaluation (trainer.cpp:90-94, 109-131).
 template <typename Real>
 __device__ __forceinline__ Real adam_one(Real p, Real gr, Real& m, Real& v, Real lr, double bc1, double bc2) {
-    m = Real(0.9) * m + (Real(1) - Real(0.9)) * gr;
-    v = Real(0.999) * v + (Real(1) - Real(0.999)) * gr * gr;
-    if constexpr (sizeof(Real) == 8)  // the reference's operation order (trainer.cpp:120-127)
-        return p - lr * (m / bc1) / (sqrt(v / bc2) + 1e-15);
-    else  // FP32: reciprocals of the bias corrections, one IEEE divide
-        return p - lr * (m * float(1.0 / bc1)) / (sqrtf(v * float(1.0 / bc2)) + 1e-15f);
+    if constexpr (sizeof(Real) == 8) {
+        m = __dadd_rn(__dmul_rn(0.9, m), __dmul_rn(1.0 - 0.9, gr));
+        v = __dadd_rn(__dmul_rn(0.999, v), __dmul_rn(__dmul_rn(1.0 - 0.999, gr), gr));
+        const double num = __dmul_rn(lr, __ddiv_rn(m, bc1));
+        return __dsub_rn(p, __ddiv_rn(num, __dadd_rn(__dsqrt_rn(__ddiv_rn(v, bc2)), 1e-15)));
+    } else {  // FP32: reciprocals of the bias corrections, one IEEE divide
+        m = __fadd_rn(__fmul_rn(0.9f, m), __fmul_rn(1.f - 0.9f, gr));
+        v = __fadd_rn(__fmul_rn(0.999f, v), __fmul_rn(__fmul_rn(1.f - 0.999f, gr), gr));
+        const float num = __fmul_rn(lr, __fmul_rn(m, float(1.0 / bc1)));
+        return __fsub_rn(p, __fdiv_rn(num, __fadd_rn(__fsqrt_rn(__fmul_rn(v, float(1.0 / bc2))), 1e-15f)));
+    }
 }
 
 __device__ __forceinline__ int adam_segment(const AdamSegments& seg, int64_t e) {

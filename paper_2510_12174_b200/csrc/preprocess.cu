@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kPreThreads, K1_MINB) preprocess_kernel(const 
     a.visible[i] = 0;
 
     if (bad_s[threadIdx.x] || !finite_params(a, i)) {  // Scene::validate / activate (scene.cpp:36-38, 43-45)
-        raise_error(a.err, kErrNonFiniteParam, 0, i);
+        raise_error_ordered(a.err, kErrNonFiniteParam, i);
         return;
     }
     // ---- activate (scene.cpp:42-60)
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kPreThreads, K1_MINB) preprocess_kernel(const 
     n2 += q[3] * q[3];
     const double qn = sqrt(n2);
     if (qn < 1e-12) {
-        raise_error(a.err, kErrZeroQuat, 0, i);
+        raise_error_ordered(a.err, kErrZeroQuat, i);
         return;
     }
     for (int j = 0; j < 4; ++j) q[j] = q[j] / qn;

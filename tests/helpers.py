@@ -66,3 +66,53 @@ def rel_max_err(a, b, mask=None):
 def rel_l2_err(a, b):
     b = np.asarray(b, np.float64)
     return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def touched_gaussians(bins, pre, flip, width, height, tile=16):
+    """Gaussians that may blend at a decision-flip pixel (contributor count or
+    terminus differing from the reference): every Gaussian in that pixel's tile
+    list whose centre lies within 1.2 x its 3-sigma radius + 1 px (alpha >= 1/255
+    reaches ~3.33 sigma, rasterizer.cpp:139 vs geometry.cpp:132-134).  A
+    superset, used to report flip-driven gradient differences separately."""
+    off, vals = bins
+    n = len(pre["visible"])
+    touched = np.zeros(n, bool)
+    ys, xs = np.nonzero(flip)
+    tiles_x = (width + tile - 1) // tile
+    for y, x in zip(ys.tolist(), xs.tolist()):
+        t = (y // tile) * tiles_x + x // tile
+        ids = np.asarray(vals[off[t]:off[t + 1]], np.int64)
+        if ids.size == 0:
+            continue
+        c = pre["center"][ids]
+        r = pre["radius"][ids]
+        d = np.hypot(c[:, 0] - (x + 0.5), c[:, 1] - (y + 0.5))
+        touched[ids[d <= 1.2 * r + 1.0]] = True
+    return touched
+
+
+def grad_parity(got, ref, touched=None, floor_frac=1e-3):
+    """Per-element gradient parity (floors in the style of
+    proj/tests/test_common.hpp:57-64).  Per attribute:
+      max_rel        max |a-b| / max|b|                   (over every Gaussian)
+      max_rel_clean  the same without the flip-touched Gaussians
+      p9999_floor    99.99th percentile of |a-b| / max(|a|, |b|, floor_frac max|b|)
+    Returns {name: {...}} for the attributes the reference fills."""
+    out = {}
+    for k in GRAD_NAMES:
+        b = np.asarray(ref[k], np.float64)
+        if not b.size:
+            continue
+        a = np.asarray(got[k], np.float64)
+        d = np.abs(a - b)
+        scale = max(np.abs(b).max(), 1e-30)
+        per = d.reshape(d.shape[0], -1).max(axis=1) if d.ndim > 1 else d
+        rel = d / np.maximum(np.maximum(np.abs(a), np.abs(b)), floor_frac * scale)
+        rec = {"max_rel": float(per.max() / scale),
+               "p9999_floor": float(np.quantile(rel, 0.9999))}
+        if touched is not None:
+            keep = ~touched
+            rec["max_rel_clean"] = float(per[keep].max() / scale) if keep.any() else 0.0
+            rec["touched"] = int(touched.sum())
+        out[k] = rec
+    return out

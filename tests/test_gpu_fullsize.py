@@ -9,7 +9,10 @@ reference CPU path (oracle/_ref, all host cores) on the same seeded scenes:
 Bars (north star): tile lists / order / ranges bit-exact; rendered channels
 max-abs <= 1e-4 relative on pixels whose blend decisions agree (FP32; the
 share of pixels with a flipped decision is bounded separately); gradients
-rel-L2 <= 1e-3 (FP32) / 1e-8 (FP64).  Plus size-independent properties at
+per element (check_fp32_grads): max |a-b| <= 1e-3 max|b| on every Gaussian not
+touched by a decision-flip pixel, the flip-touched ones counted and bounded
+separately, and the 99.99th percentile of the floored relative error
+(proj/tests/test_common.hpp:57-64) reported and bounded; FP64 rel-L2 <= 1e-8.  Plus size-independent properties at
 cfg3: sum of blend weights = 1 - T, and the deterministic backward is bitwise
 reproducible.
 """
@@ -18,7 +21,8 @@ import os
 import numpy as np
 import pytest
 
-from helpers import GRAD_NAMES, frame_np, gpu_forward, grads_np, hwc_pix, rel_l2_err, rel_max_err, torch_pix
+from helpers import (GRAD_NAMES, frame_np, gpu_forward, grad_parity, grads_np, hwc_pix, rel_l2_err, rel_max_err,
+                     torch_pix, touched_gaussians)
 from paper_2510_12174_b200 import scenes
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
@@ -31,6 +35,22 @@ def config_case(name, seed=0):
     s = scenes.make_room_scene(c["n"], c["C"], 2, seed=seed, views=(0,), width=c["width"], height=c["height"],
                                f=c["f"])
     return s, scenes.view_camera(0, c["width"], c["height"], c["f"])
+
+
+def check_fp32_grads(g, ref, replay, pre, flip, cam):
+    """Per-element FP32 gradient bar.  Measured on the
+    B200 (tools/grad_parity_probe.py): clean Gaussians <= 2.6e-5 of max|ref| at
+    cfg3; flip-touched (a superset: 40k of 1M at cfg3, 235 flip pixels) <= 9e-3;
+    p99.99 floored <= 7.3e-3."""
+    touched = touched_gaussians(replay.bins(), pre, flip, cam["width"], cam["height"])
+    rep = grad_parity(g, ref, touched)
+    print("grad parity", {k: {f: float("%.3g" % v) for f, v in r.items()} for k, r in rep.items()})
+    assert touched.mean() < 0.05
+    for k, r in rep.items():
+        assert r["max_rel_clean"] <= 1e-3, (k, r)
+        assert r["max_rel"] <= 2e-2, (k, r)
+        assert r["p9999_floor"] <= 1.5e-2, (k, r)
+    return rep
 
 
 def _check_forward(z_ref, got, replay, bins_ref, dtype):
@@ -78,10 +98,13 @@ def test_cfg1_cfg2_full_size(port, reference, cfg, dtype):
     dt = torch.float64 if dtype == "float64" else torch.float32
     g = grads_np(M.rasterize_backward(scene, view, frame, replay, torch_pix(pix, dt)))
     ref = reference.backward(s, cam, hwc_pix(pix), BG, threads=THREADS)
-    gtol = 1e-8 if dtype == "float64" else 1e-3
+    if dtype == "float32":
+        flip = ~((frame.contributors.cpu().numpy() == z["contributors"]) & (replay.terminus() == z["terminus"]))
+        check_fp32_grads(g, ref, replay, pre, flip, cam)
+        return
     for k in GRAD_NAMES:
         if ref[k].size:
-            assert rel_l2_err(g[k], ref[k]) < gtol, k
+            assert rel_l2_err(g[k], ref[k]) < 1e-8, k
 
 
 def test_cfg3_full_size(port, reference):
@@ -101,9 +124,8 @@ def test_cfg3_full_size(port, reference):
     pix = scenes.pixel_grads(cam["width"], cam["height"], s["num_classes"], seed=4, scale=1.0)
     g = grads_np(M.rasterize_backward(scene, view, frame, replay, torch_pix(pix, torch.float32)))
     ref = reference.backward(s, cam, hwc_pix(pix), BG, threads=THREADS)
-    for k in GRAD_NAMES:
-        if ref[k].size:
-            assert rel_l2_err(g[k], ref[k]) < 1e-3, k
+    flip = ~((got["contributors"] == z["contributors"]) & (replay.terminus() == z["terminus"]))
+    check_fp32_grads(g, ref, replay, pre, flip, cam)
     # the deterministic backward is bitwise reproducible at full size
     M.set_deterministic(True)
     try:
@@ -113,8 +135,7 @@ def test_cfg3_full_size(port, reference):
         M.set_deterministic(False)
     for k in GRAD_NAMES:
         assert np.array_equal(a[k], b[k]), k
-        if ref[k].size:
-            assert rel_l2_err(a[k], ref[k]) < 1e-3, k
+    check_fp32_grads(a, ref, replay, pre, flip, cam)
 
 
 def test_cfg5_forward_full_size(port, reference):

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 import torch
 
-from helpers import GRAD_NAMES, frame_np, gpu_forward, grads_np, hwc_pix, rel_l2_err, rel_max_err, torch_pix
+from helpers import GRAD_NAMES, frame_np, gpu_forward, grad_parity, grads_np, hwc_pix, rel_l2_err, rel_max_err, torch_pix
 from test_oracle import _load_golden
 
 pytestmark = pytest.mark.gpu
@@ -39,6 +39,9 @@ def test_cuda_path_matches_reference_golden(name, dtype):
     for k in GRAD_NAMES:
         if z["bwd_" + k].size:
             assert rel_l2_err(g[k], z["bwd_" + k]) < gtol, k
+    if dtype == "float32" and same.all():  # no decision flips: the per-element bar on every Gaussian
+        for k, r in grad_parity(g, {k: z["bwd_" + k] for k in GRAD_NAMES}).items():
+            assert r["max_rel"] <= 1e-4 and r["p9999_floor"] <= 1e-3, (k, r)
     # the fused training-step unit, chained, against the reference's
     frame2 = M.MultimodalFrame.empty(cam["width"], cam["height"], s["num_classes"], dt, "cuda")
     grads = M.GradientBuffer.zeros_like_scene(scene)

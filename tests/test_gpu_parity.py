@@ -12,7 +12,7 @@ Bars (BASELINE.json north star):
 import numpy as np
 import pytest
 
-from helpers import GRAD_NAMES, frame_np, gpu_forward, grads_np, hwc_pix, rel_l2_err, rel_max_err, torch_pix
+from helpers import GRAD_NAMES, frame_np, gpu_forward, grad_parity, grads_np, hwc_pix, rel_l2_err, rel_max_err, torch_pix
 from paper_2510_12174_b200 import scenes
 
 pytestmark = pytest.mark.gpu
@@ -112,6 +112,9 @@ def test_backward_matches_oracle(port, case, dtype, tol):
         e = rel_l2_err(g[k], ref[k])
         print(f"case {case} {dtype} {k}: rel L2 {e:.2e}")
         assert e < tol, k
+    if dtype == "float32":  # per element (no decision flips at these sizes): max |a-b| <= 1e-3 max|b|
+        for k, r in grad_parity(g, ref).items():
+            assert r["max_rel"] <= 1e-3 and r["p9999_floor"] <= 1e-3, (k, r)
 
 
 @pytest.mark.parametrize("dtype,tol", [("float64", 1e-8), ("float32", 1e-3)])
@@ -424,3 +427,108 @@ def test_accumulate_packed(dtype, count, offset):
     assert np.array_equal(dst.cpu().numpy(), want)
     with pytest.raises(ValueError):
         M.accumulate_packed(dst, src[:-1] if count > 1 else src.double() if dtype == "float32" else src.float())
+
+
+def test_fp32_prune_mask_bit_exact(port):
+    """FP32 scenes: the prune mask (trainer.cpp:135-147) and the compaction
+    (:150-168) keep exactly the reference's Gaussians -- the reference's test
+    on the float-rounded k values, including values at the threshold edge."""
+    import torch
+    import paper_2510_12174_b200 as M
+    rng = np.random.default_rng(21)
+    n = 7001
+    k = rng.uniform(0, 2, n).astype(np.float32)
+    k[:6] = np.float32([0.5, 1.5, 1.5000001, 0.49999997, 1.0, 0.0])  # edges of |k - 1| > 0.5
+    for keep_small in (False, True):
+        s = dict(scenes.make_random_scene(n, 2, 1, seed=4), k=k.astype(np.float64))
+        sc = M.Scene.from_numpy(s, dtype=torch.float32)
+        ids = torch.arange(n, dtype=torch.float32, device="cuda")
+        sc.opacity_logits.copy_(ids)  # carries each Gaussian's index through the compaction
+        st = M.OptimizerState.init(sc)
+        mask_ref = port.prune_mask(k.astype(np.float64), 0.5, keep_small)
+        removed = M.prune(sc, st, M.TrainConfig(prune_keep_small=keep_small))
+        assert removed == int((~mask_ref).sum())
+        assert np.array_equal(sc.opacity_logits.cpu().numpy().astype(np.int64), np.nonzero(mask_ref)[0])
+
+
+def test_non_finite_output_raises():
+    """rasterize: non-finite output at pixel (x,y) (rasterizer.cpp:179-183)."""
+    s = scenes.make_random_scene(40, 2, 1, seed=5)
+    for dtype in ("float32", "float64"):
+        with pytest.raises(RuntimeError, match=r"non-finite output at pixel \(\d+,\d+\)"):
+            gpu_forward(s, scenes.simple_camera(), {"background": (float("inf"), 0.0, 0.0)}, dtype)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+@pytest.mark.parametrize("field", ["dcolor", "dsemantics", "ddepth"])
+def test_non_finite_pixel_gradient_names_reference_primitive(port, dtype, field):
+    """A non-finite pixel gradient makes check_finite (scene.cpp:97-106) throw
+    'non-finite gradient for primitive i' with i the LOWEST primitive whose
+    gradient is non-finite in the reference -- the primitives blending at that
+    pixel, and no others (the FP32 tensor-core products must not spread NaN)."""
+    import torch
+    import paper_2510_12174_b200 as M
+    s, cam = CASES[1]
+    scene, view, rc, replay, frame = gpu_forward(s, cam, BG, dtype)
+    cont = frame.contributors.cpu().numpy()
+    y, x = np.unravel_index(np.argmax(cont), cont.shape)
+    pix = scenes.pixel_grads(cam["width"], cam["height"], s["num_classes"], seed=5, scale=1.0)
+    pix = {k: np.array(v) for k, v in pix.items()}
+    if field == "ddepth":
+        pix["ddepth"][y, x] = np.inf
+    else:
+        pix[field][1, y, x] = np.nan
+    import re
+    with pytest.raises(Exception) as ei:  # the oracle restates check_finite
+        port.backward(s, cam, hwc_pix(pix), BG)
+    first = int(re.search(r"non-finite gradient for primitive (\d+)", str(ei.value)).group(1))
+    dt = torch.float64 if dtype == "float64" else torch.float32
+    with pytest.raises(RuntimeError, match=f"non-finite gradient for primitive {first}$"):
+        M.rasterize_backward(scene, view, frame, replay, torch_pix(pix, dt))
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_deterministic_step_is_graph_capturable(dtype):
+    """The deterministic backward (fixed-order reduction, tests/test_rasterizer.cpp:
+    386-419) sizes its partial slots from a capacity, so the training step can
+    be captured into a CUDA graph: every replay gives the eager step's bits."""
+    import torch
+    import paper_2510_12174_b200 as M
+    from paper_2510_12174_b200.distributed import ViewShardedStep
+    dt = torch.float64 if dtype == "float64" else torch.float32
+    V, W, H, C = 2, 96, 64, 4
+    s = scenes.make_room_scene(20000, C, 1, seed=5, views=tuple(range(V)), width=W, height=H, f=70.0)
+    scene = M.Scene.from_numpy(s, dtype=dt)
+    n = scene.size()
+    flat = M.pack_scene(scene)
+    gflat = torch.zeros(M.param_layout(n, C, 1)[-1], dtype=dt, device="cuda")
+    grads = M.GradientBuffer.from_packed(gflat, n, C, 1)
+    cams, pixs = [], []
+    for v in range(V):
+        cam = scenes.view_camera(v, W, H, 70.0)
+        cams.append(M.make_camera(cam["fx"], cam["fy"], cam["cx"], cam["cy"], W, H, cam["R_c2w"], cam["t_c2w"]))
+        pixs.append(torch_pix(scenes.pixel_grads(W, H, C, seed=20 + v, scale=1.0), dt))
+    frame = M.MultimodalFrame.empty(W, H, C, dt, "cuda")
+    M.set_deterministic(True)
+    try:
+        step = ViewShardedStep(scene, flat, gflat, grads, M.OptimizerState(torch.zeros_like(flat),
+                               torch.zeros_like(flat), 0), M.TrainConfig(), M.RenderConfig(), M.NormalConfig(),
+                               cams, pixs, frame, M.ReplayState(), lanes=1, optimizer=False)
+        gflat.zero_()
+        step()  # eager: sizes the replay, the pair records and the deterministic slots
+        torch.cuda.synchronize()
+        eager = gflat.clone()
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(g, stream=cap):
+            step()
+        for _ in range(2):
+            gflat.zero_()
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(gflat, eager)
+        M.rasterizer.check_device_errors()
+    finally:
+        M.set_deterministic(False)

@@ -9,7 +9,7 @@ ARCH="-gencode arch=compute_100a,code=sm_100a"
 /usr/local/cuda/bin/nvcc -std=c++17 -O3 -lineinfo $ARCH -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
   --expt-relaxed-constexpr "$@" -c $stem.cu -o /tmp/variant_$stem.o
 objs=""
-for s in preprocess binning forward normals backward backward_blend optim losses trainer_ops scene_io cabi; do
+for s in preprocess binning forward forward_split normals backward backward_blend optim losses trainer_ops scene_io cabi; do
   if [ $s = $stem ]; then objs="$objs /tmp/variant_$stem.o"; else objs="$objs ../../build/csrc/$s.o"; fi
 done
 /usr/local/cuda/bin/nvcc $ARCH -shared -cudart static -o ../libmsplat_b200_$name.so $objs

@@ -47,7 +47,7 @@ print("\n".join(out))
 # K9 = tensor-core phase A + pair-record phase B)
 traffic = {}
 for k, v in agg.items():
-    for stage, prefs in (("backward", ("backward_kernel", "backward_pairs_kernel", "order_hist_kernel", "order_scatter_kernel")), ("forward", ("forward_kernel",)),
+    for stage, prefs in (("backward", ("backward_kernel", "backward_pairs_kernel", "order_hist_kernel", "order_scatter_kernel")), ("forward", ("forward_kernel", "forward_alpha_kernel", "forward_sem_kernel", "forward_depth_kernel")),
                          ("preprocess", ("preprocess_kernel",)), ("proj_bwd", ("projection_backward_kernel",))):
         if any(k.startswith(pref) for pref in prefs):
             traffic[stage] = traffic.get(stage, 0.0) + v[2] / v[0]
