@@ -277,9 +277,9 @@ __device__ __forceinline__ void flush_pairs(const BackwardArgs<Real>& a, const Q
 }
 
 // K9 phase B on n (<= 32) of the 16-byte pair records phase A wrote
-// ({gid, pixel lane, v0 = G dalpha, dd = dD w}): dopacity = v0, dmean2d / dconic
-// from dpower = opacity v0 (= alpha dalpha; 0 when alpha was clamped), the
-// depth chain from dd; segmented by Gaussian, one vector reduction per row.
+// ({gid, pixel lane, dpower = alpha dalpha (0 when alpha was clamped), dd =
+// dD w}): dopacity = G dalpha = dpower / opacity, dmean2d / dconic from dpower,
+// the depth chain from dd; segmented by Gaussian, one vector reduction per row.
 __device__ __forceinline__ void flush_records(const BackwardArgs<float>& a, const uint4* rec, int n, int bx, int by,
                                               const float4* rays, float zoff) {
     const int lane = threadIdx.x & 31;
@@ -302,14 +302,13 @@ __device__ __forceinline__ void flush_records(const BackwardArgs<float>& a, cons
     if (act) {
         const int L = int(r.y);
         const int xL = bx + (L & 7), yL = by + (L >> 3);
-        const float v0 = __uint_as_float(r.z), dd = __uint_as_float(r.w);
-        if (v0 != 0.f) {  // rasterizer_backward.cpp:234-244
+        const float dpower = __uint_as_float(r.z), dd = __uint_as_float(r.w);
+        if (dpower != 0.f) {  // rasterizer_backward.cpp:234-244
             const AlphaRec<float>& ar = a.arec[g];
             const float4 c0 = *reinterpret_cast<const float4*>(&ar.cx);        // cx, cy, ca, cb
-            const float2 c1 = *reinterpret_cast<const float2*>(&ar.cc);        // cc, opacity
+            const float4 c1 = *reinterpret_cast<const float4*>(&ar.cc);        // cc, opacity, log_thr, 1 / opacity
             const float dx = float(xL) + 0.5f - c0.x, dy = float(yL) + 0.5f - c0.y;
-            const float dpower = c1.y * v0;
-            v[0] = v0;
+            v[0] = dpower * c1.w;
             v[1] = dpower * (c0.z * dx + c0.w * dy);
             v[2] = dpower * (c0.w * dx + c1.x * dy);
             v[3] = dpower * (-0.5f * dx * dx);
@@ -620,6 +619,16 @@ __device__ __forceinline__ void stage_rows_tc(float* Fb, int sp, const AlphaRec<
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
+// kRows: the forward ran split (forward_split.cu) and left one row of 32 blend
+// weights per event (negated where alpha was clamped at 0.99).  The recursion then needs no
+// alpha records and no alpha test: w comes from the row, the transmittance is
+// restored by addition (T_j = T_{j+1} + w_j, exact in real arithmetic since
+// T_{j+1} = T_j (1 - alpha_j) and w_j = alpha_j T_j), alpha_j = w_j / T_j, and
+// with B_j = sum_{k>j} w_k FS_k (the pixel's suffix sum) the reference's
+//   dalpha = (FS_j - acc) T_j - T_final bg / (1 - alpha_j)
+// is T_j (FS_j - (B_j + T_final bg) / T_{j+1}) (rasterizer_backward.cpp:222-232).
+// GEMM2 reads the same rows.
+template <bool kRows>
 __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_constant__ BackwardArgs<float> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int C = a.C, sp = seed_pitch(C), S = C + 4, K8 = seed_k8(C);
@@ -693,10 +702,13 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
     ws->dDs[lane] = dD;
     ws->bgd[lane] = float(a.rp.bg[0]) * my_seed[0] + float(a.rp.bg[1]) * my_seed[1] + float(a.rp.bg[2]) * my_seed[2];
     float T = T_final, accA = 0.f, lastFS = 0.f, last_alpha = 0.f;
+    const float Tfb = T_final * ws->bgd[lane];  // kRows: T_final (bg . dC)
     const uint2 range = a.tile_range[tile];
     const uint32_t list0 = range.x;
     const uint32_t nev = a.ev_count[seg];
-    const uint2* const evl = a.ev_list + size_t(8) * list0 + size_t(wl) * (range.y - list0);
+    const size_t ev0 = size_t(8) * list0 + size_t(wl) * (range.y - list0);  // this segment's event-log region
+    const uint2* const evl = a.ev_list + ev0;
+    const float* const wrows = kRows ? a.ev_w + ev0 * 32 : nullptr;
     const int mtiles2 = (S + 15) / 16;  // GEMM2 channel tiles
     if (bad_mask) {  // error path only (warp-uniform)
         for (int e = lane; e < int(nev); e += 32) {
@@ -730,7 +742,7 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
             asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
             asm volatile("prefetch.global.L2 [%0];" ::"l"(row + 4 * C - 4));
             if (C > 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + 128));
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(a.arec + g)));
+            if (!kRows) asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(a.arec + g)));
         }
         if (cb - 32 - lane >= 0) {
             const uint2 ev = evl[cb - 32 - lane];
@@ -751,9 +763,25 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
         const int nb = cb + 1 < 32 ? cb + 1 : 32;
         for (int s0 = 0; s0 < nb; s0 += kSub) {
             const int ns = nb - s0 < kSub ? nb - s0 : kSub;
-            // (a) F rows (cp.async) and alpha records of the sub-batch.
+            // (a) F rows (cp.async) and alpha records of the sub-batch (kRows:
+            // the events' weight rows instead; slot s0 + e is event cb - s0 - e).
+            if constexpr (kRows) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {  // 8 rows x 8 16-byte pieces
+                    const int i = lane + 32 * h, e = i >> 3, q = i & 7;
+                    float* const dst = Wb + e * kTilePitch + 4 * q;
+                    if (e < ns) {
+                        const unsigned d = unsigned(__cvta_generic_to_shared(dst));
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d),
+                                     "l"(wrows + size_t(cb - s0 - e) * 32 + 4 * q)
+                                     : "memory");
+                    } else {
+                        *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                }
+            }
             stage_rows_tc(Fb, sp, a.arec, a.semantics, C, a.sem_vec != 0, ws->gid + s0, ns, lane);
-            if (lane < ns) ws->rec[lane] = a.arec[ws->gid[s0 + lane]];
+            if (!kRows && lane < ns) ws->rec[lane] = a.arec[ws->gid[s0 + lane]];
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncwarp();
             // (b) GEMM1: FS[px][e], px on M (two 16-row tiles), events on N.
@@ -778,6 +806,30 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
 #pragma unroll kK9Unroll
             for (int e = 0; e < ns; ++e) {
                 const unsigned fmask = ws->emask[s0 + e];
+                if constexpr (kRows) {  // the forward's weights and decisions
+                    if ((fmask >> lane) & 1u) {
+                        const float ws_ = Wb[e * kTilePitch + lane];
+                        const bool clamped = ws_ < 0.f;
+                        const float w = fabsf(ws_);
+                        Wb[e * kTilePitch + lane] = w;  // GEMM2 reads plain weights
+                        const float Tj = T + w;
+                        const float FS = FSs[e * kTilePitch + lane];
+                        const float rT = T > 0.f ? __fdividef(1.f, T) : 0.f;  // 1 / T_{j+1}
+                        const float dalpha = Tj * (FS - (accA + Tfb) * rT);   // accA = B_j here
+                        accA = fmaf(w, FS, accA);
+                        const float dpower = clamped ? 0.f : __fdividef(w, Tj) * dalpha;  // alpha dalpha
+                        const int64_t qe = qn + __popc(fmask & ((1u << lane) - 1u));
+                        if (qe < pcap) {
+                            a.pr[pbase + qe] = make_uint4(ws->gid[s0 + e], uint32_t(lane), __float_as_uint(dpower),
+                                                          __float_as_uint(ws->dDs[lane] * w));
+                        } else {
+                            raise_error(a.err, kErrPairOverflow, pbase + qe, a.pair_cap);
+                        }
+                        T = Tj;
+                    }
+                    qn += __popc(fmask);
+                    continue;
+                }
                 AlphaEval<float> ae;
                 ae.pass = false;
                 if ((fmask >> lane) & 1u)
@@ -796,8 +848,8 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
                     // the pair record for phase B (backward_pairs_kernel)
                     const int64_t qe = qn + __popc(mask & ((1u << lane) - 1u));
                     if (qe < pcap) {
-                        const float v0 = ae.clamped ? 0.f : ae.gauss * dalpha;
-                        a.pr[pbase + qe] = make_uint4(ws->gid[s0 + e], uint32_t(lane), __float_as_uint(v0),
+                        const float dpower = ae.clamped ? 0.f : ae.alpha * dalpha;
+                        a.pr[pbase + qe] = make_uint4(ws->gid[s0 + e], uint32_t(lane), __float_as_uint(dpower),
                                                       __float_as_uint(ws->dDs[lane] * w));
                     } else {
                         raise_error(a.err, kErrPairOverflow, pbase + qe, a.pair_cap);
@@ -808,7 +860,8 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_c
                 qn += __popc(mask);
                 __syncwarp();
             }
-            for (int e = ns; e < kSub; ++e) Wb[e * kTilePitch + lane] = 0.f;
+            if (!kRows)
+                for (int e = ns; e < kSub; ++e) Wb[e * kTilePitch + lane] = 0.f;
             __syncwarp();
             // (d) GEMM2: dF[ch][e] = sum_px S[px][ch] w_e[px], channels on M.
             // this lane's two events (columns 2 t4, 2 t4 + 1): semantic channel ch
@@ -988,9 +1041,14 @@ void launch_backward_blend(const BackwardArgs<Real>& a, int ntiles, cudaStream_t
     if (a.partial) {
         backward_kernel<Real, true><<<ntiles, kThreads, backward_smem_bytes<Real>(a.C), s>>>(a);
     } else if constexpr (sizeof(Real) == 4) {
-        static std::atomic<unsigned long long> attr_tc{0};
-        opt_in_smem(reinterpret_cast<const void*>(backward_kernel_tc), attr_tc);
-        backward_kernel_tc<<<ntiles, kThreads, backward_tc_smem_bytes(a.C), s>>>(a);
+        static std::atomic<unsigned long long> attr_tc{0}, attr_rows{0};
+        if (a.ev_w) {
+            opt_in_smem(reinterpret_cast<const void*>(backward_kernel_tc<true>), attr_rows);
+            backward_kernel_tc<true><<<ntiles, kThreads, backward_tc_smem_bytes(a.C), s>>>(a);
+        } else {
+            opt_in_smem(reinterpret_cast<const void*>(backward_kernel_tc<false>), attr_tc);
+            backward_kernel_tc<false><<<ntiles, kThreads, backward_tc_smem_bytes(a.C), s>>>(a);
+        }
         backward_pairs_kernel<<<unsigned((ntiles * 8 + 7) / 8), 256, 0, s>>>(a, ntiles * 8);
         count_launches(1);
     } else {

@@ -196,6 +196,7 @@ struct msplat_replay {
         d_inst_count, d_inst_total32, hist, hist_scanned, scan_tiles, terminus, weight_sums, saved_means,
         saved_k, cap_center, cap_conic, cap_depth, cap_radius, cap_rgb, visible_count, ev_list, ev_count, ev_npairs,
         pair_off, pair_n, pair_scan, pair_total, pair_rec, wq_order, wq_scratch, ev_w;
+    bool split_fwd = false;  // the last forward ran split: its weight rows are valid
     int64_t pair_cap = 0;  // pair-record capacity of the FP32 split backward
     uint32_t* sorted_gauss = nullptr;
 
@@ -543,8 +544,10 @@ msplat_status rasterize_impl(msplat_context* ctx, const msplat_scene* s, const m
             a.sem_vec = (a.C % 2 == 0) && (reinterpret_cast<uintptr_t>(s->semantics) % 8 == 0);
             launch_forward_split(a, r->tiles_x * r->tiles_y, ctx->stream,
                                  dynamic_schedule() ? r->wq_order.as<uint32_t>() : nullptr, r->wq_scratch.as<uint32_t>());
+            r->split_fwd = true;
         } else {
             launch_forward<Real>(a, r->tiles_x * r->tiles_y, ctx->stream);
+            r->split_fwd = false;
         }
     } else {
         launch_forward<Real>(a, r->tiles_x * r->tiles_y, ctx->stream);
@@ -700,6 +703,7 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
         BackwardArgs<float>& af = reinterpret_cast<BackwardArgs<float>&>(a);
         af.pair_off = rw->pair_off.as<uint32_t>();
         af.pair_n = rw->pair_n.as<uint32_t>();
+        if (r->split_fwd) af.ev_w = r->ev_w.as<float>();
         af.pr = rw->pair_rec.as<uint4>();
         af.pair_cap = rw->pair_cap;
         if (dynamic_schedule()) af.work_order = rw->wq_order.as<uint32_t>();

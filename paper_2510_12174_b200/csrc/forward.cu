@@ -257,7 +257,10 @@ __global__ void __launch_bounds__(kThreads, kSplit ? K6_SPLIT_MINB : 2) forward_
             if (mask == 0) continue;
             if (evl) {  // the backward replays exactly these events
                 if (lane == 0) evl[n_ev] = make_uint2(uint32_t(c * 32 + slot), mask);
-                if constexpr (kSplit) wd[size_t(n_ev) * 32 + lane] = ae.pass ? ae.alpha * T : Real(0);
+                if constexpr (kSplit) {  // w = alpha T; negated when alpha was clamped at 0.99 (for the backward)
+                    const Real w = ae.alpha * T;
+                    wd[size_t(n_ev) * 32 + lane] = ae.pass ? (ae.clamped ? -w : w) : Real(0);
+                }
                 ++n_ev;
                 n_pairs += __popc(mask);
             }

@@ -35,6 +35,9 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kNtMax = 8;  // semantic n-tiles in registers: C <= 64
 constexpr int kQueue = 64;
+#ifndef K6B_TILE_ORDER
+#define K6B_TILE_ORDER 0  // 1: the semantic pass in tile order (L2 sharing between neighbouring tiles)
+#endif
 #ifndef K6_SPLIT_DEPTH
 #define K6_SPLIT_DEPTH 0  // 1: depth in its own pass after a depth-free blend (measured slower)
 #endif
@@ -215,10 +218,10 @@ __device__ __forceinline__ void sem_batch(const PairSmem* ws, int buf, float (&a
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi) {  // A[px][ev]: rows px = 16 mi + g4 (+ 8), cols ev = t (+ 4)
         const int r0 = mi * 16 + g4, r1 = r0 + 8;
-        split_tf32(w0[r0], ah[mi][0], al[mi][0]);
-        split_tf32(w0[r1], ah[mi][1], al[mi][1]);
-        split_tf32(w1[r0], ah[mi][2], al[mi][2]);
-        split_tf32(w1[r1], ah[mi][3], al[mi][3]);
+        split_tf32(fabsf(w0[r0]), ah[mi][0], al[mi][0]);  // (the sign marks a clamped alpha)
+        split_tf32(fabsf(w0[r1]), ah[mi][1], al[mi][1]);
+        split_tf32(fabsf(w1[r0]), ah[mi][2], al[mi][2]);
+        split_tf32(fabsf(w1[r1]), ah[mi][3], al[mi][3]);
     }
     const float* const s0 = ws->srow[buf][t];
     const float* const s1 = ws->srow[buf][t + 4];
@@ -341,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, NT > 0 ? 2 : K6C_MINB) forward_pairs
         // depth: enqueue each event's blending lanes, flush 32 at a time
 #pragma unroll 1
         for (int k = 0; kDepth && k < nb; ++k) {
-            const float wk = ws->wt[buf][k][lane];
+            const float wk = fabsf(ws->wt[buf][k][lane]);
             const unsigned m = __ballot_sync(0xffffffffu, wk != 0.f);
             if (wk != 0.f) {
                 const int e = qn + __popc(m & lt);
@@ -406,10 +409,12 @@ void launch_forward_split(const ForwardArgs<float>& a, int ntiles, cudaStream_t 
 #endif
     ForwardArgs<float> b = a;
     b.work_order = nullptr;
-    if (seg_order && order_scratch) {  // longest-first segment order (by event count), shared with the backward
+#if !K6B_TILE_ORDER
+    if (seg_order && order_scratch) {  // longest-first segment order (by event count)
         launch_work_order(a.ev_count, ntiles * 8, const_cast<uint32_t*>(seg_order), order_scratch, s);
         b.work_order = seg_order;
     }
+#endif
     const size_t smem = 8 * sizeof(PairSmem);
     static std::atomic<unsigned long long> attr[9];  // per instantiation, per device
 #define K6B_LAUNCH(NT_)                                                                               \

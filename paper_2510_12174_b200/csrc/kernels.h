@@ -133,7 +133,8 @@ struct ForwardArgs {
     uint32_t* ev_count;
     uint32_t* ev_npairs;  // blended pairs per (tile, warp): the backward's pair-record segments
     // FP32 split forward (forward_split.cu): per event one row of 32 blend
-    // weights (0 for lanes that did not blend), in the region [32 (8 range.x +
+    // weights (0 for lanes that did not blend, negated where alpha was clamped
+    // at 0.99), in the region [32 (8 range.x +
     // warp len), + 32 len) -- the event log's region scaled by 32 -- and the
     // optional longest-first segment order of its per-pair kernel.
     float* ev_w;
@@ -277,6 +278,9 @@ struct BackwardArgs {
     // 20 + C values [opac, dmean2, dconic3, pos3, rot4, scale3, dcolor3, k, sem C].
     Real* partial;
     int V;
+    // The split forward's per-event weight rows (null when the forward ran
+    // fused): phase A then replays without alpha tests.
+    const float* ev_w;
     // Segment schedule of the FP32 split backward (optional): warp w of CTA b
     // replays segment work_order[8 b + w] = tile * 8 + block (longest first,
     // launch_work_order), and phase B takes segments in the same order.  Null:

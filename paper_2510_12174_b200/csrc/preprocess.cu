@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kPreThreads, K1_MINB) preprocess_kernel(const 
     ar.opacity = Real(opacity);
     const Real log_thr = log(Real(1) / (Real(255) * opacity));
     ar.log_thr = log_thr;
-    ar.pad = Real(0);
+    ar.pad = Real(1) / opacity;  // phase B's dopacity = dpower / opacity
     {
         // d^T conic d <= r2 with r2 = -2 (log_thr - 1e-3); the tight box of that
         // ellipse has half-widths sqrt(r2 cov_xx), sqrt(r2 cov_yy) (cov = conic^-1).
