@@ -63,6 +63,9 @@ def parse(argv=None):
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-dropin", action="store_true",
+                   help="skip the C++ drop-in record (msplat::rasterize + rasterize_backward with host Eigen AoS "
+                        "data at the reference API, tools/dropin_bench.cpp)")
     p.add_argument("--no-train-step", action="store_true", help="skip the training-step measurements")
     p.add_argument("--dry-run", action="store_true",
                    help="no CUDA: launcher + gloo exchange of the packed buffer only (no render, no value)")
@@ -866,6 +869,16 @@ def main(argv=None):
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
                                         "sample": f"unavailable: {e}"}
+        if world == 1 and not args.no_dropin and args.config in ("cfg2", "cfg3"):
+            # the plugin boundary: the reference API (rasterizer.hpp:67-83) through the C++ drop-in, host
+            # AoS in and out, one render per call (view 0 of the same scene), FP32 / FP64 x deterministic
+            try:
+                sys.path.insert(0, os.path.join(ROOT, "tools"))
+                import dropin_bench
+                line["dropin_e2e"] = {"unit": "renders/s (one fwd+bwd per call, wall clock)",
+                                      "records": dropin_bench.run_modes(args.config, iters=2, warmup=1)}
+            except Exception as e:  # noqa: BLE001
+                line["dropin_e2e"] = {"unavailable": str(e)[:300]}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -79,12 +79,16 @@ TileBins bin_and_sort(const std::vector<std::optional<Splat2D>>& splats, int wid
 
 // rasterize -- core/src/rasterizer.cpp:87-205
 MultimodalFrame rasterize(const Scene& scene, const CameraView& view, const RenderConfig& cfg, ReplayState* replay) {
+    PhaseTimer pt("rasterize");
     scene.validate();
+    pt.mark("validate");
     const bool f32 = use_fp32();
     const int W = view.width, H = view.height, C = scene.num_classes;
     const size_t HW = size_t(W) * H;
     DeviceScene ds(scene, f32);
-    DBuf color(3 * HW, f32), depth(HW, f32), sem(size_t(C) * HW, f32), kmap(HW, f32), T(HW, f32), normals(3 * HW, f32);
+    pt.mark("scene upload");
+    DBuf color(3 * HW, f32, false), depth(HW, f32, false), sem(size_t(C) * HW, f32, false), kmap(HW, f32, false),
+        T(HW, f32, false);
     int32_t* contrib = nullptr;
     cuda_check(cudaMalloc(&contrib, std::max<size_t>(HW, 1) * 4), "cudaMalloc");
     std::unique_ptr<int32_t, decltype(&cudaFree)> contrib_guard(contrib, cudaFree);
@@ -93,32 +97,41 @@ MultimodalFrame rasterize(const Scene& scene, const CameraView& view, const Rend
     const msplat_scene s = ds.abi();
     const msplat_camera c = to_abi(view);
     const msplat_render_config rc = to_abi(cfg);
+    pt.mark("buffers");
     rethrow(msplat_rasterize(context(), &s, &c, &rc, &fr, dev ? dev->handle : nullptr));
+    pt.mark("msplat_rasterize");
 
     MultimodalFrame f;
     f.width = W;
     f.height = H;
     f.num_classes = C;
-    f.color = from_planar(color.download(), W, H, 3);
-    f.depth = from_planar(depth.download(), W, H, 1);
-    f.semantics = C ? from_planar(sem.download(), W, H, C) : GridF(W, H, 0, 0.0);
-    f.kmap = from_planar(kmap.download(), W, H, 1);
-    f.transmittance = from_planar(T.download(), W, H, 1);
+    f.color = download_planar(color, W, H, 3);
+    f.depth = download_planar(depth, W, H, 1);
+    f.semantics = C ? download_planar(sem, W, H, C) : GridF(W, H, 0, 0.0);
+    f.kmap = download_planar(kmap, W, H, 1);
+    f.transmittance = download_planar(T, W, H, 1);
     f.normals = GridF(W, H, 3, 0.0);  // filled by estimate_normals, as in the reference
     f.contributors = Grid<int>(W, H, 1, 0);
     cuda_check(cudaMemcpy(f.contributors.data(), contrib, HW * 4, cudaMemcpyDeviceToHost), "download");
+    pt.mark("frame download");
 
     if (replay) {
         const size_t n = scene.size();
         replay->device = dev;
-        replay->activated = activate_scene(scene);  // borrows from `scene`, like the reference
+        // activate_scene (borrows from `scene`, like the reference), in parallel
+        replay->activated.assign(n, ActivatedGaussian{});
+        parallel_for(n, [&](size_t b, size_t e) {
+            for (size_t i = b; i < e; ++i) replay->activated[i] = activate(scene.gaussians[i], i);
+        });
+        pt.mark("replay activated");
         std::vector<uint8_t> vis(n), cl(3 * n);
         std::vector<double> center(2 * n), conic(3 * n), sdepth(n), radius(n), rgb(3 * n);
         rethrow(msplat_replay_splats(dev->handle, vis.data(), center.data(), conic.data(), sdepth.data(),
                                      radius.data(), rgb.data(), cl.data()));
         replay->splats.assign(n, std::nullopt);
         replay->colors.assign(n, ShColor{});
-        for (size_t i = 0; i < n; ++i) {
+        parallel_for(n, [&](size_t b, size_t e) {
+          for (size_t i = b; i < e; ++i) {
             if (!vis[i]) continue;
             Splat2D sp;
             sp.center = Vec2(center[2 * i], center[2 * i + 1]);
@@ -132,7 +145,9 @@ MultimodalFrame rasterize(const Scene& scene, const CameraView& view, const Rend
                 replay->colors[i].rgb[ch] = rgb[3 * i + ch];
                 replay->colors[i].clamped[ch] = cl[3 * i + ch] != 0;
             }
-        }
+          }
+        });
+        pt.mark("replay splats");
         msplat_counters cn{};
         rethrow(msplat_replay_counters(dev->handle, &cn));
         std::vector<int64_t> off(size_t(cn.tiles) + 1);
@@ -141,8 +156,9 @@ MultimodalFrame rasterize(const Scene& scene, const CameraView& view, const Rend
         replay->bins.tiles_x = (W + TileBins::kTileSize - 1) / TileBins::kTileSize;
         replay->bins.tiles_y = (H + TileBins::kTileSize - 1) / TileBins::kTileSize;
         replay->bins.bins.assign(size_t(cn.tiles), {});
-        for (size_t t = 0; t < size_t(cn.tiles); ++t)
-            replay->bins.bins[t].assign(vals.begin() + off[t], vals.begin() + off[t + 1]);
+        parallel_for(size_t(cn.tiles), [&](size_t b, size_t e) {
+            for (size_t t = b; t < e; ++t) replay->bins.bins[t].assign(vals.begin() + off[t], vals.begin() + off[t + 1]);
+        }, 64);
         replay->terminus = Grid<int>(W, H, 1, 0);
         rethrow(msplat_replay_terminus(dev->handle, replay->terminus.data()));
         replay->weight_sums.assign(n, 0.0);
@@ -151,35 +167,68 @@ MultimodalFrame rasterize(const Scene& scene, const CameraView& view, const Rend
         replay->sh_degree = scene.sh_degree;
         replay->num_classes = scene.num_classes;
         replay->cfg = cfg;
+        pt.mark("replay bins/terminus/ws");
     }
     return f;
 }
 
 namespace {
 
-void grads_from_device(GradientBuffer& g, const Scene& scene, DBuf& dpos, DBuf& drot, DBuf& dsc, DBuf& dop, DBuf& dk,
-                       DBuf& dsh, DBuf& dsem) {
-    g.resize_zero(scene);
-    const int K = scene.sh_coeff_count(), C = scene.num_classes;
-    const auto p = dpos.download(), r = drot.download(), s = dsc.download(), o = dop.download(), k = dk.download(),
-               h = dsh.download(), e = dsem.download();
-    for (size_t i = 0; i < scene.size(); ++i) {
-        g.dposition[i] = Vec3(p[3 * i], p[3 * i + 1], p[3 * i + 2]);
-        g.drotation[i] = Vec4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
-        g.dscale[i] = Vec3(s[3 * i], s[3 * i + 1], s[3 * i + 2]);
-        g.dopacity[i] = o[i];
-        g.dk[i] = k[i];
-        for (int c = 0; c < 3; ++c)
-            for (int j = 0; j < K; ++j) g.dsh[i](c, j) = h[(i * 3 + c) * K + j];
-        for (int c = 0; c < C; ++c) g.dsemantics[i][c] = e[i * C + c];
+// The gradient arrays as one device allocation (the packed order of
+// DeviceScene), downloaded once and scattered into the AoS GradientBuffer
+// (GradientBuffer::resize_zero's shapes, scene.cpp:70-95) in parallel.
+struct DeviceGrads {
+    size_t off[8];
+    DBuf all;
+    DeviceGrads(const Scene& scene, bool f32)
+        : all(DeviceScene::total(int64_t(scene.size()), scene.num_classes, scene.sh_coeff_count()), f32, false) {
+        const size_t N = scene.size();
+        const int K = scene.sh_coeff_count(), C = scene.num_classes;
+        const size_t len[7] = {3 * N, 4 * N, 3 * N, N, N, size_t(3 * K) * N, size_t(C) * N};
+        off[0] = 0;
+        for (int i = 0; i < 7; ++i) off[i + 1] = off[i] + len[i];
     }
-}
+    void* ptr(int i) const { return static_cast<char*>(all.p) + off[i] * (all.f32 ? 4 : 8); }
+    // buffer order: position, rotation, scale, opacity, k, sh, semantics
+    msplat_grads abi(int C) const { return msplat_grads{ptr(0), ptr(1), ptr(2), ptr(3), ptr(4), ptr(5), C ? ptr(6) : nullptr}; }
+    void to_host(GradientBuffer& g, const Scene& scene) const {
+        const size_t n = scene.size();
+        const int K = scene.sh_coeff_count(), C = scene.num_classes;
+        g.dposition.resize(n);
+        g.drotation.resize(n);
+        g.dscale.resize(n);
+        g.dopacity.resize(n);
+        g.dk.resize(n);
+        g.dsh.resize(n);
+        g.dsemantics.resize(n);
+        g.raw_space = false;
+        all.download_with([&](const auto* d) {
+            const auto *p = d + off[0], *r = d + off[1], *s = d + off[2], *o = d + off[3], *k = d + off[4],
+                       *h = d + off[5], *e = d + off[6];
+            parallel_for(n, [&](size_t b, size_t e_) {
+                for (size_t i = b; i < e_; ++i) {
+                    g.dposition[i] = Vec3(p[3 * i], p[3 * i + 1], p[3 * i + 2]);
+                    g.drotation[i] = Vec4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+                    g.dscale[i] = Vec3(s[3 * i], s[3 * i + 1], s[3 * i + 2]);
+                    g.dopacity[i] = o[i];
+                    g.dk[i] = k[i];
+                    g.dsh[i].resize(3, K);
+                    for (int c = 0; c < 3; ++c)
+                        for (int j = 0; j < K; ++j) g.dsh[i](c, j) = h[(i * 3 + c) * K + j];
+                    g.dsemantics[i].resize(C);
+                    for (int c = 0; c < C; ++c) g.dsemantics[i][c] = e[i * C + c];
+                }
+            }, 4096);
+        });
+    }
+};
 
 }  // namespace
 
 // rasterize_backward -- core/src/rasterizer_backward.cpp:127-264 (check_replay :35-53)
 GradientBuffer rasterize_backward(const Scene& scene, const CameraView& view, const MultimodalFrame& frame,
                                   const ReplayState& replay, const PixelGradients& pix) {
+    PhaseTimer pt("backward");
     if (replay.num_gaussians != scene.size() || replay.sh_degree != scene.sh_degree ||
         replay.num_classes != scene.num_classes || !replay.device)
         throw std::runtime_error("rasterize_backward: replay state does not match the scene");
@@ -195,27 +244,31 @@ GradientBuffer rasterize_backward(const Scene& scene, const CameraView& view, co
                     pix.dsemantics.same_shape(frame.semantics) && pix.dkmap.same_shape(frame.kmap);
     if (!ok) throw std::runtime_error("rasterize_backward: pixel-gradient shape mismatch");
 
+    pt.mark("checks");
     const bool f32 = replay.device->f32;
     const int W = frame.width, H = frame.height, C = scene.num_classes;
-    const size_t HW = size_t(W) * H, n = scene.size();
+    const size_t HW = size_t(W) * H;
     DeviceScene ds(scene, f32);
-    DBuf T(HW, f32), dC(3 * HW, f32), dD(HW, f32), dO(size_t(C) * HW, f32), dK(HW, f32);
-    T.upload(to_planar(frame.transmittance));
-    dC.upload(to_planar(pix.dcolor));
-    dD.upload(to_planar(pix.ddepth));
-    if (C) dO.upload(to_planar(pix.dsemantics));
-    dK.upload(to_planar(pix.dkmap));
-    const int K = scene.sh_coeff_count();
-    DBuf gpos(3 * n, f32), grot(4 * n, f32), gsc(3 * n, f32), gop(n, f32), gk(n, f32), gsh(size_t(3 * K) * n, f32),
-        gsem(size_t(C) * n, f32);
+    pt.mark("scene upload");
+    DBuf T(HW, f32, false), dC(3 * HW, f32, false), dD(HW, f32, false), dO(size_t(C) * HW, f32, false),
+        dK(HW, f32, false);
+    upload_planar(T, frame.transmittance);
+    upload_planar(dC, pix.dcolor);
+    upload_planar(dD, pix.ddepth);
+    if (C) upload_planar(dO, pix.dsemantics);
+    upload_planar(dK, pix.dkmap);
+    DeviceGrads dg(scene, f32);  // zeroed by the backward
     msplat_frame fr{nullptr, nullptr, nullptr, nullptr, T.p, nullptr, nullptr};
     msplat_pixel_grads pg{dC.p, dD.p, C ? dO.p : nullptr, dK.p, nullptr};
-    msplat_grads g{gpos.p, grot.p, gsc.p, gop.p, gk.p, gsh.p, C ? gsem.p : nullptr};
+    msplat_grads g = dg.abi(C);
     const msplat_scene s = ds.abi();
     const msplat_camera c = to_abi(view);
+    pt.mark("pixel-grad upload");
     rethrow(msplat_rasterize_backward(context(), &s, &c, &fr, replay.device->handle, &pg, &g));
+    pt.mark("msplat_rasterize_backward");
     GradientBuffer out;
-    grads_from_device(out, scene, gpos, grot, gsc, gop, gk, gsh, gsem);
+    dg.to_host(out, scene);
+    pt.mark("grads download");
     return out;
 }
 
