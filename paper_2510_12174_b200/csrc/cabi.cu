@@ -943,7 +943,15 @@ static msplat_status rasterize_entry(msplat_context* ctx, const msplat_scene* s,
 msplat_status msplat_rasterize(msplat_context* ctx, const msplat_scene* s, const msplat_camera* cam,
                                const msplat_render_config* cfg, const msplat_frame* f, msplat_replay* replay) {
     CTX_DEVICE_GUARD(ctx);
-    return rasterize_entry(ctx, s, cam, cfg, f, replay, true);
+    // Inside a CUDA-graph capture the call stays asynchronous (no capacity
+    // read-back, errors latched for the next synchronizing call); the replay
+    // must have been sized by an eager call first.
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (ctx) CUDA_TRY(cudaStreamIsCapturing(ctx->stream, &cs));
+    const bool capturing = cs != cudaStreamCaptureStatusNone;
+    if (capturing && (!replay || replay->inst_cap == 0 || !replay->valid))
+        return set_error(MSPLAT_ERR_RUNTIME, "rasterize: capture before any eager call with this replay");
+    return rasterize_entry(ctx, s, cam, cfg, f, replay, !capturing);
 }
 
 msplat_status msplat_estimate_normals(msplat_context* ctx, int dtype, const void* depth, const void* T,

@@ -216,6 +216,12 @@ __global__ void __launch_bounds__(kThreads, kSplit ? K6_SPLIT_MINB : 2) forward_
     uint2* const evl = a.ev_list ? a.ev_list + size_t(8) * range.x + size_t(warp) * len : nullptr;
     float* const wd = kSplit ? a.ev_w + (size_t(8) * range.x + size_t(warp) * len) * 32 : nullptr;
     uint32_t n_ev = 0, n_pairs = 0;
+    if (kSplit && int64_t(size_t(8) * range.x + size_t(warp) * len + len) * 32 > a.ev_w_cap) {
+        // a captured replay outgrew the weight rows (sized by the last eager render)
+        if (lane == 0) raise_error(a.err, kErrInstanceOverflow, int64_t(size_t(8) * range.x + size_t(warp) * len + len) * 32,
+                                   a.ev_w_cap);
+        done = true;
+    }
 
 #if K6_NEXT_PREFETCH
     uint32_t g_next = lane < len ? a.inst_gauss[range.x + lane] : 0u;
