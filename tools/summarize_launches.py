@@ -47,9 +47,18 @@ print("\n".join(out))
 # K9 = tensor-core phase A + pair-record phase B)
 traffic = {}
 for k, v in agg.items():
-    for stage, prefs in (("backward", ("backward_kernel", "backward_pairs_kernel", "order_hist_kernel", "order_scatter_kernel")), ("forward", ("forward_kernel", "forward_alpha_kernel", "forward_sem_kernel", "forward_depth_kernel")),
+    for stage, prefs in (("backward", ("backward_kernel", "backward_pairs_kernel", "order_hist_kernel", "order_scatter_kernel")), ("forward", ("forward_kernel", "forward_pairs_kernel")),
                          ("preprocess", ("preprocess_kernel",)), ("proj_bwd", ("projection_backward_kernel",))):
         if any(k.startswith(pref) for pref in prefs):
             traffic[stage] = traffic.get(stage, 0.0) + v[2] / v[0]
+# keyed by BASELINE config (bench.py reads its own config's entry; default cfg3)
+cfg = sys.argv[4] if len(sys.argv) > 4 else "cfg3"
 path = os.path.join(os.path.dirname(sys.argv[2]), "ncu_traffic.json")
-json.dump(traffic, open(path, "w"), indent=1)
+try:
+    allt = json.load(open(path))
+    if not all(isinstance(v, dict) for v in allt.values()):
+        allt = {}
+except Exception:
+    allt = {}
+allt[cfg] = traffic
+json.dump(allt, open(path, "w"), indent=1)
