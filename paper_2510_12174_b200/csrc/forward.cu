@@ -38,8 +38,14 @@ constexpr int kThreads = 256;
 #define K6_NEXT_PREFETCH 1  // next chunk ids one chunk ahead + L1 prefetch of their records: 2.05 ms vs 2.11
 #endif
 constexpr int kQueue = 64;
+// The semantics-free blend: 4-warp CTAs (half a tile) at 5 CTAs / SM = 96
+// registers, 20 warps / SM: 1.74 ms vs 1.80 with 8-warp CTAs at 3 / SM (80
+// registers, 24 warps, more spills) or 4 / SM (128 registers, 16 warps).
+#ifndef K6_SPLIT_WARPS
+#define K6_SPLIT_WARPS 4  // warps per CTA of the semantics-free variant
+#endif
 #ifndef K6_SPLIT_MINB
-#define K6_SPLIT_MINB 3  // CTAs per SM of the semantics-free variant
+#define K6_SPLIT_MINB 5  // its CTAs per SM
 #endif
 
 __host__ __device__ inline int sem_pitch(int C) { return C | 1; }  // odd pitch: conflict-free rows
@@ -65,7 +71,7 @@ struct SemTC {
 __host__ __device__ inline int sem_ntiles(int C) { return (C + 7) / 8; }
 
 template <typename Real>
-size_t forward_smem_bytes(int C) {
+size_t forward_smem_bytes(int C, int warps = 8) {
     size_t per_warp = sizeof(FwdWarpSmem<Real>);
     if (C > 0) {
         if constexpr (sizeof(Real) == 4)
@@ -73,7 +79,7 @@ size_t forward_smem_bytes(int C) {
         else
             per_warp += sizeof(Real) * 32 * size_t(sem_pitch(C));
     }
-    return 8 * per_warp + 64;
+    return size_t(warps) * per_warp + 64;
 }
 
 // W is stored per pixel row with the event index permuted (k -> 2(k&3) + k/4)
@@ -169,10 +175,17 @@ __device__ __forceinline__ void flush_depth(const ForwardArgs<Real>& a, FwdWarpS
 // (forward_split.cu, K6b), which replays the event log with the blend weights
 // this kernel writes (one 32-float row per event); nothing semantic is live
 // here.
+// A CTA covers one tile with 8 warps, or (kSplit, K6_SPLIT_WARPS = 4) half a
+// tile with 4: the warps never synchronise, so smaller CTAs only change how
+// registers and shared memory are granted per SM.
+constexpr int kSplitWarps = K6_SPLIT_WARPS;
 template <typename Real, bool kSplit>
-__global__ void __launch_bounds__(kThreads, kSplit ? K6_SPLIT_MINB : 2) forward_kernel(const __grid_constant__ ForwardArgs<Real> a) {
+__global__ void __launch_bounds__(kSplit ? 32 * kSplitWarps : kThreads, kSplit ? K6_SPLIT_MINB : 2)
+    forward_kernel(const __grid_constant__ ForwardArgs<Real> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;  // warp: the CTA's shared-memory slot
+    constexpr int kParts = kSplit ? 8 / kSplitWarps : 1;            // CTAs per tile
+    const int wq = kParts > 1 ? int(blockIdx.x % kParts) * kSplitWarps + warp : warp;  // 8x4 block of the tile
     const int C = kSplit ? 0 : a.C, pitch = sem_pitch(C);
     constexpr bool kTC = sizeof(Real) == 4;  // tensor-core semantic accumulation (FP32)
     FwdWarpSmem<Real>* ws = reinterpret_cast<FwdWarpSmem<Real>*>(smem_raw) + warp;
@@ -190,9 +203,9 @@ __global__ void __launch_bounds__(kThreads, kSplit ? K6_SPLIT_MINB : 2) forward_
     }
     int nb = 0;  // FP32: events in the open semantic batch
 
-    const int tile = blockIdx.x;
+    const int tile = kParts > 1 ? int(blockIdx.x / kParts) : int(blockIdx.x);
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    const int bx = tx * kTile + (warp & 1) * 8, by = ty * kTile + (warp >> 1) * 4;
+    const int bx = tx * kTile + (wq & 1) * 8, by = ty * kTile + (wq >> 1) * 4;
     const int x = bx + (lane & 7), y = by + (lane >> 3);
     const bool inside = x < a.W && y < a.H;
     if constexpr (kTC) {
@@ -213,12 +226,12 @@ __global__ void __launch_bounds__(kThreads, kSplit ? K6_SPLIT_MINB : 2) forward_
     const bool c0 = lane < C, c1 = lane + 32 < C;
     int qn = 0;
     unsigned long long own = 0;  // queue entries owned by this pixel
-    uint2* const evl = a.ev_list ? a.ev_list + size_t(8) * range.x + size_t(warp) * len : nullptr;
-    float* const wd = kSplit ? a.ev_w + (size_t(8) * range.x + size_t(warp) * len) * 32 : nullptr;
+    uint2* const evl = a.ev_list ? a.ev_list + size_t(8) * range.x + size_t(wq) * len : nullptr;
+    float* const wd = kSplit ? a.ev_w + (size_t(8) * range.x + size_t(wq) * len) * 32 : nullptr;
     uint32_t n_ev = 0, n_pairs = 0;
-    if (kSplit && int64_t(size_t(8) * range.x + size_t(warp) * len + len) * 32 > a.ev_w_cap) {
+    if (kSplit && int64_t(size_t(8) * range.x + size_t(wq) * len + len) * 32 > a.ev_w_cap) {
         // a captured replay outgrew the weight rows (sized by the last eager render)
-        if (lane == 0) raise_error(a.err, kErrInstanceOverflow, int64_t(size_t(8) * range.x + size_t(warp) * len + len) * 32,
+        if (lane == 0) raise_error(a.err, kErrInstanceOverflow, int64_t(size_t(8) * range.x + size_t(wq) * len + len) * 32,
                                    a.ev_w_cap);
         done = true;
     }
@@ -373,8 +386,8 @@ __global__ void __launch_bounds__(kThreads, kSplit ? K6_SPLIT_MINB : 2) forward_
         }
     }
     if (a.ev_count && lane == 0) {
-        a.ev_count[size_t(tile) * 8 + warp] = n_ev;
-        a.ev_npairs[size_t(tile) * 8 + warp] = n_pairs;
+        a.ev_count[size_t(tile) * 8 + wq] = n_ev;
+        a.ev_npairs[size_t(tile) * 8 + wq] = n_pairs;
     }
     if constexpr (kTC) {
         if (a.sem_out) {  // straight from the fragments: lane (g4, t) holds rows g4, g4 + 8 x cols 2t, 2t + 1
@@ -426,10 +439,10 @@ void launch_forward(const ForwardArgs<Real>& a, int ntiles, cudaStream_t s) {
 
 void launch_forward_blend_split(const ForwardArgs<float>& a, int ntiles, cudaStream_t s) {
     if (ntiles == 0) return;
-    const size_t smem = forward_smem_bytes<float>(0);
+    const size_t smem = forward_smem_bytes<float>(0, kSplitWarps);
     static std::atomic<unsigned long long> attr{0};
     opt_in_smem(reinterpret_cast<const void*>(forward_kernel<float, true>), attr);
-    forward_kernel<float, true><<<ntiles, kThreads, smem, s>>>(a);
+    forward_kernel<float, true><<<ntiles * (8 / kSplitWarps), 32 * kSplitWarps, smem, s>>>(a);
     count_launches(1);
 }
 
