@@ -575,8 +575,18 @@ __host__ __device__ inline int tc_stage_floats(int C) {
 __host__ __device__ inline int tc_warp_floats(int C) {
     return 32 * seed_pitch(C) + tc_stage_floats(C) + kSub * kTilePitch;
 }
+// Phase A in 4-warp CTAs at 4 / SM (the same 16 warps / SM as 8-warp CTAs at
+// 2, but CTAs retire at a finer grain at the end of the longest-first order):
+// 2.246 ms vs 2.257; 6-warp CTAs at 3 / SM (96 registers): 2.30.
+#ifndef K9A_WARPS
+#define K9A_WARPS 4  // warps per phase-A CTA (segments are independent: any CTA size works)
+#endif
+#ifndef K9A_MINB
+#define K9A_MINB (16 / K9A_WARPS)
+#endif
+constexpr int kTcWarps = K9A_WARPS;
 size_t backward_tc_smem_bytes(int C) {
-    return 8 * (sizeof(WarpSmemTC) + sizeof(float) * size_t(tc_warp_floats(C))) + 64;
+    return kTcWarps * (sizeof(WarpSmemTC) + sizeof(float) * size_t(tc_warp_floats(C))) + 64;
 }
 
 }  // namespace
@@ -629,21 +639,23 @@ __device__ __forceinline__ void stage_rows_tc(float* Fb, int sp, const AlphaRec<
 // is T_j (FS_j - (B_j + T_final bg) / T_{j+1}) (rasterizer_backward.cpp:222-232).
 // GEMM2 reads the same rows.
 template <bool kRows>
-__global__ void __launch_bounds__(kThreads, 2) backward_kernel_tc(const __grid_constant__ BackwardArgs<float> a) {
+__global__ void __launch_bounds__(32 * kTcWarps, K9A_MINB) backward_kernel_tc(const __grid_constant__ BackwardArgs<float> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int C = a.C, sp = seed_pitch(C), S = C + 4, K8 = seed_k8(C);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g4 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
     WarpSmemTC* ws = reinterpret_cast<WarpSmemTC*>(smem_raw) + warp;
     float* const warp_seed =
-        reinterpret_cast<float*>(reinterpret_cast<WarpSmemTC*>(smem_raw) + 8) + size_t(warp) * tc_warp_floats(C);
+        reinterpret_cast<float*>(reinterpret_cast<WarpSmemTC*>(smem_raw) + kTcWarps) + size_t(warp) * tc_warp_floats(C);
     float* const my_seed = warp_seed + size_t(lane) * sp;
     float* const Fb = warp_seed + size_t(32) * sp;  // [kSub][sp] F rows; then FS [kSub][36] in place
     float* const FSs = Fb;
     float* const Wb = Fb + tc_stage_floats(C);      // [kSub][36] blend weights
 
-    // this warp's (tile, 8x4 block) segment: longest-first order, or block `warp` of tile blockIdx.x
-    const int seg_i = a.work_order ? int(a.work_order[blockIdx.x * 8 + warp]) : int(blockIdx.x) * 8 + warp;
+    // this warp's (tile, 8x4 block) segment: longest-first order, or in tile order
+    const int item = int(blockIdx.x) * kTcWarps + warp;
+    if (item >= a.nseg) return;
+    const int seg_i = a.work_order ? int(a.work_order[item]) : item;
     const int tile = seg_i >> 3, wl = seg_i & 7;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     const int bx = tx * kTile + (wl & 1) * 8, by = ty * kTile + (wl >> 1) * 4;
@@ -1042,12 +1054,15 @@ void launch_backward_blend(const BackwardArgs<Real>& a, int ntiles, cudaStream_t
         backward_kernel<Real, true><<<ntiles, kThreads, backward_smem_bytes<Real>(a.C), s>>>(a);
     } else if constexpr (sizeof(Real) == 4) {
         static std::atomic<unsigned long long> attr_tc{0}, attr_rows{0};
+        BackwardArgs<float> b = reinterpret_cast<const BackwardArgs<float>&>(a);
+        b.nseg = ntiles * 8;
+        const unsigned ctas = unsigned((ntiles * 8 + kTcWarps - 1) / kTcWarps);
         if (a.ev_w) {
             opt_in_smem(reinterpret_cast<const void*>(backward_kernel_tc<true>), attr_rows);
-            backward_kernel_tc<true><<<ntiles, kThreads, backward_tc_smem_bytes(a.C), s>>>(a);
+            backward_kernel_tc<true><<<ctas, 32 * kTcWarps, backward_tc_smem_bytes(a.C), s>>>(b);
         } else {
             opt_in_smem(reinterpret_cast<const void*>(backward_kernel_tc<false>), attr_tc);
-            backward_kernel_tc<false><<<ntiles, kThreads, backward_tc_smem_bytes(a.C), s>>>(a);
+            backward_kernel_tc<false><<<ctas, 32 * kTcWarps, backward_tc_smem_bytes(a.C), s>>>(b);
         }
         backward_pairs_kernel<<<unsigned((ntiles * 8 + 7) / 8), 256, 0, s>>>(a, ntiles * 8);
         count_launches(1);

@@ -30,7 +30,6 @@ namespace msplat_cuda {
 
 namespace {
 
-constexpr int kThreads = 256;
 constexpr int kNtMax = 8;  // semantic n-tiles in registers: C <= 64
 
 
@@ -119,13 +118,23 @@ __device__ __forceinline__ void sem_batch(const PairSmem* ws, int buf, float (&a
     }
 }
 
+#ifndef K6B_WARPS
+#define K6B_WARPS 8  // warps per CTA of the semantic pass
+#endif
+#ifndef K6B_MINB
+#define K6B_MINB (16 / K6B_WARPS)
+#endif
+constexpr int kSemWarps = K6B_WARPS;
+
 // NT = ceil(C / 8) semantic n-tiles of accumulators in registers.
 template <int NT>
-__global__ void __launch_bounds__(kThreads, 2) forward_pairs_kernel(const __grid_constant__ ForwardArgs<float> a) {
+__global__ void __launch_bounds__(32 * kSemWarps, K6B_MINB) forward_pairs_kernel(const __grid_constant__ ForwardArgs<float> a) {
     extern __shared__ __align__(16) unsigned char k6b_smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     PairSmem* const ws = reinterpret_cast<PairSmem*>(k6b_smem) + warp;
-    const int seg = a.work_order ? int(a.work_order[blockIdx.x * 8 + warp]) : int(blockIdx.x) * 8 + warp;
+    const int item = int(blockIdx.x) * kSemWarps + warp;
+    if (item >= a.nseg) return;
+    const int seg = a.work_order ? int(a.work_order[item]) : item;
     const int tile = seg >> 3, wl = seg & 7;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     const int bx = tx * kTile + (wl & 1) * 8, by = ty * kTile + (wl >> 1) * 4;
@@ -207,11 +216,13 @@ void launch_forward_split(const ForwardArgs<float>& a, int ntiles, cudaStream_t 
         launch_work_order(a.ev_count, ntiles * 8, const_cast<uint32_t*>(seg_order), order_scratch, s);
         b.work_order = seg_order;
     }
-    const size_t smem = 8 * sizeof(PairSmem);
+    b.nseg = ntiles * 8;
+    const unsigned ctas = unsigned((ntiles * 8 + kSemWarps - 1) / kSemWarps);
+    const size_t smem = kSemWarps * sizeof(PairSmem);
     static std::atomic<unsigned long long> attr[kNtMax + 1];  // per instantiation, per device
 #define K6B_LAUNCH(NT_)                                                                          \
     opt_in_smem(reinterpret_cast<const void*>(forward_pairs_kernel<NT_>), attr[NT_], int(smem)); \
-    forward_pairs_kernel<NT_><<<ntiles, kThreads, smem, s>>>(b);
+    forward_pairs_kernel<NT_><<<ctas, 32 * kSemWarps, smem, s>>>(b);
     switch ((a.C + 7) / 8) {
         case 1: K6B_LAUNCH(1) break;
         case 2: K6B_LAUNCH(2) break;

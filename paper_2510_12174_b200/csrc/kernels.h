@@ -141,6 +141,7 @@ struct ForwardArgs {
     int64_t ev_w_cap;  // floats
     int sem_vec;       // semantic rows may be staged in 8-byte pieces (C even, 8-byte aligned)
     const uint32_t* work_order;
+    int nseg;          // (tile, warp) segments (set by the launcher)
     DeviceError* err;
 };
 template <typename Real>
@@ -286,6 +287,7 @@ struct BackwardArgs {
     // launch_work_order), and phase B takes segments in the same order.  Null:
     // warp w of CTA b replays block w of tile b.
     const uint32_t* work_order;
+    int nseg;  // (tile, warp) segments of the FP32 phase A (set by the launcher)
     // FP32: semantic rows may be moved in 8-byte pieces (C even and both the
     // scene's and the gradient buffer's semantic arrays 8-byte aligned).
     int sem_vec;
