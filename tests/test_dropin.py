@@ -78,3 +78,36 @@ def test_dropin_fp32_reference_tests():
         "[FAIL] dk against dL/dK=1 reproduces recorded per-gaussian weight sums",
     }
     assert set(fails) <= allowed, "\n".join(lines[-60:])
+
+
+@pytest.mark.gpu
+def test_dropin_boundary_benchmark_runs(tmp_path):
+    """tools/dropin_bench (the reference API timed with host Eigen AoS data)
+    on a small scene, in all four precision x determinism modes: same frame
+    and gradient checksum up to the precision."""
+    import json
+    import numpy as np
+    import torch
+    import paper_2510_12174_b200 as M
+    from paper_2510_12174_b200 import scenes
+    exe = os.path.join(ROOT, "tools", "_bin", "dropin_bench")
+    if not os.path.exists(exe):
+        pytest.skip("dropin_bench not built")
+    s = scenes.make_random_scene(2000, 5, 2, seed=3)
+    path = str(tmp_path / "s.ply")
+    M.save_scene_ply(path, M.Scene.from_numpy(s, dtype=torch.float32))
+    cam = scenes.simple_camera(96, 64, 60.0)
+    args = [exe, path, *(repr(float(cam[k])) for k in ("fx", "fy", "cx", "cy")), "96", "64",
+            *(repr(float(v)) for v in np.eye(3).reshape(-1)), "0.0", "0.0", "-0.5", "0", "1"]
+    recs = []
+    for prec in ("32", "64"):
+        for det in ("0", "1"):
+            r = subprocess.run(args, capture_output=True, text=True, timeout=300,
+                               env=dict(os.environ, MSPLAT_PRECISION=prec, MSPLAT_DETERMINISTIC=det))
+            assert r.returncode == 0, r.stderr
+            recs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert [x["precision"] for x in recs] == ["f32", "f32", "f64", "f64"]
+    assert [x["deterministic"] for x in recs] == [False, True, False, True]
+    c = [x["checksum"] for x in recs]
+    assert c[2] == c[3] and abs(c[0] - c[2]) <= 1e-4 * max(abs(c[2]), 1e-6), c
+    assert all(x["fwd_bwd_ms"] > 0 for x in recs)

@@ -532,3 +532,33 @@ def test_deterministic_step_is_graph_capturable(dtype):
         M.rasterizer.check_device_errors()
     finally:
         M.set_deterministic(False)
+
+
+@pytest.mark.parametrize("C", [0, 1, 8, 9, 57, 64, 65, 72])
+def test_forward_paths_across_class_counts(port, C):
+    """Both FP32 forward paths against the oracle: the split forward (blend +
+    tensor-core semantic pass, C <= 64, n-tile count a template parameter:
+    C = 1, 8, 9, 57, 64 cover NT = 1, 1, 2, 8, 8 and partial tiles) and the
+    fused kernel (C > 64); C = 0 has no semantic pass.  Then the backward on
+    top (weight-row replay after the split forward, the alpha test after the
+    fused one) against the oracle's gradients."""
+    import torch
+    import paper_2510_12174_b200 as M
+    cam = {"fx": 40.0, "fy": 36.0, "cx": 33.0, "cy": 21.0, "width": 70, "height": 45,
+           "R_c2w": scenes._rot_y(0.1) @ scenes._rot_x(-0.05), "t_c2w": np.array([-0.1, 0.05, -0.4])}
+    s = scenes.make_random_scene(400, C, 2, seed=300 + C)
+    scene, view, rc, replay, frame = gpu_forward(s, cam, BG, "float32")
+    ref = port.render(s, cam, BG)
+    got = frame_np(frame)
+    same = (got["contributors"] == ref["contributors"]) & (replay.terminus() == ref["terminus"])
+    assert 1.0 - same.mean() < 0.01
+    for k in ("color", "depth", "kmap", "transmittance"):
+        assert rel_max_err(got[k], ref[k], same) < 1e-4, k
+    if C:
+        assert rel_max_err(got["semantics"], ref["semantics"],
+                           np.broadcast_to(same[..., None], got["semantics"].shape)) < 1e-4
+    pix = scenes.pixel_grads(cam["width"], cam["height"], C, seed=9, scale=1.0)
+    g = grads_np(M.rasterize_backward(scene, view, frame, replay, torch_pix(pix, torch.float32)))
+    gref = port.backward(s, cam, hwc_pix(pix), BG)
+    for k, r in grad_parity(g, gref).items():
+        assert r["max_rel"] <= 1e-3, (k, r)
