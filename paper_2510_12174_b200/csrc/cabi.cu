@@ -195,7 +195,7 @@ struct msplat_replay {
         count_sorted, offset_sorted, inst_tile, inst_tile_alt, inst_gauss, inst_gauss_alt, tile_range,
         d_inst_count, d_inst_total32, hist, hist_scanned, scan_tiles, terminus, weight_sums, saved_means,
         saved_k, cap_center, cap_conic, cap_depth, cap_radius, cap_rgb, visible_count, ev_list, ev_count, ev_npairs,
-        pair_off, pair_n, pair_scan, pair_total, pair_rec, wq_order, wq_scratch, ev_w;
+        pair_off, pair_n, pair_scan, pair_total, pair_rec, wq_order, wq_scratch, ev_w, tile_cnt, tile_cur, inst_key, big_tiles, key_range;
     bool split_fwd = false;  // the last forward ran split: its weight rows are valid
     int64_t pair_cap = 0;  // pair-record capacity of the FP32 split backward
     uint32_t* sorted_gauss = nullptr;
@@ -207,7 +207,7 @@ struct msplat_replay {
                           &hist_scanned, &scan_tiles, &terminus, &weight_sums, &saved_means, &saved_k,
                           &cap_center, &cap_conic, &cap_depth, &cap_radius, &cap_rgb, &visible_count, &ev_list,
                           &ev_count, &ev_npairs, &pair_off, &pair_n, &pair_scan, &pair_total, &pair_rec,
-                          &wq_order, &wq_scratch, &ev_w})
+                          &wq_order, &wq_scratch, &ev_w, &tile_cnt, &tile_cur, &inst_key, &big_tiles, &key_range})
             b->release();
     }
 };
@@ -358,6 +358,7 @@ msplat_status size_replay(msplat_replay* r, int dtype, int64_t n, int C, int deg
     const size_t ic = size_t(r->inst_cap);
     CUDA_TRY(r->inst_tile.ensure(ic * 4));
     CUDA_TRY(r->inst_tile_alt.ensure(ic * 4));
+    CUDA_TRY(r->inst_key.ensure(ic * 8));
     CUDA_TRY(r->ev_list.ensure(ic * 8 * sizeof(uint2)));  // 8 warps x (position, mask) per instance
 
     CUDA_TRY(r->ev_count.ensure(size_t(tiles) * 8 * 4));
@@ -367,8 +368,12 @@ msplat_status size_replay(msplat_replay* r, int dtype, int64_t n, int C, int deg
     CUDA_TRY(r->inst_gauss.ensure(ic * 4));
     CUDA_TRY(r->inst_gauss_alt.ensure(ic * 4));
     CUDA_TRY(r->tile_range.ensure(size_t(tiles) * 8));
+    CUDA_TRY(r->tile_cnt.ensure(size_t(tiles) * 4));
+    CUDA_TRY(r->tile_cur.ensure(size_t(tiles) * 4));
+    CUDA_TRY(r->big_tiles.ensure(size_t(tiles + 1) * 4));
+    CUDA_TRY(r->key_range.ensure(16));
     CUDA_TRY(r->d_inst_count.ensure(8));
-    CUDA_TRY(r->d_inst_total32.ensure(4));
+    CUDA_TRY(r->d_inst_total32.ensure(8));
     CUDA_TRY(r->visible_count.ensure(8));
     const size_t hist = binning_scratch_elems(int64_t(nn), r->inst_cap);
     CUDA_TRY(r->hist.ensure(hist * 4));
@@ -411,6 +416,11 @@ BinningBuffers binning_view(msplat_replay* r) {
     b.tile_range = r->tile_range.as<uint2>();
     b.d_inst_count = r->d_inst_count.as<int64_t>();
     b.d_inst_total32 = r->d_inst_total32.as<uint32_t>();
+    b.tile_cnt = r->tile_cnt.as<uint32_t>();
+    b.tile_cur = r->tile_cur.as<uint32_t>();
+    b.inst_key = r->inst_key.as<uint64_t>();
+    b.big_tiles = r->big_tiles.as<uint32_t>();
+    b.key_range = r->key_range.as<unsigned long long>();
     b.hist = r->hist.as<uint32_t>();
     b.hist_scanned = r->hist_scanned.as<uint32_t>();
     b.scan_tiles = r->scan_tiles.as<uint32_t>();
@@ -429,9 +439,9 @@ msplat_status binning_with_capacity(msplat_replay* r, bool sync) {
         r->sorted_gauss = b.sorted_gauss;
         CUDA_TRY(cudaGetLastError());
         if (!sync) return MSPLAT_OK;
-        CUDA_TRY(cudaMemcpyAsync(ctx->h_u64, b.d_inst_total32, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(ctx->h_u64, b.d_inst_total32, 8, cudaMemcpyDeviceToHost, ctx->stream));
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-        const int64_t need = int64_t(*reinterpret_cast<uint32_t*>(ctx->h_u64));
+        const int64_t need = int64_t(reinterpret_cast<uint32_t*>(ctx->h_u64)[0]);
         if (need <= r->inst_cap) {
             // split FP32 forward: <= 32 compacted blend weights per event-log
             // entry (8 per instance), sized from this render's instances (a

@@ -91,7 +91,13 @@ struct BinningBuffers {
     uint2* tile_range;  // [start, end) into the sorted instance list
     // scalars (device)
     int64_t* d_inst_count;
-    uint32_t* d_inst_total32;
+    uint32_t* d_inst_total32;  // [0] instance total, [1] longest tile list (per-tile path)
+    // per-tile path: per-tile counters and cursors, per-instance depth keys,
+    // shared-memory capacity (entries) of the tile sort
+    uint32_t *tile_cnt, *tile_cur;
+    uint64_t* inst_key;     // per-instance sort items (depth-key high word, Gaussian id)
+    uint32_t* big_tiles;    // [0] = count, then the tiles whose list exceeds one CTA's register sort
+    unsigned long long* key_range;  // [0] max ~key, [1] max key over the binned Gaussians
     // scratch
     uint32_t *hist, *hist_scanned, *scan_tiles;
     DeviceError* err;

@@ -415,8 +415,9 @@ __global__ void rects_from_splats_kernel(int64_t n, const uint8_t* __restrict__ 
     tile_count[i] = uint32_t((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
     // Arbitrary doubles: map to an order-preserving unsigned key (negative
     // values flip all bits, positive set the sign bit) -- the explicit-splat
-    // entry point is not restricted to z > 0.
-    const uint64_t b = uint64_t(__double_as_longlong(depth[i]));
+    // entry point is not restricted to z > 0.  -0.0 + 0.0 = +0.0: the two
+    // zeros compare equal in the reference's comparator (index tie-break).
+    const uint64_t b = uint64_t(__double_as_longlong(depth[i] + 0.0));
     depth_key[i] = (b >> 63) ? ~b : (b | (1ull << 63));
 }
 

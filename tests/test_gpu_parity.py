@@ -337,6 +337,42 @@ def test_bin_and_sort_reference_kat():
             assert rb.tile(tx, ty) == exp
 
 
+@pytest.mark.parametrize("n", [6000, 40000])
+def test_bin_and_sort_long_lists_and_depth_ties(n):
+    """Per-tile (depth, index) order (rasterizer.cpp:25-28) on tile lists longer
+    than one CTA's register sort (2048: the persistent large-list sort; 8192:
+    its in-place global-memory network), with many exactly equal depths (index
+    tie-break), equal high words (the full-key fix-up) and negative depths."""
+    import paper_2510_12174_b200 as M
+    rng = np.random.default_rng(n)
+    W, H = 64, 48
+    cx = rng.random(n) * 80 - 8
+    cy = rng.random(n) * 60 - 6
+    rad = rng.random(n) * 30
+    dep = rng.choice(np.array([-1.5, -0.0, 0.0, 0.25, 0.5, 2.0, 1e-300, 7.0]), n) + \
+        np.where(rng.random(n) < 0.5, 0.0, rng.random(n))
+    splats = [{"center": (float(cx[i]), float(cy[i])), "radius": float(rad[i]), "sort_depth": float(dep[i])}
+              for i in range(n)]
+    x0 = np.maximum(0, np.floor(cx - rad)).astype(int)
+    x1 = np.minimum(W - 1, np.floor(cx + rad)).astype(int)
+    y0 = np.maximum(0, np.floor(cy - rad)).astype(int)
+    y1 = np.minimum(H - 1, np.floor(cy + rad)).astype(int)
+    ok = (x1 >= x0) & (y1 >= y0)
+    for _ in range(2):  # repeatable
+        rb = M.bin_and_sort(splats, W, H)
+        longest = 0
+        for ty in range(3):
+            for tx in range(4):
+                m = ok & (x0 // 16 <= tx) & (tx <= x1 // 16) & (y0 // 16 <= ty) & (ty <= y1 // 16)
+                idx = np.nonzero(m)[0]
+                # -0.0 == 0.0 for the reference's std::sort comparator
+                exp = idx[np.lexsort((idx, dep[idx] + 0.0))]
+                got = rb.tile(tx, ty)
+                longest = max(longest, len(got))
+                assert got == exp.tolist(), (tx, ty)
+        assert longest > 2048
+
+
 def test_scene_modified_since_forward_is_detected():
     import torch
     import paper_2510_12174_b200 as M
