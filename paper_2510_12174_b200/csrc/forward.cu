@@ -214,8 +214,6 @@ __global__ void __launch_bounds__(kSplit ? 32 * kSplitWarps : kThreads, kSplit ?
         if (lane == 0) ws->zoff = r.zoff;
     }
     const Real pxf = Real(x) + Real(0.5), pyf = Real(y) + Real(0.5);
-    const Real rx0 = Real(bx) + Real(0.5), rx1 = rx0 + Real(7);
-    const Real ry0 = Real(by) + Real(0.5), ry1 = ry0 + Real(3);
     const uint2 range = a.tile_range[tile];
     const int len = int(range.y - range.x);
 
@@ -240,7 +238,15 @@ __global__ void __launch_bounds__(kSplit ? 32 * kSplitWarps : kThreads, kSplit ?
     uint32_t g_next = lane < len ? a.inst_gauss[range.x + lane] : 0u;
 #endif
     for (int c = 0; c * 32 < len; ++c) {
-        if (__all_sync(0xffffffffu, done)) break;
+        // Cull against the bounding box of the block's still-active pixels: a
+        // Gaussian whose alpha-support box misses it cannot blend any pixel
+        // that is not done (saturated or outside the image).
+        const unsigned live = __ballot_sync(0xffffffffu, !done);
+        if (live == 0u) break;
+        const unsigned cols = (live | (live >> 8) | (live >> 16) | (live >> 24)) & 0xffu;
+        const int r0 = (__ffs(live) - 1) >> 3, r1 = (31 - __clz(live)) >> 3;
+        const Real rx0 = Real(bx + __ffs(cols) - 1) + Real(0.5), rx1 = Real(bx + 31 - __clz(cols)) + Real(0.5);
+        const Real ry0 = Real(by + r0) + Real(0.5), ry1 = Real(by + r1) + Real(0.5);
         const int pos = c * 32 + lane;
         bool hit = false;
 #if K6_NEXT_PREFETCH
