@@ -191,7 +191,7 @@ struct msplat_replay {
     RenderParams rp{};
     int64_t inst_cap = 0;
     bool binned_explicit = false;
-    DevBuf arec, brec, visible, clamped, depth_key, depth_key_alt, order, order_alt, tile_count, tile_rect,
+    DevBuf arec, brec, drec, visible, clamped, depth_key, depth_key_alt, order, order_alt, tile_count, tile_rect,
         count_sorted, offset_sorted, inst_tile, inst_tile_alt, inst_gauss, inst_gauss_alt, tile_range,
         d_inst_count, d_inst_total32, hist, hist_scanned, scan_tiles, terminus, weight_sums, saved_means,
         saved_k, cap_center, cap_conic, cap_depth, cap_radius, cap_rgb, visible_count, ev_list, ev_count, ev_npairs,
@@ -201,7 +201,7 @@ struct msplat_replay {
     uint32_t* sorted_gauss = nullptr;
 
     void release_all() {
-        for (DevBuf* b : {&arec, &brec, &visible, &clamped, &depth_key, &depth_key_alt, &order, &order_alt,
+        for (DevBuf* b : {&arec, &brec, &drec, &visible, &clamped, &depth_key, &depth_key_alt, &order, &order_alt,
                           &tile_count, &tile_rect, &count_sorted, &offset_sorted, &inst_tile, &inst_tile_alt,
                           &inst_gauss, &inst_gauss_alt, &tile_range, &d_inst_count, &d_inst_total32, &hist,
                           &hist_scanned, &scan_tiles, &terminus, &weight_sums, &saved_means, &saved_k,
@@ -345,6 +345,7 @@ msplat_status size_replay(msplat_replay* r, int dtype, int64_t n, int C, int deg
     if (r->inst_cap == 0) r->inst_cap = std::max<int64_t>(int64_t(1) << 20, 4 * n);
     CUDA_TRY(r->arec.ensure(nn * sizeof(AlphaRec<double>) / 8 * R));
     CUDA_TRY(r->brec.ensure(nn * 32 * R));
+    if (dtype != MSPLAT_F64) CUDA_TRY(r->drec.ensure(nn * sizeof(DepthRec)));
     CUDA_TRY(r->visible.ensure(nn));
     CUDA_TRY(r->clamped.ensure(nn));
     CUDA_TRY(r->depth_key.ensure(nn * 8));
@@ -487,6 +488,7 @@ PreprocessArgs<Real> preprocess_args(msplat_replay* r, const msplat_scene* s, co
     a.clamped_bits = r->clamped.as<uint8_t>();
     a.arec = r->arec.as<AlphaRec<Real>>();
     a.brec = r->brec.as<BlendRec<Real>>();
+    a.drec = sizeof(Real) == 4 ? r->drec.as<DepthRec>() : nullptr;
     if (r->capture & 1) {
         a.cap_center = r->cap_center.as<double>();
         a.cap_conic = r->cap_conic.as<double>();
@@ -531,6 +533,7 @@ msplat_status rasterize_impl(msplat_context* ctx, const msplat_scene* s, const m
     a.inst_gauss = r->sorted_gauss;
     a.arec = r->arec.as<AlphaRec<Real>>();
     a.brec = r->brec.as<BlendRec<Real>>();
+    a.drec = sizeof(Real) == 4 ? r->drec.as<DepthRec>() : nullptr;
     a.semantics = static_cast<const Real*>(s->semantics);
     a.raw = RawParams<Real>{static_cast<const Real*>(s->means), static_cast<const Real*>(s->quats),
                             static_cast<const Real*>(s->log_scales), cfg->sigma_scale};

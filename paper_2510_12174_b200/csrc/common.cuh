@@ -110,6 +110,28 @@ struct __align__(16) BlendRec {  // 128 B (FP32): eight 16-byte stores
     Real vl[3];       // v_l = R^T (o - mu), unscaled local camera offset (per view)
 };
 
+// FP32 forward depth of a blended pair (K6's depth flush), per Gaussian and
+// view: intersect (core/src/geometry.cpp:37-68) rewritten as quadratic forms
+// in the pixel offset (dx, dy) from the projected centre (the AlphaRec's
+// cx, cy).  With the unnormalised ray d~ = R_c2w (p~ = ((px-cx)/fx,
+// (py-cy)/fy, 1)), m = M d~ (M = diag(1/axes) R^T) and v_s:
+//   a~ = |m|^2            = A0 + A1 dx + A2 dy + A3 dx^2 + A4 dx dy + A5 dy^2
+//   h  = v_s . m          = H0 + H1 dx + H2 dy
+//   disc/4 = |m|^2 - |v_s x m|^2 (the Lagrange form of h^2 - a~ c)
+//                         = E0 + E1 dx + E2 dy + E3 dx^2 + E4 dx dy + E5 dy^2
+// hit <=> disc >= 0 and t = -h / a~ > 0, and the midpoint depth is
+// zoff - h / a~ (d~ has camera z = 1).  The coefficients are computed in
+// FP64 by K1 about the centre, so the FP32 evaluation is well conditioned;
+// decisions within 1e-5 of the terms' magnitude are re-taken in FP64 exactly
+// as the reference computes them (intersect_fp64).  A degenerate splat
+// (axis < 1e-8) has E = (-1, 0, ...): never a hit.
+struct __align__(16) DepthRec {  // 64 B
+    float E[6];
+    float H[3];
+    float zc;  // camera-z of the centre: the no-hit depth
+    float A[6];
+};
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 }  // namespace msplat_cuda

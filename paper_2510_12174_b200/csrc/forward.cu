@@ -53,13 +53,13 @@ __host__ __device__ inline int sem_pitch(int C) { return C | 1; }  // odd pitch:
 template <typename Real>
 struct FwdWarpSmem {
     AlphaRec<Real> rec[32];
-    float4 ray[32];  // FP32: the block's pixel rays (cached_ray)
-    float zoff;
+    float zoff;  // FP32: the camera's z offset (midpoint depth = zoff - h / a~)
     uint32_t gid[32];
     uint32_t q_lane[kQueue];
     uint32_t q_gid[kQueue];
     Real q_w[kQueue];
     Real q_wd[kQueue];
+    float q_dx[kQueue], q_dy[kQueue];  // FP32: the pixel's offset from the splat centre (DepthRec)
 };
 
 // FP32 semantic tiles: per warp W[32 px][8 ev] (1 KB), the batch's Gaussian ids,
@@ -147,16 +147,37 @@ __device__ __forceinline__ void flush_depth(const ForwardArgs<Real>& a, FwdWarpS
     if (lane < n) {
         const int L = int(ws->q_lane[lane]);
         const uint32_t g = ws->q_gid[lane];
-        const BlendRec<Real>& br = a.brec[g];
         const int xL = bx + (L & 7), yL = by + (L >> 3);
-        PixelRay<Real> ray;
-        if constexpr (sizeof(Real) == 4)
-            ray = cached_ray(ws->ray[L], ws->zoff, xL, yL);
-        else
-            ray = make_ray<Real>(a.cam, xL, yL);
-        const HitEval<Real> h = intersect<Real>(br, ray, a.cam, a.raw, g);
-        const Real d = !h.hit ? br.zc
-                              : (h.depth_fp64 >= Real(0) ? h.depth_fp64 : midpoint_depth<Real>(a.cam, ray, h.t_mid));
+        Real d;
+        if constexpr (sizeof(Real) == 4) {
+            // the quadratic forms of DepthRec (common.cuh) at this pixel's offset
+            const float4* const q4 = reinterpret_cast<const float4*>(a.drec + g);
+            const float4 e0 = q4[0], e1 = q4[1], e2 = q4[2], e3 = q4[3];  // E0..3 | E4 E5 H0 H1 | H2 zc A0 A1 | A2..5
+            const float dx = ws->q_dx[lane], dy = ws->q_dy[lane];
+            const float xx = dx * dx, xy = dx * dy, yy = dy * dy;
+            const float t1 = e0.y * dx, t2 = e0.z * dy, t3 = e0.w * xx, t4 = e1.x * xy, t5 = e1.y * yy;
+            const float disc = ((e0.x + t1) + (t2 + t3)) + (t4 + t5);
+            const float sdisc = ((fabsf(e0.x) + fabsf(t1)) + (fabsf(t2) + fabsf(t3))) + (fabsf(t4) + fabsf(t5));
+            const float u1 = e1.w * dx, u2 = e2.x * dy;
+            const float h = e1.z + u1 + u2;
+            const float sh = fabsf(e1.z) + fabsf(u1) + fabsf(u2);
+            if (fabsf(disc) <= 1e-5f * sdisc || fabsf(h) <= 1e-5f * sh) {  // near a decision boundary
+                double t, aa, bb, ds[3], dep;
+                const bool ok = intersect_fp64<float>(a.cam, a.raw, g, float(xL) + 0.5f, float(yL) + 0.5f, &t, &aa,
+                                                      &bb, ds, &dep);
+                d = ok ? float(dep) : e2.y;
+            } else if (disc >= 0.f && h < 0.f) {
+                const float at = ((e2.z + e2.w * dx) + (e3.x * dy + e3.y * xx)) + (e3.z * xy + e3.w * yy);
+                d = ws->zoff - __fdividef(h, at);
+            } else {
+                d = e2.y;
+            }
+        } else {
+            const BlendRec<Real>& br = a.brec[g];
+            const PixelRay<Real> ray = make_ray<Real>(a.cam, xL, yL);
+            const HitEval<Real> h = intersect<Real>(br, ray, a.cam, a.raw, g);
+            d = !h.hit ? br.zc : (h.depth_fp64 >= Real(0) ? h.depth_fp64 : midpoint_depth<Real>(a.cam, ray, h.t_mid));
+        }
         if (!isfinite(d)) raise_error(a.err, kErrNonFiniteBlend, (long long)yL * a.W + xL, g);
         ws->q_wd[lane] = ws->q_w[lane] * d;
     }
@@ -209,9 +230,7 @@ __global__ void __launch_bounds__(kSplit ? 32 * kSplitWarps : kThreads, kSplit ?
     const int x = bx + (lane & 7), y = by + (lane >> 3);
     const bool inside = x < a.W && y < a.H;
     if constexpr (kTC) {
-        const PixelRay<Real> r = make_ray<Real>(a.cam, x, y);
-        ws->ray[lane] = ray_cache_entry(r);
-        if (lane == 0) ws->zoff = r.zoff;
+        if (lane == 0) ws->zoff = make_ray<Real>(a.cam, x, y).zoff;
     }
     const Real pxf = Real(x) + Real(0.5), pyf = Real(y) + Real(0.5);
     const uint2 range = a.tile_range[tile];
@@ -265,7 +284,12 @@ __global__ void __launch_bounds__(kSplit ? 32 * kSplitWarps : kThreads, kSplit ?
             ws->rec[lane] = r;
             ws->gid[lane] = g;
             hit = !(r.bx1 < rx0 || r.bx0 > rx1 || r.by1 < ry0 || r.by0 > ry1);
-            if (hit) asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(a.brec + g)));
+            if (hit) {
+                if constexpr (kTC)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(a.drec + g)));
+                else
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(a.brec + g)));
+            }
         }
         unsigned bits = __ballot_sync(0xffffffffu, hit);
         __syncwarp();
@@ -308,6 +332,10 @@ __global__ void __launch_bounds__(kSplit ? 32 * kSplitWarps : kThreads, kSplit ?
                 ws->q_lane[e] = uint32_t(lane);
                 ws->q_gid[e] = g;
                 ws->q_w[e] = w;
+                if constexpr (kTC) {
+                    ws->q_dx[e] = float(ae.dx);
+                    ws->q_dy[e] = float(ae.dy);
+                }
                 T *= (Real(1) - ae.alpha);
                 ++count;
                 last = c * 32 + slot + 1;
@@ -378,6 +406,10 @@ __global__ void __launch_bounds__(kSplit ? 32 * kSplitWarps : kThreads, kSplit ?
                     ws->q_lane[lane] = ws->q_lane[32 + lane];
                     ws->q_gid[lane] = ws->q_gid[32 + lane];
                     ws->q_w[lane] = ws->q_w[32 + lane];
+                    if constexpr (kTC) {
+                        ws->q_dx[lane] = ws->q_dx[32 + lane];
+                        ws->q_dy[lane] = ws->q_dy[32 + lane];
+                    }
                 }
                 qn = rest;
                 __syncwarp();

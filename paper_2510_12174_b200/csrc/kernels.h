@@ -63,6 +63,7 @@ struct PreprocessArgs {
     uint8_t* clamped_bits;
     AlphaRec<Real>* arec;
     BlendRec<Real>* brec;
+    DepthRec* drec;  // FP32 only (the forward's depth flush); may be null
     double *cap_center, *cap_conic, *cap_depth, *cap_radius, *cap_rgb;  // optional
     unsigned long long* visible_count;
     DeviceError* err;
@@ -125,6 +126,7 @@ struct ForwardArgs {
     const uint32_t* inst_gauss;
     const AlphaRec<Real>* arec;
     const BlendRec<Real>* brec;
+    const DepthRec* drec;   // FP32: the depth flush's quadratic forms
     const Real* semantics;  // [n][C] scene parameters
     RawParams<Real> raw;    // means/quats/log_scales for the FP64 re-decision
     Real *color, *depth, *sem_out, *kmap, *T;  // planar outputs (T required)

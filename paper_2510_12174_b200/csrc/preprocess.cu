@@ -30,6 +30,11 @@ __device__ __forceinline__ double dot3(const double* a, const double* b) {
     s += a[2] * b[2];
     return s;
 }
+__device__ __forceinline__ void cross3(const double* a, const double* b, double* o) {
+    o[0] = a[1] * b[2] - a[2] * b[1];
+    o[1] = a[2] * b[0] - a[0] * b[2];
+    o[2] = a[0] * b[1] - a[1] * b[0];
+}
 
 // x86 cvttsd2si semantics of the reference's int(std::floor(v)): NaN and
 // out-of-range values become INT_MIN (rasterizer.cpp:32-35 on this platform).
@@ -365,6 +370,54 @@ __global__ void __launch_bounds__(kPreThreads, K1_MINB) preprocess_kernel(const 
     br.hit_ok = Real(amin < kDegenerateScale ? 0 : 1);
     for (int j = 0; j < 4; ++j) br.q[j] = Real(q[j]);
     a.brec[i] = br;
+
+    if constexpr (sizeof(Real) == 4) {
+        if (a.drec) {  // DepthRec (common.cuh): the forward depth as quadratic forms about the centre
+            DepthRec dr;
+            dr.zc = float(z);
+            if (amin < kDegenerateScale) {
+                for (int j = 0; j < 6; ++j) dr.E[j] = dr.A[j] = 0.f;
+                for (int j = 0; j < 3; ++j) dr.H[j] = 0.f;
+                dr.E[0] = -1.f;
+                dr.A[0] = 1.f;
+            } else {
+                const double u0 = double(float(cxp)), v0 = double(float(cyp));  // the AlphaRec centre
+                const double ifx = 1.0 / c.fx, ify = 1.0 / c.fy;
+                const double p0[2] = {(u0 - c.cx) * ifx, (v0 - c.cy) * ify};
+                double m0[3], mx[3], my[3];
+#pragma unroll 1
+                for (int j = 0; j < 3; ++j) {
+                    double mc[3];  // row j of M R_c2w
+                    const double ia = 1.0 / axes[j];
+                    for (int k2 = 0; k2 < 3; ++k2) {
+                        double t = R[0 * 3 + j] * c.Rc2w[0 * 3 + k2];
+                        t += R[1 * 3 + j] * c.Rc2w[1 * 3 + k2];
+                        t += R[2 * 3 + j] * c.Rc2w[2 * 3 + k2];
+                        mc[k2] = t * ia;
+                    }
+                    m0[j] = mc[0] * p0[0] + mc[1] * p0[1] + mc[2];
+                    mx[j] = mc[0] * ifx;
+                    my[j] = mc[1] * ify;
+                }
+                double w0[3], wx[3], wy[3];
+                cross3(vs, m0, w0);
+                cross3(vs, mx, wx);
+                cross3(vs, my, wy);
+                const double A[6] = {dot3(m0, m0), 2.0 * dot3(m0, mx), 2.0 * dot3(m0, my),
+                                     dot3(mx, mx), 2.0 * dot3(mx, my), dot3(my, my)};
+                const double W2[6] = {dot3(w0, w0), 2.0 * dot3(w0, wx), 2.0 * dot3(w0, wy),
+                                      dot3(wx, wx), 2.0 * dot3(wx, wy), dot3(wy, wy)};
+                for (int j = 0; j < 6; ++j) {
+                    dr.A[j] = float(A[j]);
+                    dr.E[j] = float(A[j] - W2[j]);
+                }
+                dr.H[0] = float(dot3(vs, m0));
+                dr.H[1] = float(dot3(vs, mx));
+                dr.H[2] = float(dot3(vs, my));
+            }
+            a.drec[i] = dr;
+        }
+    }
 
     a.clamped_bits[i] = uint8_t(clamped[0] | (clamped[1] << 1) | (clamped[2] << 2));
     if (a.cap_center) {  // replay capture for parity checks (msplat_replay_splats)
