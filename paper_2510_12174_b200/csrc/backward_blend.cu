@@ -408,15 +408,15 @@ __global__ void __launch_bounds__(kThreads, 2) backward_kernel(const __grid_cons
     // fetched in parallel; no culling or alpha test of non-blending pairs.
     const unsigned act_mask = __ballot_sync(0xffffffffu, term > 0);
     const uint32_t nev = a.ev_count[size_t(tile) * 8 + warp];
-    const uint2* const evl = a.ev_list + size_t(8) * list0 + size_t(warp) * (range.y - list0);
+    const uint4* const evl = a.ev_list + size_t(8) * list0 + size_t(warp) * (range.y - list0);
 
     for (int cb = int(nev) - 1; cb >= 0; cb -= 32) {
         __syncwarp();  // the previous batch's records are no longer read
         {
             const int e = cb - lane;
             if (e >= 0) {
-                const uint2 ev = evl[e];
-                const uint32_t g = a.inst_gauss[list0 + ev.x];
+                const uint4 ev = evl[e];
+                const uint32_t g = ev.z;
                 ws->rec[lane] = a.arec[g];
                 ws->gid[lane] = g;
                 ws->emask[lane] = ev.y & act_mask;
@@ -719,13 +719,13 @@ __global__ void __launch_bounds__(32 * kTcWarps, K9A_MINB) backward_kernel_tc(co
     const uint32_t list0 = range.x;
     const uint32_t nev = a.ev_count[seg];
     const size_t ev0 = size_t(8) * list0 + size_t(wl) * (range.y - list0);  // this segment's event-log region
-    const uint2* const evl = a.ev_list + ev0;
+    const uint4* const evl = a.ev_list + ev0;
     const float* const wrows = kRows ? a.ev_w + ev0 * 32 : nullptr;
     const int mtiles2 = (S + 15) / 16;  // GEMM2 channel tiles
     if (bad_mask) {  // error path only (warp-uniform)
         for (int e = lane; e < int(nev); e += 32) {
-            const uint2 ev = evl[e];
-            if (ev.y & bad_mask) raise_error_ordered(a.err, kErrNonFiniteGrad, a.inst_gauss[list0 + ev.x]);
+            const uint4 ev = evl[e];
+            if (ev.y & bad_mask) raise_error_ordered(a.err, kErrNonFiniteGrad, ev.z);
         }
     }
     int qn = 0;
@@ -738,8 +738,8 @@ __global__ void __launch_bounds__(32 * kTcWarps, K9A_MINB) backward_kernel_tc(co
     // into L1, so only the first sub-batch waits on memory.
     uint32_t nx_gid = 0u, nx_mask = 0u;
     if (int(nev) - 1 - lane >= 0) {
-        const uint2 ev = evl[int(nev) - 1 - lane];
-        nx_gid = a.inst_gauss[list0 + ev.x];
+        const uint4 ev = evl[int(nev) - 1 - lane];
+        nx_gid = ev.z;
         nx_mask = ev.y & act_mask;
     }
 #endif
@@ -757,16 +757,16 @@ __global__ void __launch_bounds__(32 * kTcWarps, K9A_MINB) backward_kernel_tc(co
             if (!kRows) asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(a.arec + g)));
         }
         if (cb - 32 - lane >= 0) {
-            const uint2 ev = evl[cb - 32 - lane];
-            nx_gid = a.inst_gauss[list0 + ev.x];
+            const uint4 ev = evl[cb - 32 - lane];
+            nx_gid = ev.z;
             nx_mask = ev.y & act_mask;
         }
 #else
         {
             const int e = cb - lane;
             if (e >= 0) {
-                const uint2 ev = evl[e];
-                ws->gid[lane] = a.inst_gauss[list0 + ev.x];
+                const uint4 ev = evl[e];
+                ws->gid[lane] = ev.z;
                 ws->emask[lane] = ev.y & act_mask;
             }
         }

@@ -360,7 +360,7 @@ msplat_status size_replay(msplat_replay* r, int dtype, int64_t n, int C, int deg
     CUDA_TRY(r->inst_tile.ensure(ic * 4));
     CUDA_TRY(r->inst_tile_alt.ensure(ic * 4));
     CUDA_TRY(r->inst_key.ensure(ic * 8));
-    CUDA_TRY(r->ev_list.ensure(ic * 8 * sizeof(uint2)));  // 8 warps x (position, mask) per instance
+    CUDA_TRY(r->ev_list.ensure(ic * 8 * sizeof(uint4)));  // 8 warps x (position, mask, id) per instance
 
     CUDA_TRY(r->ev_count.ensure(size_t(tiles) * 8 * 4));
     CUDA_TRY(r->ev_npairs.ensure(size_t(tiles) * 8 * 4));
@@ -545,7 +545,7 @@ msplat_status rasterize_impl(msplat_context* ctx, const msplat_scene* s, const m
     a.contributors = f->contributors;
     a.terminus = r->terminus.as<int32_t>();
     a.weight_sums = (r->capture & 2) ? r->weight_sums.as<Real>() : nullptr;
-    a.ev_list = r->ev_list.as<uint2>();
+    a.ev_list = r->ev_list.as<uint4>();
     a.ev_count = r->ev_count.as<uint32_t>();
     a.ev_npairs = r->ev_npairs.as<uint32_t>();
     a.err = ctx->d_err;
@@ -634,7 +634,7 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
     a.semantics = static_cast<const Real*>(s->semantics);
     a.raw = RawParams<Real>{static_cast<const Real*>(s->means), static_cast<const Real*>(s->quats),
                             static_cast<const Real*>(s->log_scales), r->rp.sigma_scale};
-    a.ev_list = r->ev_list.as<uint2>();
+    a.ev_list = r->ev_list.as<uint4>();
     a.ev_count = r->ev_count.as<uint32_t>();
     a.T_final = static_cast<const Real*>(f->transmittance);
     a.terminus = r->terminus.as<int32_t>();

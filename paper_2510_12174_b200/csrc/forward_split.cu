@@ -141,7 +141,6 @@ __global__ void __launch_bounds__(32 * kSemWarps, K6B_MINB) forward_pairs_kernel
     const int C = a.C;
     const uint2 range = a.tile_range[tile];
     const size_t ev0 = size_t(8) * range.x + size_t(wl) * (range.y - range.x);
-    const uint2* const evl = a.ev_list + ev0;
     const float* const wrows = a.ev_w + ev0 * 32;
     const int n_ev = int(a.ev_count[seg]);
     const int nbatch = (n_ev + 7) / 8;
@@ -156,9 +155,10 @@ __global__ void __launch_bounds__(32 * kSemWarps, K6B_MINB) forward_pairs_kernel
 
     // ids of batch b are fetched at iteration b - 2 (lanes < 8), stored and
     // staged at iteration b - 1, consumed at iteration b
+    const uint4* const evl = a.ev_list + ev0;  // the blend logs each event's Gaussian id
     auto fetch_gid = [&](int b) -> uint32_t {
         const int e = 8 * b + lane;
-        return (lane < 8 && e < n_ev) ? a.inst_gauss[range.x + evl[e].x] : 0u;
+        return (lane < 8 && e < n_ev) ? evl[e].z : 0u;
     };
     uint32_t g_next = 0u;  // ids of batch b + 1
     if (nbatch > 0) {

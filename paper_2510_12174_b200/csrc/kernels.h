@@ -137,7 +137,7 @@ struct ForwardArgs {
     // in which some lane blended, front to back, as (list position, lane mask),
     // in the region [8 * range.x + warp * len, + len) of a buffer of 8 I
     // entries; ev_count[tile * 8 + warp] = number of events.
-    uint2* ev_list;
+    uint4* ev_list;    // (list position, lane mask, Gaussian id, 0)
     uint32_t* ev_count;
     uint32_t* ev_npairs;  // blended pairs per (tile, warp): the backward's pair-record segments
     // FP32 split forward (forward_split.cu): per event one row of 32 blend
@@ -263,7 +263,7 @@ struct BackwardArgs {
     const BlendRec<Real>* brec;
     const Real* semantics;
     RawParams<Real> raw;
-    const uint2* ev_list;     // the forward's blend-event log (ForwardArgs::ev_list)
+    const uint4* ev_list;     // the forward's blend-event log (ForwardArgs::ev_list)
     const uint32_t* ev_count;
     // FP32 split backward: per-(tile, warp) pair-record segments written by the
     // tensor-core phase A and consumed by the phase-B kernel: one 16-byte
