@@ -60,6 +60,8 @@ struct DevBuf {
     size_t bytes = 0;
     cudaError_t ensure(size_t want) {
         if (want <= bytes) return cudaSuccess;
+        if (const char* e = std::getenv("MSPLAT_DEBUG_CAPTURE"); e && e[0] == '1')
+            std::fprintf(stderr, "[msplat debug] DevBuf grow %zu -> %zu\n", bytes, want);
         if (p) cudaFree(p);
         p = nullptr;
         bytes = 0;
@@ -116,13 +118,30 @@ struct StageTimer {
         else
             cudaEventRecord(e, s);
     }
+    // MSPLAT_DEBUG_CAPTURE=1: report, at every stage boundary, a capture
+    // that has been invalidated or a pending launch error (debugging aid).
+    static void debug_check(int stage, const char* where, cudaStream_t s) {
+        static const bool on = [] {
+            const char* e = std::getenv("MSPLAT_DEBUG_CAPTURE");
+            return e && e[0] == '1';
+        }();
+        if (!on) return;
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        const cudaError_t e1 = cudaStreamIsCapturing(s, &cs);
+        const cudaError_t e2 = cudaPeekAtLastError();
+        if (cs == cudaStreamCaptureStatusInvalidated || e1 != cudaSuccess || e2 != cudaSuccess)
+            std::fprintf(stderr, "[msplat debug] stage %d %s: capture status %d, %s / %s\n", stage, where, int(cs),
+                         cudaGetErrorString(e1), cudaGetErrorString(e2));
+    }
     void begin(int stage, cudaStream_t s) {
+        debug_check(stage, "begin", s);
         if (!enabled) return;
         open_stage = stage;
         open_ev = next();
         record(open_ev, s);
     }
     void end(cudaStream_t s) {
+        debug_check(open_stage, "end", s);
         if (!enabled || open_stage < 0) return;
         cudaEvent_t e = next();
         record(e, s);
@@ -156,7 +175,21 @@ struct StageTimer {
 }  // namespace
 
 namespace msplat_cuda {
-void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+void count_launches(int n) {
+    g_launches.fetch_add(n, std::memory_order_relaxed);
+    // MSPLAT_DEBUG_CAPTURE=1: report launch errors as they happen (inside a
+    // graph capture they only surface at the end of the capture otherwise)
+    static const bool dbg = [] {
+        const char* e = std::getenv("MSPLAT_DEBUG_CAPTURE");
+        return e && e[0] == '1';
+    }();
+    if (dbg) {
+        const cudaError_t e = cudaPeekAtLastError();
+        if (e != cudaSuccess)
+            std::fprintf(stderr, "[msplat debug] launch error after launch #%lld: %s\n", (long long)g_launches.load(),
+                         cudaGetErrorString(e));
+    }
+}
 }  // namespace msplat_cuda
 
 struct msplat_context {

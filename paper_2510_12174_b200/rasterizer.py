@@ -321,6 +321,22 @@ def param_layout(n: int, C: int, deg: int):
 
 
 # ---------------------------------------------------------------- context
+_deferred_replays: list = []
+
+
+def _capturing() -> bool:
+    try:
+        return bool(torch.cuda.is_current_stream_capturing())
+    except Exception:
+        return False
+
+
+def _release_deferred() -> None:
+    """Destroys replays whose finalizer ran during a CUDA-graph capture."""
+    while _deferred_replays and not _capturing():
+        _lib.lib().msplat_replay_destroy(_deferred_replays.pop())
+
+
 class _Context:
     """One msplat_context per (device, lane); follows torch's current stream.
     Lanes are independent contexts (own scratch and error word) so that
@@ -349,6 +365,8 @@ class _Context:
         if c is None:
             c = cls._per_device[(dev, lane)] = _Context(dev)
         check(_lib.lib().msplat_context_set_stream(c.h, ct.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+        if _deferred_replays:
+            _release_deferred()
         return c
 
     @classmethod
@@ -380,9 +398,16 @@ class ReplayState:
         self.width = self.height = 0
 
     def __del__(self):
+        # Freeing device memory (cudaFree) inside a CUDA-graph capture would
+        # invalidate the capture, and the garbage collector may run here at
+        # any point: during a capture the handle is parked and released by
+        # the next non-capturing ReplayState / context call.
         try:
             if getattr(self, "h", None):
-                _lib.lib().msplat_replay_destroy(self.h)
+                if _capturing():
+                    _deferred_replays.append(self.h)
+                else:
+                    _lib.lib().msplat_replay_destroy(self.h)
                 self.h = None
         except Exception:
             pass
