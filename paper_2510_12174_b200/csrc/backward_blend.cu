@@ -668,31 +668,40 @@ __global__ void __launch_bounds__(32 * kTcWarps, K9A_MINB) backward_kernel_tc(co
     bool any = false;
     for (int ch = 0; ch < sp; ++ch) my_seed[ch] = 0.f;
     for (int i = lane; i < tc_stage_floats(C) + kSub * kTilePitch; i += 32) Fb[i] = 0.f;
-    if (inside) {
-        term = a.terminus[p];
-        T_final = a.T_final[p];
-        dD = a.ddepth[p];
-        for (int ch = 0; ch < 3; ++ch) {
-            my_seed[ch] = a.dcolor[ch * HW + p];
-            any |= my_seed[ch] != 0.f;
-        }
-        my_seed[3] = a.dkmap[p];
-        any |= my_seed[3] != 0.f || dD != 0.f;
-        for (int ch = 0; ch < C; ++ch) {
-            my_seed[4 + ch] = a.dsem[size_t(ch) * HW + p];
-            any |= my_seed[4 + ch] != 0.f;
-        }
-    }
-    // rasterize_backward.cpp:156-171: nothing to do without blends or seeds.
-    if (!(inside && term > 0 && any)) term = 0;
     // Non-finite seeds (an error path): check_finite (scene.cpp:97-106) then
     // names the lowest primitive blending at such a pixel.  They are zeroed
     // for the tensor-core products (0 * inf in another event's column would
     // spread NaN to primitives that never touch the pixel) and every primitive
     // the forward blended at such a pixel is reported (a pass over the event
     // log, off the hot loop), so the named primitive is the reference's.
-    bool bad = !isfinite(dD);
-    for (int ch = 0; ch < S; ++ch) bad |= !isfinite(my_seed[ch]);
+    bool bad = false;
+    if (inside) {
+        term = a.terminus[p];
+        T_final = a.T_final[p];
+        dD = a.ddepth[p];
+        const float s0 = a.dcolor[p], s1 = a.dcolor[HW + p], s2 = a.dcolor[2 * HW + p], s3 = a.dkmap[p];
+        my_seed[0] = s0;
+        my_seed[1] = s1;
+        my_seed[2] = s2;
+        my_seed[3] = s3;
+        any = s0 != 0.f || s1 != 0.f || s2 != 0.f || s3 != 0.f || dD != 0.f;
+        bad = !isfinite(s0) || !isfinite(s1) || !isfinite(s2) || !isfinite(s3) || !isfinite(dD);
+        // the semantic seed planes straight into the pixel's shared row, all in
+        // flight at once (cp.async: no register staging)
+        for (int ch = 0; ch < C; ++ch)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(unsigned(__cvta_generic_to_shared(
+                             my_seed + 4 + ch))),
+                         "l"(a.dsem + size_t(ch) * HW + p)
+                         : "memory");
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+        for (int ch = 0; ch < C; ++ch) {
+            const float v = my_seed[4 + ch];
+            any |= v != 0.f;
+            bad |= !isfinite(v);
+        }
+    }
+    // rasterize_backward.cpp:156-171: nothing to do without blends or seeds.
+    if (!(inside && term > 0 && any)) term = 0;
     if (bad) {
         for (int ch = 0; ch < sp; ++ch) my_seed[ch] = 0.f;
         dD = 0.f;
