@@ -84,9 +84,57 @@ __device__ __forceinline__ bool projection_backward_one(const ProjBackwardArgs<R
     // K9's per-pair sums (acc16 row): opacity, position, rotation, scale
     const Real* A16 = a.acc16 + size_t(i) * 16;
     go += A16[0];
-    for (int k = 0; k < 3; ++k) gp[k] += A16[6 + k];
-    for (int k = 0; k < 4; ++k) gr[k] += A16[9 + k];
-    for (int k = 0; k < 3; ++k) gs[k] += A16[13 + k];
+    if (a.depth_moments) {
+        // The FP32 phase B's depth moments (backward_blend.cu depth_moments):
+        // dposition = Sigma^-1 R_c2w u + miss * z_cam, dL/dR = S R D,
+        // dscale_k = -sigma (R^T S R)_kk / a_k^3 with S = R_c2w S_c R_c2w^T
+        // (rotations and diagonal scalings only: well conditioned in FP32).
+        float R[9], ia2[3], dR[9];
+        {
+            const float w = float(u[0]), x = float(u[1]), y = float(u[2]), z = float(u[3]);
+            R[0] = 1 - 2 * (y * y + z * z); R[1] = 2 * (x * y - w * z); R[2] = 2 * (x * z + w * y);
+            R[3] = 2 * (x * y + w * z); R[4] = 1 - 2 * (x * x + z * z); R[5] = 2 * (y * z - w * x);
+            R[6] = 2 * (x * z - w * y); R[7] = 2 * (y * z + w * x); R[8] = 1 - 2 * (x * x + y * y);
+        }
+        float sig_a3[3];
+        for (int k = 0; k < 3; ++k) {
+            const float ak = float(a.sigma) * float(s[k]);
+            ia2[k] = 1.f / (ak * ak);
+            sig_a3[k] = float(a.sigma) * ia2[k] / ak;
+        }
+        const float Sc[9] = {float(A16[9]), float(A16[12]), float(A16[13]), float(A16[12]), float(A16[10]),
+                             float(A16[14]), float(A16[13]), float(A16[14]), float(A16[11])};
+        float Mc[9];  // camera -> world
+        for (int k = 0; k < 9; ++k) Mc[k] = float(c.Rc2w[k]);
+        float uw[3], RtM[9], B[9];
+        for (int r = 0; r < 3; ++r)
+            uw[r] = Mc[r * 3] * float(A16[6]) + Mc[r * 3 + 1] * float(A16[7]) + Mc[r * 3 + 2] * float(A16[8]);
+        // R^T S R = (R^T Mc) S_c (R^T Mc)^T; S R = Mc S_c (R^T Mc)^T
+        for (int r = 0; r < 3; ++r)
+            for (int k = 0; k < 3; ++k) RtM[r * 3 + k] = R[r] * Mc[k] + R[3 + r] * Mc[3 + k] + R[6 + r] * Mc[6 + k];
+        for (int r = 0; r < 3; ++r)  // B = S_c (R^T Mc)^T
+            for (int k = 0; k < 3; ++k)
+                B[r * 3 + k] = Sc[r * 3] * RtM[k * 3] + Sc[r * 3 + 1] * RtM[k * 3 + 1] + Sc[r * 3 + 2] * RtM[k * 3 + 2];
+        const float miss = float(A16[15]);
+        float Rtu[3];
+        for (int k = 0; k < 3; ++k) Rtu[k] = (R[k] * uw[0] + R[3 + k] * uw[1] + R[6 + k] * uw[2]) * ia2[k];
+        for (int r = 0; r < 3; ++r)
+            gp[r] += Real(R[r * 3] * Rtu[0] + R[r * 3 + 1] * Rtu[1] + R[r * 3 + 2] * Rtu[2] + miss * float(c.Rw2c[6 + r]));
+        for (int r = 0; r < 3; ++r)
+            for (int k = 0; k < 3; ++k)
+                dR[r * 3 + k] = (Mc[r * 3] * B[k] + Mc[r * 3 + 1] * B[3 + k] + Mc[r * 3 + 2] * B[6 + k]) * ia2[k];
+        for (int k = 0; k < 3; ++k) {
+            const float d = RtM[k * 3] * B[k] + RtM[k * 3 + 1] * B[3 + k] + RtM[k * 3 + 2] * B[6 + k];
+            gs[k] += Real(-d * sig_a3[k]);
+        }
+        float uf[4] = {float(u[0]), float(u[1]), float(u[2]), float(u[3])}, dq[4];
+        quat_rotation_backward<float>(uf, dR, dq);
+        for (int j = 0; j < 4; ++j) gr[j] += Real(dq[j]);
+    } else {
+        for (int k = 0; k < 3; ++k) gp[k] += A16[6 + k];
+        for (int k = 0; k < 4; ++k) gr[k] += A16[9 + k];
+        for (int k = 0; k < 3; ++k) gs[k] += A16[13 + k];
+    }
 
     if (a.visible[i]) {
         Real R[9];

@@ -280,8 +280,62 @@ __device__ __forceinline__ void flush_pairs(const BackwardArgs<Real>& a, const Q
 // ({gid, pixel lane, dpower = alpha dalpha (0 when alpha was clamped), dd =
 // dD w}): dopacity = G dalpha = dpower / opacity, dmean2d / dconic from dpower,
 // the depth chain from dd; segmented by Gaussian, one vector reduction per row.
-__device__ __forceinline__ void flush_records(const BackwardArgs<float>& a, const uint4* rec, int n, int bx, int by,
-                                              const float4* rays, float zoff) {
+// The depth chain of one blended pair (rasterizer_backward.cpp:205-218,
+// geometry.cpp:70-105) as moments: with the unnormalised camera-space ray
+// p~ = ((px-cx)/fx, (py-cy)/fy, 1), a~ = |M R_c2w p~|^2, the midpoint P and
+// s = dd / a~, the reference's adjoint is
+//   dposition = Sigma^-1 R_c2w u,                u = sum s p~
+//   dL/dSigma^-1 = -sum s (P - mu) d~^T  ->  S = R_c2w S_c R_c2w^T,
+//                S_c = -sum s ((P-mu)_c p~^T + p~ (P-mu)_c^T)
+//   drotation = qrb(S R D), dscale_k = -sigma (R^T S R)_kk / a_k^3
+// (Sigma^-1 = R D R^T, D = diag(1 / a^2), a = sigma * scale).  Phase B sums
+// u (3), S_c (6: xx yy zz xy xz yz) and, for pairs that miss the ellipsoid
+// (depth = centre depth), dd (1) per Gaussian; K10 finishes in FP64.  The
+// hit decision is the forward's (same DepthRec forms, same FP64 fallback).
+__device__ __forceinline__ void depth_moments(const BackwardArgs<float>& a, uint32_t g, int xL, int yL, float dx,
+                                              float dy, float u0, float v0, float dd, float (&v)[16]) {
+    const float4* const q4 = reinterpret_cast<const float4*>(a.drec + g);
+    const float4 e0 = q4[0], e1 = q4[1], e2 = q4[2];  // E0..3 | E4 E5 H0 H1 | H2 zc A0 A1
+    const float xx = dx * dx, xy = dx * dy, yy = dy * dy;
+    const float t1 = e0.y * dx, t2 = e0.z * dy, t3 = e0.w * xx, t4 = e1.x * xy, t5 = e1.y * yy;
+    const float disc = ((e0.x + t1) + (t2 + t3)) + (t4 + t5);
+    const float sdisc = ((fabsf(e0.x) + fabsf(t1)) + (fabsf(t2) + fabsf(t3))) + (fabsf(t4) + fabsf(t5));
+    const float w1 = e1.w * dx, w2 = e2.x * dy;
+    const float h = e1.z + w1 + w2;
+    const float sh = fabsf(e1.z) + fabsf(w1) + fabsf(w2);
+    bool hit;
+    if (fabsf(disc) <= 1e-5f * sdisc || fabsf(h) <= 1e-5f * sh) {  // as the forward: FP64 decision
+        double t, aa, bb, ds[3], dep;
+        hit = intersect_fp64<float>(a.cam, a.raw, g, float(xL) + 0.5f, float(yL) + 0.5f, &t, &aa, &bb, ds, &dep);
+    } else {
+        hit = disc >= 0.f && h < 0.f;
+    }
+    if (!hit) {
+        v[15] = dd;
+        return;
+    }
+    const float4 e3 = q4[3], e4 = q4[4], e5 = q4[5];  // A2..5 | K0..3 | K4 K5 ex ey
+    const float at = ((e2.z + e2.w * dx) + (e3.x * dy + e3.y * xx)) + (e3.z * xy + e3.w * yy);
+    const float kq = ((e4.x + e4.y * dx) + (e4.z * dy + e4.w * xx)) + (e5.x * xy + e5.y * yy);
+    const float ra = 1.f / at;
+    const float delta = -kq * ra, t = e2.y + delta;  // t - z_c, t
+    const float s = dd * ra;
+    const float ifx = float(1.0 / a.cam.fx), ify = float(1.0 / a.cam.fy);
+    const float p0x = (u0 - float(a.cam.cx)) * ifx, p0y = (v0 - float(a.cam.cy)) * ify;
+    const float xp = p0x + dx * ifx, yp = p0y + dy * ify;  // p~
+    const float qx = delta * p0x + t * dx * ifx - e5.z, qy = delta * p0y + t * dy * ify - e5.w, qz = delta;
+    v[6] = s * xp;
+    v[7] = s * yp;
+    v[8] = s;
+    v[9] = -2.f * s * qx * xp;
+    v[10] = -2.f * s * qy * yp;
+    v[11] = -2.f * s * qz;
+    v[12] = -s * (qx * yp + qy * xp);
+    v[13] = -s * (qx + qz * xp);
+    v[14] = -s * (qy + qz * yp);
+}
+
+__device__ __forceinline__ void flush_records(const BackwardArgs<float>& a, const uint4* rec, int n, int bx, int by) {
     const int lane = threadIdx.x & 31;
     const bool act = lane < n;
     const uint4 r = act ? rec[lane] : make_uint4(0xffffffffu - lane, 0u, 0u, 0u);  // padding: unique keys
@@ -303,19 +357,21 @@ __device__ __forceinline__ void flush_records(const BackwardArgs<float>& a, cons
         const int L = int(r.y);
         const int xL = bx + (L & 7), yL = by + (L >> 3);
         const float dpower = __uint_as_float(r.z), dd = __uint_as_float(r.w);
-        if (dpower != 0.f) {  // rasterizer_backward.cpp:234-244
+        if (dpower != 0.f || dd != 0.f) {
             const AlphaRec<float>& ar = a.arec[g];
-            const float4 c0 = *reinterpret_cast<const float4*>(&ar.cx);        // cx, cy, ca, cb
-            const float4 c1 = *reinterpret_cast<const float4*>(&ar.cc);        // cc, opacity, log_thr, 1 / opacity
+            const float4 c0 = *reinterpret_cast<const float4*>(&ar.cx);  // cx, cy, ca, cb
             const float dx = float(xL) + 0.5f - c0.x, dy = float(yL) + 0.5f - c0.y;
-            v[0] = dpower * c1.w;
-            v[1] = dpower * (c0.z * dx + c0.w * dy);
-            v[2] = dpower * (c0.w * dx + c1.x * dy);
-            v[3] = dpower * (-0.5f * dx * dx);
-            v[4] = dpower * (-0.5f * dx * dy);
-            v[5] = dpower * (-0.5f * dy * dy);
+            if (dpower != 0.f) {  // rasterizer_backward.cpp:234-244
+                const float4 c1 = *reinterpret_cast<const float4*>(&ar.cc);  // cc, opacity, log_thr, 1 / opacity
+                v[0] = dpower * c1.w;
+                v[1] = dpower * (c0.z * dx + c0.w * dy);
+                v[2] = dpower * (c0.w * dx + c1.x * dy);
+                v[3] = dpower * (-0.5f * dx * dx);
+                v[4] = dpower * (-0.5f * dx * dy);
+                v[5] = dpower * (-0.5f * dy * dy);
+            }
+            if (dd != 0.f) depth_moments(a, g, xL, yL, dx, dy, c0.x, c0.y, dd, v);
         }
-        if (dd != 0.f) depth_chain_adjoint<float>(a, g, cached_ray(rays[L], zoff, xL, yL), dd, v);
     }
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
@@ -949,14 +1005,12 @@ __global__ void __launch_bounds__(32 * kTcWarps, K9A_MINB) backward_kernel_tc(co
 }
 
 // K9 phase B (FP32): one warp per (tile, warp) pair-record segment, the
-// geometric gradients of every blended pair 32 at a time (flush_pairs: the
-// depth chain through the ray-ellipsoid adjoint, dopacity / dmean2d / dconic),
+// geometric terms of every blended pair 32 at a time (flush_records:
+// dopacity / dmean2d / dconic and the depth chain as moments, depth_moments),
 // reduced per Gaussian inside the warp into the acc16 rows.  Split from phase A
 // so that neither carries the other's registers; 5 blocks/SM (48 registers,
 // spills hit the large L1 this kernel leaves) hides its gather latency best.
 __global__ void __launch_bounds__(256, K9B_MINB) backward_pairs_kernel(const __grid_constant__ BackwardArgs<float> a, int nseg) {
-    __shared__ float4 rays[8][32];  // the segment's pixel rays (cached_ray)
-    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int item = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
     if (item >= nseg) return;
     const int seg = a.work_order ? int(a.work_order[item]) : item;
@@ -965,12 +1019,8 @@ __global__ void __launch_bounds__(256, K9B_MINB) backward_pairs_kernel(const __g
     const int tile = seg >> 3, w = seg & 7;
     const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
     const int bx = tx * kTile + (w & 1) * 8, by = ty * kTile + (w >> 1) * 4;
-    const PixelRay<float> r = make_ray<float>(a.cam, bx + (lane & 7), by + (lane >> 3));
-    rays[wib][lane] = ray_cache_entry(r);
-    __syncwarp();
     const uint4* const rec = a.pr + a.pair_off[seg];
-    for (uint32_t k0 = 0; k0 < n; k0 += 32)
-        flush_records(a, rec + k0, int(n - k0 < 32 ? n - k0 : 32), bx, by, rays[wib], r.zoff);
+    for (uint32_t k0 = 0; k0 < n; k0 += 32) flush_records(a, rec + k0, int(n - k0 < 32 ? n - k0 : 32), bx, by);
 }
 
 // ---------------------------------------------------------------------------

@@ -378,7 +378,7 @@ msplat_status size_replay(msplat_replay* r, int dtype, int64_t n, int C, int deg
     if (r->inst_cap == 0) r->inst_cap = std::max<int64_t>(int64_t(1) << 20, 4 * n);
     CUDA_TRY(r->arec.ensure(nn * sizeof(AlphaRec<double>) / 8 * R));
     CUDA_TRY(r->brec.ensure(nn * 32 * R));
-    if (dtype != MSPLAT_F64) CUDA_TRY(r->drec.ensure(nn * sizeof(DepthRec)));
+    if (dtype != MSPLAT_F64) CUDA_TRY(r->drec.ensure(nn * sizeof(DepthRec)));  // (FP32 only)
     CUDA_TRY(r->visible.ensure(nn));
     CUDA_TRY(r->clamped.ensure(nn));
     CUDA_TRY(r->depth_key.ensure(nn * 8));
@@ -664,6 +664,7 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
     a.inst_gauss = r->sorted_gauss;
     a.arec = r->arec.as<AlphaRec<Real>>();
     a.brec = r->brec.as<BlendRec<Real>>();
+    a.drec = sizeof(Real) == 4 ? r->drec.as<DepthRec>() : nullptr;
     a.semantics = static_cast<const Real*>(s->semantics);
     a.raw = RawParams<Real>{static_cast<const Real*>(s->means), static_cast<const Real*>(s->quats),
                             static_cast<const Real*>(s->log_scales), r->rp.sigma_scale};
@@ -789,6 +790,8 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
     // chain_activations is linear per Gaussian, so a multi-view sum is chained
     // once by the caller (msplat_chain_activations) after the last view.
     p.chain = chain && !accumulate;
+    p.depth_moments = sizeof(Real) == 4 && !a.partial;  // the FP32 phase B (backward_pairs_kernel)
+    p.sigma = r->rp.sigma_scale;
     p.err = ctx->d_err;
     ctx->timer.begin(MSPLAT_STAGE_PROJ_BWD, st);
     launch_projection_backward<Real>(p, st);

@@ -125,11 +125,19 @@ struct __align__(16) BlendRec {  // 128 B (FP32): eight 16-byte stores
 // decisions within 1e-5 of the terms' magnitude are re-taken in FP64 exactly
 // as the reference computes them (intersect_fp64).  A degenerate splat
 // (axis < 1e-8) has E = (-1, 0, ...): never a hit.
-struct __align__(16) DepthRec {  // 64 B
+// The backward (phase B) also needs the small offset of the midpoint from the
+// centre: Delta = t - z_c = -(h + z_c a~) / a~ with K = H + z_c A (FP64), and
+// (ex, ey) = camera-space (x, y) of the mean minus z_c p0 (p0 = the centre's
+// normalised image point), so that P - mu in camera space is
+//   (Delta p0x + t dx / fx - ex, Delta p0y + t dy / fy - ey, Delta)
+// without cancellation.  The forward reads the first 64 bytes only.
+struct __align__(16) DepthRec {  // 96 B
     float E[6];
     float H[3];
     float zc;  // camera-z of the centre: the no-hit depth
     float A[6];
+    float K[6];
+    float ex, ey;
 };
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }

@@ -261,6 +261,7 @@ struct BackwardArgs {
     const uint32_t* inst_gauss;
     const AlphaRec<Real>* arec;
     const BlendRec<Real>* brec;
+    const DepthRec* drec;     // FP32 phase B: the depth moments (DepthRec)
     const Real* semantics;
     RawParams<Real> raw;
     const uint4* ev_list;     // the forward's blend-event log (ForwardArgs::ev_list)
@@ -281,7 +282,9 @@ struct BackwardArgs {
     Real* acc_dcolor;  // scratch [n][3]
     // scratch [n][16]: the per-pair geometric sums of K9 in one 64-byte row,
     // [opacity, dmean2, dconic3, dposition3, drotation4, dscale3]; K10 folds
-    // it into the gradient buffer.
+    // it into the gradient buffer.  FP32 phase B (ProjBackwardArgs::
+    // depth_moments) instead keeps the depth chain as camera-space moments
+    // [.., u3, S6, miss] that K10 turns into dposition / drotation / dscale.
     Real* acc16;
     // Deterministic mode (null = atomics): per-(instance, warp) slots of V =
     // 20 + C values [opac, dmean2, dconic3, pos3, rot4, scale3, dcolor3, k, sem C].
@@ -332,6 +335,10 @@ struct ProjBackwardArgs {
     const Real *acc_dcolor, *acc16;
     Real *g_pos, *g_rot, *g_scale, *g_opac, *g_sh, *g_k, *g_sem;
     int chain;  // fuse chain_activations (scene.cpp:108-129); only for single-view buffers
+    // acc16[6..15] holds the FP32 phase B's depth moments (u_c[3], S_c[6]
+    // = xx yy zz xy xz yz, miss sum) instead of dposition / drotation / dscale
+    int depth_moments;
+    double sigma;  // RenderConfig::sigma_scale (axes = sigma * scale)
     DeviceError* err;
 };
 template <typename Real>

@@ -376,10 +376,11 @@ __global__ void __launch_bounds__(kPreThreads, K1_MINB) preprocess_kernel(const 
             DepthRec dr;
             dr.zc = float(z);
             if (amin < kDegenerateScale) {
-                for (int j = 0; j < 6; ++j) dr.E[j] = dr.A[j] = 0.f;
+                for (int j = 0; j < 6; ++j) dr.E[j] = dr.A[j] = dr.K[j] = 0.f;
                 for (int j = 0; j < 3; ++j) dr.H[j] = 0.f;
                 dr.E[0] = -1.f;
                 dr.A[0] = 1.f;
+                dr.ex = dr.ey = 0.f;
             } else {
                 const double u0 = double(float(cxp)), v0 = double(float(cyp));  // the AlphaRec centre
                 const double ifx = 1.0 / c.fx, ify = 1.0 / c.fy;
@@ -411,9 +412,11 @@ __global__ void __launch_bounds__(kPreThreads, K1_MINB) preprocess_kernel(const 
                     dr.A[j] = float(A[j]);
                     dr.E[j] = float(A[j] - W2[j]);
                 }
-                dr.H[0] = float(dot3(vs, m0));
-                dr.H[1] = float(dot3(vs, mx));
-                dr.H[2] = float(dot3(vs, my));
+                const double H[3] = {dot3(vs, m0), dot3(vs, mx), dot3(vs, my)};
+                for (int j = 0; j < 3; ++j) dr.H[j] = float(H[j]);
+                for (int j = 0; j < 6; ++j) dr.K[j] = float((j < 3 ? H[j] : 0.0) + z * A[j]);
+                dr.ex = float(x - z * p0[0]);
+                dr.ey = float(y - z * p0[1]);
             }
             a.drec[i] = dr;
         }
