@@ -600,7 +600,7 @@ namespace {
 
 constexpr int kK9Unroll = K9_UNROLL;
 #ifndef K9B_MINB
-#define K9B_MINB 5  // phase-B CTAs per SM
+#define K9B_MINB 6  // phase-B CTAs per SM (moments: 0.730 ms vs 0.747 at 5, 0.763 at 7)
 #endif
 #ifndef K9_RED2_MT0
 #define K9_RED2_MT0 1  // also the semantic pairs of channel tile 0 (colour / k stay scalar): 2.486 ms vs 2.494
