@@ -230,6 +230,7 @@ struct msplat_replay {
         saved_k, cap_center, cap_conic, cap_depth, cap_radius, cap_rgb, visible_count, ev_list, ev_count, ev_npairs,
         pair_off, pair_n, pair_scan, pair_total, pair_rec, wq_order, wq_scratch, ev_w, tile_cnt, tile_cur, inst_key, big_tiles, key_range;
     bool split_fwd = false;  // the last forward ran split: its weight rows are valid
+    bool brec_written = false;  // K1 wrote the BlendRecs (FP64 or deterministic mode; the FP32 atomic path has no reader)
     int64_t pair_cap = 0;  // pair-record capacity of the FP32 split backward
     uint32_t* sorted_gauss = nullptr;
 
@@ -520,7 +521,8 @@ PreprocessArgs<Real> preprocess_args(msplat_replay* r, const msplat_scene* s, co
     a.visible = r->visible.as<uint8_t>();
     a.clamped_bits = r->clamped.as<uint8_t>();
     a.arec = r->arec.as<AlphaRec<Real>>();
-    a.brec = r->brec.as<BlendRec<Real>>();
+    // the BlendRecs feed the FP64 kernels and the deterministic backward only
+    a.brec = (sizeof(Real) == 8 || r->ctx->deterministic) ? r->brec.as<BlendRec<Real>>() : nullptr;
     a.drec = sizeof(Real) == 4 ? r->drec.as<DepthRec>() : nullptr;
     if (r->capture & 1) {
         a.cap_center = r->cap_center.as<double>();
@@ -540,7 +542,11 @@ msplat_status rasterize_impl(msplat_context* ctx, const msplat_scene* s, const m
     const size_t R = sizeof(Real);
     CUDA_TRY(cudaMemsetAsync(r->visible_count.p, 0, 8, ctx->stream));
     ctx->timer.begin(MSPLAT_STAGE_PREPROCESS, ctx->stream);
-    launch_preprocess<Real>(preprocess_args<Real>(r, s, cfg), ctx->stream);
+    {
+        const PreprocessArgs<Real> pa = preprocess_args<Real>(r, s, cfg);
+        launch_preprocess<Real>(pa, ctx->stream);
+        r->brec_written = pa.brec != nullptr;
+    }
     ctx->timer.end(ctx->stream);
     CUDA_TRY(cudaGetLastError());
     r->binned_explicit = false;
@@ -652,6 +658,18 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
     }
     launch_check_replay<Real>(n, static_cast<const Real*>(s->means), static_cast<const Real*>(s->k),
                               r->saved_means.as<Real>(), r->saved_k.as<Real>(), ctx->d_err, st);
+    if (ctx->deterministic && !r->brec_written && n > 0) {
+        // deterministic mode switched on after an FP32 forward: K1 again for
+        // the BlendRecs (its other outputs are rewritten with the same values)
+        msplat_replay* rw = const_cast<msplat_replay*>(r);
+        msplat_render_config rc{};
+        rc.sigma_scale = r->rp.sigma_scale;
+        CUDA_TRY(cudaMemsetAsync(rw->visible_count.p, 0, 8, st));
+        const PreprocessArgs<Real> pa = preprocess_args<Real>(rw, s, &rc);
+        launch_preprocess<Real>(pa, st);
+        rw->brec_written = true;
+        CUDA_TRY(cudaGetLastError());
+    }
     BackwardArgs<Real> a{};
     a.W = r->W;
     a.H = r->H;

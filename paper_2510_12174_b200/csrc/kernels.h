@@ -62,7 +62,7 @@ struct PreprocessArgs {
     uint8_t* visible;
     uint8_t* clamped_bits;
     AlphaRec<Real>* arec;
-    BlendRec<Real>* brec;
+    BlendRec<Real>* brec;  // null: not written (FP32 atomic path: no reader)
     DepthRec* drec;  // FP32 only (the forward's depth flush); may be null
     double *cap_center, *cap_conic, *cap_depth, *cap_radius, *cap_rgb;  // optional
     unsigned long long* visible_count;

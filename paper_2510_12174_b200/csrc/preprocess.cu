@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(kPreThreads, K1_MINB) preprocess_kernel(const 
     br.k = a.k[i];
     br.hit_ok = Real(amin < kDegenerateScale ? 0 : 1);
     for (int j = 0; j < 4; ++j) br.q[j] = Real(q[j]);
-    a.brec[i] = br;
+    if (a.brec) a.brec[i] = br;
 
     if constexpr (sizeof(Real) == 4) {
         if (a.drec) {  // DepthRec (common.cuh): the forward depth as quadratic forms about the centre

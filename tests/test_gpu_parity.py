@@ -144,6 +144,32 @@ def test_deterministic_backward_is_bitwise_reproducible(port, dtype, tol):
             assert rel_l2_err(runs[0][k], ref[k]) < tol, k
 
 
+def test_deterministic_mode_switched_between_forward_and_backward():
+    """The FP32 forward skips the BlendRecs when no backward of this mode reads
+    them; a deterministic backward after a non-deterministic forward re-runs
+    K1 for them and gives the same bits as an all-deterministic pass."""
+    import torch
+    import paper_2510_12174_b200 as M
+    s = scenes.make_random_scene(3000, 6, 2, seed=78)
+    cam = {"fx": 120.0, "fy": 120.0, "cx": 80.0, "cy": 60.0, "width": 160, "height": 120,
+           "R_c2w": np.eye(3), "t_c2w": np.array([0.0, 0.0, -1.2])}
+    pix = scenes.pixel_grads(cam["width"], cam["height"], s["num_classes"], seed=6, scale=1.0)
+    M.set_deterministic(True)
+    try:
+        scene, view, rc, replay, frame = gpu_forward(s, cam, BG, "float32")
+        want = grads_np(M.rasterize_backward(scene, view, frame, replay, torch_pix(pix, torch.float32)))
+    finally:
+        M.set_deterministic(False)
+    scene, view, rc, replay, frame = gpu_forward(s, cam, BG, "float32")
+    M.set_deterministic(True)
+    try:
+        got = grads_np(M.rasterize_backward(scene, view, frame, replay, torch_pix(pix, torch.float32)))
+    finally:
+        M.set_deterministic(False)
+    for k in GRAD_NAMES:
+        assert np.array_equal(got[k], want[k]), k
+
+
 @pytest.mark.parametrize("dtype,tol", [("float64", 1e-10), ("float32", 1e-4)])
 def test_normals_forward_and_backward(port, dtype, tol):
     import torch
