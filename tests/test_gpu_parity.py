@@ -144,6 +144,58 @@ def test_deterministic_backward_is_bitwise_reproducible(port, dtype, tol):
             assert rel_l2_err(runs[0][k], ref[k]) < tol, k
 
 
+def test_degenerate_axes_fp32(port):
+    """Splats with an axis below kDegenerateScale never intersect
+    (geometry.cpp:37-43): the FP32 depth forms (DepthRec E = (-1, 0..)) give the
+    centre depth in the forward and route the depth gradient to the centre in
+    the backward's moments, as the reference does."""
+    import torch
+    import paper_2510_12174_b200 as M
+    s = scenes.make_random_scene(1500, 4, 1, seed=91)
+    s["log_scales"][::3, 2] = -25.0  # one axis ~1e-11: degenerate
+    cam = {"fx": 120.0, "fy": 120.0, "cx": 80.0, "cy": 60.0, "width": 160, "height": 120,
+           "R_c2w": np.eye(3), "t_c2w": np.array([0.0, 0.0, -1.2])}
+    scene, view, rc, replay, frame = gpu_forward(s, cam, BG, "float32")
+    ref = port.render(s, cam, BG)
+    got = frame_np(frame)
+    same = (got["contributors"] == ref["contributors"]) & (replay.terminus() == ref["terminus"])
+    assert 1.0 - same.mean() < 0.01
+    for k in ("color", "depth", "transmittance"):
+        assert rel_max_err(got[k], ref[k], same) < 1e-4, k
+    pix = scenes.pixel_grads(cam["width"], cam["height"], s["num_classes"], seed=9, scale=1.0)
+    g = grads_np(M.rasterize_backward(scene, view, frame, replay, torch_pix(pix, torch.float32)))
+    rb = port.backward(s, cam, hwc_pix(pix), BG)
+    for k, r in grad_parity(g, rb).items():
+        assert r["max_rel"] <= 1e-3, (k, r)
+
+
+def test_bin_and_sort_beyond_shared_counters():
+    """More tiles than the shared-memory tile counters hold (31,250 > 24,576):
+    the binning falls back to global atomics; lists and order as the reference
+    (rasterizer.cpp:14-45)."""
+    import paper_2510_12174_b200 as M
+    rng = np.random.default_rng(5)
+    W, H, n = 4000, 2000, 3000
+    cx, cy, rad = rng.random(n) * W, rng.random(n) * H, rng.random(n) * 40
+    dep = rng.random(n)
+    splats = [{"center": (float(cx[i]), float(cy[i])), "radius": float(rad[i]), "sort_depth": float(dep[i])}
+              for i in range(n)]
+    rb = M.bin_and_sort(splats, W, H)
+    x0 = np.maximum(0, np.floor(cx - rad)).astype(int) // 16
+    x1 = np.minimum(W - 1, np.floor(cx + rad)).astype(int) // 16
+    y0 = np.maximum(0, np.floor(cy - rad)).astype(int) // 16
+    y1 = np.minimum(H - 1, np.floor(cy + rad)).astype(int) // 16
+    lists = {}
+    for i in np.lexsort((np.arange(n), dep)):
+        for ty in range(y0[i], y1[i] + 1):
+            for tx in range(x0[i], x1[i] + 1):
+                lists.setdefault((tx, ty), []).append(int(i))
+    assert (rb.tiles_x, rb.tiles_y) == (250, 125)
+    for (tx, ty), want in lists.items():
+        assert rb.tile(tx, ty) == want, (tx, ty)
+    assert sum(len(v) for v in lists.values()) == len(rb.values)
+
+
 def test_deterministic_mode_switched_between_forward_and_backward():
     """The FP32 forward skips the BlendRecs when no backward of this mode reads
     them; a deterministic backward after a non-deterministic forward re-runs
