@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kSplit ? 32 * kSplitWarps : kThreads, kSplit ?
     int qn = 0;
     unsigned long long own = 0;  // queue entries owned by this pixel
     uint4* const evl = a.ev_list ? a.ev_list + size_t(8) * range.x + size_t(wq) * len : nullptr;
-    float* const wd = kSplit ? a.ev_w + (size_t(8) * range.x + size_t(wq) * len) * 32 : nullptr;
+    float* const wd = kSplit ? a.ev_w + (size_t(8) * range.x + size_t(wq) * len) * 32 + lane : nullptr;
     uint32_t n_ev = 0, n_pairs = 0;
     if (kSplit && int64_t(size_t(8) * range.x + size_t(wq) * len + len) * 32 > a.ev_w_cap) {
         // a captured replay outgrew the weight rows (sized by the last eager render)
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(kSplit ? 32 * kSplitWarps : kThreads, kSplit ?
                 if (lane == 0) evl[n_ev] = make_uint4(uint32_t(c * 32 + slot), mask, ws->gid[slot], 0u);
                 if constexpr (kSplit) {  // w = alpha T; negated when alpha was clamped at 0.99 (for the backward)
                     const Real w = ae.alpha * T;
-                    wd[size_t(n_ev) * 32 + lane] = ae.pass ? (ae.clamped ? -w : w) : Real(0);
+                    wd[n_ev * 32u] = ae.pass ? (ae.clamped ? -w : w) : Real(0);
                 }
                 ++n_ev;
                 n_pairs += __popc(mask);
