@@ -37,10 +37,18 @@ constexpr int kNtMax = 8;  // semantic n-tiles in registers: C <= 64
 constexpr int kWPitch = 40;    // W tile rows: (k * 40) mod 32 = 8 k, conflict-free A fragments
 constexpr int kSemPitch = 72;  // staged semantic rows: (t * 72) mod 32 = 8 t, conflict-free B fragments
 
-struct PairSmem {
+constexpr int kOutPitch = 36;   // epilogue tile [channel][36]: conflict-free fragment stores and pixel reads
+
+struct PairStage {
     float wt[2][8][kWPitch];      // W^T[8 ev][32 px] tiles (the weight rows as written), double-buffered
-    float srow[2][8][kSemPitch];  // the batch's semantic rows, double-buffered
+    float srow[2][8][kSemPitch];  // the batch's semantic rows (16-byte chunks: the row starts at soff)
     uint32_t gid[2][8];           // the batch's Gaussian ids, double-buffered
+    uint32_t soff[2][8];          // float offset of each semantic row inside its staged chunks
+};
+// The staging buffers, then (after the last batch) the output tile.
+union PairSmem {
+    PairStage st;
+    float out[8 * kNtMax][kOutPitch];
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -57,27 +65,31 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 }
 
 // Issues the cp.async staging of batch b (nb events; ids already in
-// ws->gid[b & 1]): the events' weight rows (16-byte pieces) and semantic rows
-// (8-byte pieces when sem_vec, a lane owning a piece column).  One commit group.
+// ws->st.gid[b & 1]): the events' weight rows (16-byte pieces) and semantic
+// rows (16-byte chunks, four lanes per event).  One commit group.
 __device__ __forceinline__ void stage_batch(const ForwardArgs<float>& a, PairSmem* ws, const float* wrows, int b, int nb,
                                             int lane) {
     const int buf = b & 1;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {  // 8 rows x 8 16-byte pieces
-        const int i = lane + 32 * h, k = i >> 3, q = i & 7;
-        float* const dst = &ws->wt[buf][k][4 * q];
-        if (k < nb) cp_async16(dst, wrows + size_t(8 * b + k) * 32 + 4 * q);
+        const int i = lane + 32 * h, kk = i >> 3, q = i & 7;
+        float* const dst = &ws->st.wt[buf][kk][4 * q];
+        if (kk < nb) cp_async16(dst, wrows + size_t(8 * b + kk) * 32 + 4 * q);
         else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    // semantic rows: the 16-byte chunks covering each row (any 4-byte
+    // alignment; a chunk never straddles a page, so reading whole chunks is
+    // safe), 4 lanes per event, the row's float offset in soff
     const int C = a.C;
-    if (a.sem_vec) {
-        for (int j = lane; j < (C >> 1); j += 32)
-            for (int k = 0; k < nb; ++k)
-                cp_async8(&ws->srow[buf][k][2 * j], a.semantics + size_t(ws->gid[buf][k]) * C + 2 * j);
-    } else {
-        for (int j = lane; j < C; j += 32)
-            for (int k = 0; k < nb; ++k)
-                cp_async4(&ws->srow[buf][k][j], a.semantics + size_t(ws->gid[buf][k]) * C + j);
+    const int k = lane >> 2, part = lane & 3;
+    if (k < nb) {
+        const uintptr_t r0 = reinterpret_cast<uintptr_t>(a.semantics + size_t(ws->st.gid[buf][k]) * C);
+        const uintptr_t c0 = r0 & ~uintptr_t(15);
+        const int nch = int(((r0 + uintptr_t(4 * C) + 15) & ~uintptr_t(15)) - c0) >> 4;
+        if (part == 0) ws->st.soff[buf][k] = uint32_t(r0 - c0) >> 2;
+        const float* src = reinterpret_cast<const float*>(c0) + 4 * part;
+        float* dst = ws->st.srow[buf][k] + 4 * part;
+        for (int q = part; q < nch; q += 4, src += 16, dst += 16) cp_async16(dst, src);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -87,8 +99,8 @@ template <int NT>
 __device__ __forceinline__ void sem_batch(const PairSmem* ws, int buf, float (&acc)[2][NT][4], int C, int nb,
                                           int lane) {
     const int g4 = lane >> 2, t = lane & 3;
-    const float* const w0 = ws->wt[buf][t];      // event t's weights over the 32 pixels
-    const float* const w1 = ws->wt[buf][t + 4];  // event t + 4
+    const float* const w0 = ws->st.wt[buf][t];      // event t's weights over the 32 pixels
+    const float* const w1 = ws->st.wt[buf][t + 4];  // event t + 4
     uint32_t ah[2][4], al[2][4];
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi) {  // A[px][ev]: rows px = 16 mi + g4 (+ 8), cols ev = t (+ 4)
@@ -98,8 +110,8 @@ __device__ __forceinline__ void sem_batch(const PairSmem* ws, int buf, float (&a
         split_tf32(fabsf(w1[r0]), ah[mi][2], al[mi][2]);
         split_tf32(fabsf(w1[r1]), ah[mi][3], al[mi][3]);
     }
-    const float* const s0 = ws->srow[buf][t];
-    const float* const s1 = ws->srow[buf][t + 4];
+    const float* const s0 = ws->st.srow[buf][t] + ws->st.soff[buf][t];
+    const float* const s1 = ws->st.srow[buf][t + 4] + ws->st.soff[buf][t + 4];
     const bool e0 = t < nb, e1 = t + 4 < nb;
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
@@ -163,7 +175,7 @@ __global__ void __launch_bounds__(32 * kSemWarps, K6B_MINB) forward_pairs_kernel
     uint32_t g_next = 0u;  // ids of batch b + 1
     if (nbatch > 0) {
         const uint32_t g0 = fetch_gid(0);
-        if (lane < 8) ws->gid[0][lane] = g0;
+        if (lane < 8) ws->st.gid[0][lane] = g0;
         g_next = fetch_gid(1);
         __syncwarp();
         stage_batch(a, ws, wrows, 0, n_ev < 8 ? n_ev : 8, lane);
@@ -172,7 +184,7 @@ __global__ void __launch_bounds__(32 * kSemWarps, K6B_MINB) forward_pairs_kernel
         const int nb = n_ev - 8 * b < 8 ? n_ev - 8 * b : 8;
         const int buf = b & 1;
         if (b + 1 < nbatch) {  // stage batch b + 1 (its ids arrived during the previous batch)
-            if (lane < 8) ws->gid[buf ^ 1][lane] = g_next;
+            if (lane < 8) ws->st.gid[buf ^ 1][lane] = g_next;
             g_next = fetch_gid(b + 2);
             __syncwarp();
             const int nb1 = n_ev - 8 * (b + 1) < 8 ? n_ev - 8 * (b + 1) : 8;
@@ -186,19 +198,25 @@ __global__ void __launch_bounds__(32 * kSemWarps, K6B_MINB) forward_pairs_kernel
         __syncwarp();  // batch b's buffers are free for batch b + 2
     }
     if (!a.sem_out) return;
-    // straight from the fragments: lane (g4, t) holds rows g4, g4 + 8 x cols 2t, 2t + 1
-    const size_t HW = size_t(a.W) * a.H;
+    // through shared memory: the fragments (lane (g4, t) holds pixel rows g4,
+    // g4 + 8 x channels 2t, 2t + 1) into [channel][pixel], then each lane
+    // writes its own pixel of every channel plane (4 x 32-byte rows per plane)
+    __syncwarp();  // the staging buffers are free
     const int g4 = lane >> 2, t = lane & 3;
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
         for (int j = 0; j < NT; ++j)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int row = mi * 16 + g4 + (q >> 1) * 8, ch = j * 8 + 2 * t + (q & 1);
-                const int px = bx + (row & 7), py = by + (row >> 3);
-                if (ch < C && px < a.W && py < a.H) a.sem_out[size_t(ch) * HW + size_t(py) * a.W + px] = acc[mi][j][q];
-            }
+            for (int q = 0; q < 4; ++q)
+                ws->out[j * 8 + 2 * t + (q & 1)][mi * 16 + g4 + (q >> 1) * 8] = acc[mi][j][q];
+    __syncwarp();
+    const int px = bx + (lane & 7), py = by + (lane >> 3);
+    if (px < a.W && py < a.H) {
+        const size_t HW = size_t(a.W) * a.H;
+        float* dst = a.sem_out + size_t(py) * a.W + px;
+        for (int ch = 0; ch < C; ++ch, dst += HW) *dst = ws->out[ch][lane];
+    }
 }
 
 }  // namespace
