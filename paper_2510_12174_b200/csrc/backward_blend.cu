@@ -619,6 +619,7 @@ struct WarpSmemTC {
     AlphaRec<float> rec[kSub];
     uint32_t gid[32];
     uint32_t emask[32];
+    uint32_t foff[kSub];  // float offset of each staged semantic row inside its 16-byte chunks
     float Tf[32], bgd[32];  // per-pixel T_final and background . dC
     float dDs[32];          // per-pixel dL/ddepth
 };
@@ -649,38 +650,26 @@ size_t backward_tc_smem_bytes(int C) {
 
 // Stages F rows [rgb, k | sem] of n (<= kSub) events into rows of pitch sp:
 // one 16-byte copy of (rgb, k) per row from the AlphaRec (offset 48, the line
-// the sub-batch's records come from) and the semantic row in 8-byte pieces
-// when C is even and the rows are 8-byte aligned (4-byte otherwise).  A lane owns a fixed piece column and
-// walks the rows, so the loop carries no index arithmetic.
+// the sub-batch's records come from) and the semantic row as the whole
+// 16-byte chunks covering it (any 4-byte alignment; a chunk never straddles a
+// page), four lanes per event, landing at row + 4 with the row's own data at
+// row + 4 + foff[e].  The chunks never pass row + sp (4 ceil((C+3)/4) <= K8).
 __device__ __forceinline__ void stage_rows_tc(float* Fb, int sp, const AlphaRec<float>* arec, const float* semantics,
-                                              int C, bool vec, const uint32_t* gid, int n, int lane) {
+                                              int C, uint32_t* foff, const uint32_t* gid, int n, int lane) {
     if (lane < n) {
         const unsigned dst = unsigned(__cvta_generic_to_shared(Fb + lane * sp));
         asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(&arec[gid[lane]].rgb[0]) : "memory");
     }
-    const unsigned base = unsigned(__cvta_generic_to_shared(Fb + 4));
-    if (vec) {
-        for (int j = lane; j < C / 2; j += 32) {
-            const float* const src = semantics + 2 * j;
-#pragma unroll
-            for (int e = 0; e < kSub; ++e) {
-                if (e >= n) break;
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(base + unsigned(4 * (e * sp + 2 * j))),
-                             "l"(src + size_t(gid[e]) * C)
-                             : "memory");
-            }
-        }
-    } else {
-        for (int j = lane; j < C; j += 32) {
-            const float* const src = semantics + j;
-#pragma unroll
-            for (int e = 0; e < kSub; ++e) {
-                if (e >= n) break;
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(base + unsigned(4 * (e * sp + j))),
-                             "l"(src + size_t(gid[e]) * C)
-                             : "memory");
-            }
-        }
+    const int e = lane >> 2, part = lane & 3;
+    if (e < n && C > 0) {
+        const uintptr_t r0 = reinterpret_cast<uintptr_t>(semantics + size_t(gid[e]) * C);
+        const uintptr_t c0 = r0 & ~uintptr_t(15);
+        const int nch = int(((r0 + uintptr_t(4 * C) + 15) & ~uintptr_t(15)) - c0) >> 4;
+        if (part == 0) foff[e] = uint32_t(r0 - c0) >> 2;
+        const char* src = reinterpret_cast<const char*>(c0) + 16 * part;
+        unsigned dst = unsigned(__cvta_generic_to_shared(Fb + e * sp + 4 + 4 * part));
+        for (int q = part; q < nch; q += 4, src += 64, dst += 64)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -724,6 +713,7 @@ __global__ void __launch_bounds__(32 * kTcWarps, K9A_MINB) backward_kernel_tc(co
     bool any = false;
     for (int ch = 0; ch < sp; ++ch) my_seed[ch] = 0.f;
     for (int i = lane; i < tc_stage_floats(C) + kSub * kTilePitch; i += 32) Fb[i] = 0.f;
+    if (lane < kSub) ws->foff[lane] = 0u;
     // Non-finite seeds (an error path): check_finite (scene.cpp:97-106) then
     // names the lowest primitive blending at such a pixel.  They are zeroed
     // for the tensor-core products (0 * inf in another event's column would
@@ -857,14 +847,15 @@ __global__ void __launch_bounds__(32 * kTcWarps, K9A_MINB) backward_kernel_tc(co
                     }
                 }
             }
-            stage_rows_tc(Fb, sp, a.arec, a.semantics, C, a.sem_vec != 0, ws->gid + s0, ns, lane);
+            stage_rows_tc(Fb, sp, a.arec, a.semantics, C, ws->foff, ws->gid + s0, ns, lane);
             if (!kRows && lane < ns) ws->rec[lane] = a.arec[ws->gid[s0 + lane]];
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncwarp();
             // (b) GEMM1: FS[px][e], px on M (two 16-row tiles), events on N.
             float d1[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+            const int fo = int(ws->foff[g4]);  // event g4's semantic channels start at column 4 + fo
             for (int k0 = 0; k0 < K8; k0 += 8) {
-                const float bf[2] = {Fb[g4 * sp + k0 + t4], Fb[g4 * sp + k0 + t4 + 4]};
+                const float bf[2] = {Fb[g4 * sp + k0 + t4 + (k0 ? fo : 0)], Fb[g4 * sp + k0 + t4 + 4 + fo]};
 #pragma unroll
                 for (int mt = 0; mt < 2; ++mt) {
                     const float* A0 = warp_seed + (mt * 16 + g4) * sp + k0 + t4;
