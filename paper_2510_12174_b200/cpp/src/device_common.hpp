@@ -4,6 +4,9 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <malloc.h>
+
+#include <limits>
 
 #include <algorithm>
 #include <chrono>
@@ -62,9 +65,29 @@ inline bool use_fp32() {
     return p && std::string(p) == "32";
 }
 
+// Host allocation reuse.  The reference API hands frames, gradients and the
+// ReplayState's host fields back as fresh std::vectors (~1.5 GB per fwd+bwd
+// call pair at cfg3); glibc serves blocks that large with fresh mmap'd pages,
+// and their first-touch faults dominated the marshalling (FP64 call pair
+// 1.2 s -> 0.4 s with reuse).  Large blocks are therefore kept on the heap and
+// reused (mallopt M_MMAP_MAX = 0, no trimming).  Process-wide:
+// MSPLAT_DROPIN_HOST_REUSE=0 keeps glibc's defaults.
+inline void tune_host_allocator() {
+    static const bool done = [] {
+        const char* e = std::getenv("MSPLAT_DROPIN_HOST_REUSE");
+        if (e && e[0] == '0') return false;
+        mallopt(M_MMAP_MAX, 0);
+        mallopt(M_TRIM_THRESHOLD, std::numeric_limits<int>::max());
+        mallopt(M_TOP_PAD, 64 << 20);
+        return true;
+    }();
+    (void)done;
+}
+
 inline msplat_context* context() {
     thread_local std::unique_ptr<msplat_context, void (*)(msplat_context*)> ctx(nullptr, msplat_context_destroy);
     if (!ctx) {
+        tune_host_allocator();
         const char* d = std::getenv("MSPLAT_DEVICE");
         msplat_context* c = nullptr;
         rethrow(msplat_context_create(d ? std::atoi(d) : 0, nullptr, &c));

@@ -27,14 +27,43 @@ namespace msplat {
 
 using namespace dropin;
 
+// Device replays are pooled per thread: the reference API makes a fresh
+// ReplayState for every forward, and a fresh msplat_replay would allocate and
+// free its device buffers (GBs at cfg3: the event log and the FP32 weight
+// rows) on every call.  A replay goes back to the pool of the thread (and
+// context) that made it, else it is destroyed.
+struct ReplayPool {
+    std::vector<msplat_replay*> free;
+    ~ReplayPool() {
+        for (msplat_replay* r : free) msplat_replay_destroy(r);
+    }
+};
+inline ReplayPool& replay_pool() {
+    thread_local ReplayPool pool;  // constructed after (destroyed before) the thread's context
+    return pool;
+}
+
 struct DeviceReplay {
     msplat_replay* handle = nullptr;
     bool f32 = false;
+    ReplayPool* owner = nullptr;
     explicit DeviceReplay(bool fp32) : f32(fp32) {
-        rethrow(msplat_replay_create(context(), &handle));
+        msplat_context* ctx = context();
+        owner = &replay_pool();
+        if (!owner->free.empty()) {
+            handle = owner->free.back();
+            owner->free.pop_back();
+        } else {
+            rethrow(msplat_replay_create(ctx, &handle));
+        }
         rethrow(msplat_replay_set_capture(handle, 3));
     }
-    ~DeviceReplay() { msplat_replay_destroy(handle); }
+    ~DeviceReplay() {
+        if (owner == &replay_pool() && owner->free.size() < 2)
+            owner->free.push_back(handle);
+        else
+            msplat_replay_destroy(handle);
+    }
 };
 
 PixelGradients PixelGradients::zero(int width, int height, int num_classes) {

@@ -4,6 +4,7 @@
 // per-element functions callers and the reference tests use directly, plus the
 // untiled brute-force renderer.  Each follows the reference function cited
 // (paths relative to /root/reference/proj) in double precision.
+#include "parallel.hpp"
 #include <cmath>
 #include <iostream>
 #include <stdexcept>
@@ -37,13 +38,18 @@ void Scene::validate() const {
     if (sh_degree < 0 || sh_degree > 3) throw std::invalid_argument("Scene: sh_degree must be in [0,3]");
     if (num_classes < 0) throw std::invalid_argument("Scene: num_classes must be >= 0");
     const int ch = sh_coeff_count();
-    for (size_t i = 0; i < gaussians.size(); ++i) {
-        const GaussianPrimitive& g = gaussians[i];
-        if (g.sh.cols() != ch) throw std::invalid_argument("Scene: " + prim(i) + " has wrong SH coefficient count");
-        if (g.semantic_logits.size() != num_classes)
-            throw std::invalid_argument("Scene: " + prim(i) + " has wrong semantic channel count");
-        if (!finite_primitive(g)) throw std::invalid_argument("Scene: " + prim(i) + " has non-finite fields");
-    }
+    // contiguous chunks in parallel; each chunk stops at its first bad
+    // primitive and the lowest chunk's error is re-thrown: the sequential
+    // loop's message
+    dropin::parallel_for(gaussians.size(), [&](size_t b, size_t e) {
+        for (size_t i = b; i < e; ++i) {
+            const GaussianPrimitive& g = gaussians[i];
+            if (g.sh.cols() != ch) throw std::invalid_argument("Scene: " + prim(i) + " has wrong SH coefficient count");
+            if (g.semantic_logits.size() != num_classes)
+                throw std::invalid_argument("Scene: " + prim(i) + " has wrong semantic channel count");
+            if (!finite_primitive(g)) throw std::invalid_argument("Scene: " + prim(i) + " has non-finite fields");
+        }
+    });
 }
 
 // activate -- core/src/scene.cpp:42-60
