@@ -83,7 +83,10 @@ __device__ __forceinline__ bool projection_backward_one(const ProjBackwardArgs<R
     Real go = a.g_opac[i];
     // K9's per-pair sums (acc16 row): opacity, position, rotation, scale
     const Real* A16 = a.acc16 + size_t(i) * 16;
-    go += A16[0];
+    // FP32 phase B (depth_moments): A16[0..2] are the moments sum dpower,
+    // sum dpower dx, sum dpower dy; dopacity = [0] / opacity and dmean2d =
+    // conic . ([1], [2]) below
+    if (!a.depth_moments) go += A16[0];
     if (a.depth_moments) {
         // The FP32 phase B's depth moments (backward_blend.cu depth_moments):
         // dposition = Sigma^-1 R_c2w u + miss * z_cam, dL/dR = S R D,
@@ -202,7 +205,12 @@ __device__ __forceinline__ bool projection_backward_one(const ProjBackwardArgs<R
         dp[0] = dJ[2] * (-fx / z2);
         dp[1] = dJ[5] * (-fy / z2);
         dp[2] = dJ[0] * (-fx / z2) + dJ[4] * (-fy / z2) + dJ[2] * (2 * fx * x / z3) + dJ[5] * (2 * fy * y / z3);
-        const Real dm0 = A16[1], dm1 = A16[2];
+        Real dm0 = A16[1], dm1 = A16[2];
+        if (a.depth_moments) {
+            dm0 = con[0] * A16[1] + con[1] * A16[2];
+            dm1 = con[1] * A16[1] + con[3] * A16[2];
+            go += A16[0] * (Real(1) + exp(-a.opacity_logits[i]));  // / opacity
+        }
         dp[0] += dm0 * fx / z;
         dp[1] += dm1 * fy / z;
         dp[2] += -dm0 * fx * x / z2 - dm1 * fy * y / z2;

@@ -359,13 +359,12 @@ __device__ __forceinline__ void flush_records(const BackwardArgs<float>& a, cons
         const float dpower = __uint_as_float(r.z), dd = __uint_as_float(r.w);
         if (dpower != 0.f || dd != 0.f) {
             const AlphaRec<float>& ar = a.arec[g];
-            const float4 c0 = *reinterpret_cast<const float4*>(&ar.cx);  // cx, cy, ca, cb
+            const float2 c0 = *reinterpret_cast<const float2*>(&ar.cx);  // cx, cy
             const float dx = float(xL) + 0.5f - c0.x, dy = float(yL) + 0.5f - c0.y;
-            if (dpower != 0.f) {  // rasterizer_backward.cpp:234-244
-                const float4 c1 = *reinterpret_cast<const float4*>(&ar.cc);  // cc, opacity, log_thr, 1 / opacity
-                v[0] = dpower * c1.w;
-                v[1] = dpower * (c0.z * dx + c0.w * dy);
-                v[2] = dpower * (c0.w * dx + c1.x * dy);
+            if (dpower != 0.f) {  // rasterizer_backward.cpp:234-244, as moments (K10: / opacity, conic .)
+                v[0] = dpower;
+                v[1] = dpower * dx;
+                v[2] = dpower * dy;
                 v[3] = dpower * (-0.5f * dx * dx);
                 v[4] = dpower * (-0.5f * dx * dy);
                 v[5] = dpower * (-0.5f * dy * dy);
