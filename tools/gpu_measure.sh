@@ -25,6 +25,7 @@ if [ -z "$SKIP_NCU" ]; then
     --log-file $O/launches_bench.csv python bench.py --steps 1 --warmup 3 --repeats 1 --no-cpu-baseline --no-e2e --no-train-step --no-dropin \
     > $O/ncu_bench.log 2>&1; echo "ncu launches exit $?"
   timeout 900 ncu --set full --import-source on --clock-control none \
-    -k regex:"forward_kernel|forward_pairs_kernel|backward_kernel_tc|backward_pairs_kernel|preprocess_kernel|tile_sort_small" \
+    --kernel-name-base function \
+    -k regex:"^(forward_kernel|forward_pairs_kernel|backward_kernel_tc|backward_pairs_kernel|preprocess_kernel|tile_sort_small_kernel)$" \
     --launch-skip 6 --launch-count 6 -o $O/full python tools/profile_render.py --iters 2 > $O/ncu_full.log 2>&1; echo "ncu full exit $?"
 fi
