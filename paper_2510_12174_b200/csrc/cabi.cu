@@ -231,6 +231,7 @@ struct msplat_replay {
         pair_off, pair_n, pair_scan, pair_total, pair_rec, wq_order, wq_scratch, ev_w, tile_cnt, tile_cur, inst_key, big_tiles, key_range;
     bool split_fwd = false;  // the last forward ran split: its weight rows are valid
     bool brec_written = false;  // K1 wrote the BlendRecs (FP64 or deterministic mode; the FP32 atomic path has no reader)
+    bool order_valid = false;   // wq_order holds the last forward's longest-first segment order (reused by the backward)
     int64_t pair_cap = 0;  // pair-record capacity of the FP32 split backward
     uint32_t* sorted_gauss = nullptr;
 
@@ -597,12 +598,15 @@ msplat_status rasterize_impl(msplat_context* ctx, const msplat_scene* s, const m
             launch_forward_split(a, r->tiles_x * r->tiles_y, ctx->stream,
                                  dynamic_schedule() ? r->wq_order.as<uint32_t>() : nullptr, r->wq_scratch.as<uint32_t>());
             r->split_fwd = true;
+            r->order_valid = dynamic_schedule() && a.C > 0;  // the semantic pass ordered the segments
         } else {
             launch_forward<Real>(a, r->tiles_x * r->tiles_y, ctx->stream);
             r->split_fwd = false;
+            r->order_valid = false;
         }
     } else {
         launch_forward<Real>(a, r->tiles_x * r->tiles_y, ctx->stream);
+        r->order_valid = false;
     }
     ctx->timer.end(ctx->stream);
     CUDA_TRY(cudaGetLastError());
@@ -776,7 +780,7 @@ msplat_status backward_impl(msplat_context* ctx, const msplat_scene* s, const ms
                      (reinterpret_cast<uintptr_t>(g->dsemantics) % 8 == 0);
     }
     ctx->timer.begin(MSPLAT_STAGE_BACKWARD, st);
-    if (sizeof(Real) == 4 && !ctx->deterministic && dynamic_schedule())
+    if (sizeof(Real) == 4 && !ctx->deterministic && dynamic_schedule() && !r->order_valid)  // else the forward's
         launch_work_order(r->ev_count.as<uint32_t>(), r->tiles_x * r->tiles_y * 8, r->wq_order.as<uint32_t>(),
                           r->wq_scratch.as<uint32_t>(), st);
     launch_backward_blend<Real>(a, r->tiles_x * r->tiles_y, st);
