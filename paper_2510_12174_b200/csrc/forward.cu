@@ -200,7 +200,9 @@ __device__ __forceinline__ void flush_depth(const ForwardArgs<Real>& a, FwdWarpS
 // tile with 4: the warps never synchronise, so smaller CTAs only change how
 // registers and shared memory are granted per SM.
 constexpr int kSplitWarps = K6_SPLIT_WARPS;
-template <typename Real, bool kSplit>
+// kWsum: the replay records weight sums (capture flag 2; parity checks only) --
+// a compile-time switch keeps its per-event test out of the hot loop.
+template <typename Real, bool kSplit, bool kWsum = true>
 __global__ void __launch_bounds__(kSplit ? 32 * kSplitWarps : kThreads, kSplit ? K6_SPLIT_MINB : 2)
     forward_kernel(const __grid_constant__ ForwardArgs<Real> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -326,7 +328,9 @@ __global__ void __launch_bounds__(kSplit ? 32 * kSplitWarps : kThreads, kSplit ?
                 col1 += w * br.rgb[1];
                 col2 += w * br.rgb[2];
                 kk += w * br.k;
-                if (a.weight_sums) atomicAdd(a.weight_sums + g, w);
+                if constexpr (kWsum) {
+                    if (a.weight_sums) atomicAdd(a.weight_sums + g, w);
+                }
                 const int e = qn + __popc(mask & ((1u << lane) - 1u));
                 own |= 1ull << e;
                 ws->q_lane[e] = uint32_t(lane);
@@ -479,8 +483,14 @@ void launch_forward_blend_split(const ForwardArgs<float>& a, int ntiles, cudaStr
     if (ntiles == 0) return;
     const size_t smem = forward_smem_bytes<float>(0, kSplitWarps);
     static std::atomic<unsigned long long> attr{0};
-    opt_in_smem(reinterpret_cast<const void*>(forward_kernel<float, true>), attr);
-    forward_kernel<float, true><<<ntiles * (8 / kSplitWarps), 32 * kSplitWarps, smem, s>>>(a);
+    static std::atomic<unsigned long long> attr_nw{0};
+    if (a.weight_sums) {
+        opt_in_smem(reinterpret_cast<const void*>(forward_kernel<float, true, true>), attr);
+        forward_kernel<float, true, true><<<ntiles * (8 / kSplitWarps), 32 * kSplitWarps, smem, s>>>(a);
+    } else {
+        opt_in_smem(reinterpret_cast<const void*>(forward_kernel<float, true, false>), attr_nw);
+        forward_kernel<float, true, false><<<ntiles * (8 / kSplitWarps), 32 * kSplitWarps, smem, s>>>(a);
+    }
     count_launches(1);
 }
 
