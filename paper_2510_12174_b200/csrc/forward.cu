@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kSplit ? 32 * kSplitWarps : kThreads, kSplit ?
             if (!done) ae = eval_alpha<Real>(ws->rec[slot], pxf, pyf);
             const unsigned mask = __ballot_sync(0xffffffffu, ae.pass);
             if (mask == 0) continue;
-            if (evl) {  // the backward replays exactly these events
+            if (kSplit || evl) {  // the backward replays exactly these events (always logged when split)
                 if (lane == 0) evl[n_ev] = make_uint4(uint32_t(c * 32 + slot), mask, ws->gid[slot], 0u);
                 if constexpr (kSplit) {  // w = alpha T; negated when alpha was clamped at 0.99 (for the backward)
                     const Real w = ae.alpha * T;
