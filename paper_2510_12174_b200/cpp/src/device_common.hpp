@@ -14,9 +14,11 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <type_traits>
+#include <unordered_map>
 #include <vector>
 
 #include "msplat/normals.hpp"
@@ -58,6 +60,7 @@ struct PhaseTimer {
                      std::chrono::duration<double, std::milli>(n - t).count());
         t = n;
     }
+    ~PhaseTimer() { mark("teardown"); }  // the locals' destructors (device frees) run before this one
 };
 
 inline bool use_fp32() {
@@ -124,20 +127,86 @@ inline void* pinned_staging(size_t bytes, int slot = 0) {
 }
 
 // Device buffer holding host doubles converted to the kernel precision.
+// Device block reuse.  Every reference-API call allocates its device arrays
+// afresh (the same sizes call after call); cudaFree of GB-sized blocks
+// measured 3-550 ms per call on the B200 box, so freed blocks are kept, keyed
+// by their size rounded to 2 MiB, and handed to the next request of that size.
+// Reuse is safe because every eager msplat_* call synchronizes its stream
+// before returning and the drop-in's copies are synchronous.  Capped at
+// MSPLAT_DROPIN_DEVICE_CACHE_MB (default 16384; 0 disables); dropped entirely
+// when a cudaMalloc fails.
+class DeviceBlockCache {
+  public:
+    static DeviceBlockCache& get() {
+        static DeviceBlockCache c;
+        return c;
+    }
+    static size_t rounded(size_t bytes) { return (std::max<size_t>(bytes, 1) + kGrain - 1) / kGrain * kGrain; }
+    void* take(size_t bytes) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            auto it = free_.find(bytes);
+            if (it != free_.end()) {
+                void* p = it->second;
+                free_.erase(it);
+                held_ -= bytes;
+                return p;
+            }
+        }
+        void* p = nullptr;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) {
+            (void)cudaGetLastError();
+            release_all();
+            cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+        }
+        return p;
+    }
+    void give(void* p, size_t bytes) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            if (held_ + bytes <= cap_) {
+                free_.emplace(bytes, p);
+                held_ += bytes;
+                return;
+            }
+        }
+        cudaFree(p);
+    }
+    void release_all() {
+        std::lock_guard<std::mutex> lk(mu_);
+        for (auto& kv : free_) cudaFree(kv.second);
+        free_.clear();
+        held_ = 0;
+    }
+
+  private:
+    static constexpr size_t kGrain = size_t(2) << 20;
+    DeviceBlockCache() {
+        const char* e = std::getenv("MSPLAT_DROPIN_DEVICE_CACHE_MB");
+        cap_ = size_t(e ? std::atoll(e) : 16384) << 20;
+    }
+    ~DeviceBlockCache() = default;  // process exit: the driver reclaims the blocks
+    std::mutex mu_;
+    std::unordered_multimap<size_t, void*> free_;
+    size_t held_ = 0, cap_ = 0;
+};
+
 struct DBuf {
     void* p = nullptr;
     size_t n = 0;
     bool f32 = false;
+    size_t block = 0;  // bytes of the (cached) device block
     DBuf() = default;
     // zero = false: the caller overwrites every element (upload / kernel output).
     DBuf(size_t count, bool fp32, bool zero = true) : n(count), f32(fp32) {
-        cuda_check(cudaMalloc(&p, std::max<size_t>(count, 1) * (fp32 ? 4 : 8)), "cudaMalloc");
+        block = DeviceBlockCache::rounded(count * (fp32 ? 4 : 8));
+        p = DeviceBlockCache::get().take(block);
         if (zero) cuda_check(cudaMemset(p, 0, std::max<size_t>(count, 1) * (fp32 ? 4 : 8)), "cudaMemset");
     }
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
     ~DBuf() {
-        if (p) cudaFree(p);
+        if (p) DeviceBlockCache::get().give(p, block);
     }
     void upload(const std::vector<double>& h) {
         if (h.empty()) return;

@@ -118,9 +118,8 @@ MultimodalFrame rasterize(const Scene& scene, const CameraView& view, const Rend
     pt.mark("scene upload");
     DBuf color(3 * HW, f32, false), depth(HW, f32, false), sem(size_t(C) * HW, f32, false), kmap(HW, f32, false),
         T(HW, f32, false);
-    int32_t* contrib = nullptr;
-    cuda_check(cudaMalloc(&contrib, std::max<size_t>(HW, 1) * 4), "cudaMalloc");
-    std::unique_ptr<int32_t, decltype(&cudaFree)> contrib_guard(contrib, cudaFree);
+    DBuf contrib_buf(HW, true, false);  // int32 per pixel
+    int32_t* contrib = static_cast<int32_t*>(contrib_buf.p);
     msplat_frame fr{color.p, depth.p, C ? sem.p : nullptr, kmap.p, T.p, nullptr, contrib};
     auto dev = replay ? std::make_shared<DeviceReplay>(f32) : nullptr;
     const msplat_scene s = ds.abi();
@@ -261,11 +260,16 @@ GradientBuffer rasterize_backward(const Scene& scene, const CameraView& view, co
     if (replay.num_gaussians != scene.size() || replay.sh_degree != scene.sh_degree ||
         replay.num_classes != scene.num_classes || !replay.device)
         throw std::runtime_error("rasterize_backward: replay state does not match the scene");
-    for (size_t i = 0; i < scene.size(); ++i)
-        if ((replay.activated[i].position.array() != scene.gaussians[i].position.array()).any() ||
-            replay.activated[i].k != scene.gaussians[i].gradient_factor)
-            throw std::runtime_error("rasterize_backward: scene modified since forward (primitive " +
-                                     std::to_string(i) + ")");
+    // check_replay's scan (rasterizer_backward.cpp:40-44) in parallel chunks; the
+    // lowest chunk's exception is rethrown, so the message names the first
+    // modified primitive, as the sequential loop does.
+    parallel_for(scene.size(), [&](size_t b, size_t e) {
+        for (size_t i = b; i < e; ++i)
+            if ((replay.activated[i].position.array() != scene.gaussians[i].position.array()).any() ||
+                replay.activated[i].k != scene.gaussians[i].gradient_factor)
+                throw std::runtime_error("rasterize_backward: scene modified since forward (primitive " +
+                                         std::to_string(i) + ")");
+    }, 1 << 14);
     if (frame.width != view.width || frame.height != view.height)
         throw std::runtime_error("rasterize_backward: frame/view size mismatch");
     const bool ok = pix.dcolor.width() == frame.width && pix.dcolor.height() == frame.height &&

@@ -543,6 +543,48 @@ def test_accumulate_packed(dtype, count, offset):
         M.accumulate_packed(dst, src[:-1] if count > 1 else src.double() if dtype == "float32" else src.float())
 
 
+@pytest.mark.parametrize("deg,C", [(2, 4), (0, 6), (2, 50)])
+def test_fp32_packed_scene_and_gradients_odd_n(port, deg, C):
+    """FP32 fused step (msplat_fwd_bwd) with the scene AND the gradients as views
+    of packed n*P buffers (msplat_param_layout order) at odd n: the semantic
+    blocks start at n*(12 + 3K) floats, only 4-byte aligned.
+    The 16-byte row staging (K6b, phase A) and the vector gradient adds must
+    handle that base; gradients equal the unpacked oracle's."""
+    import torch
+    import paper_2510_12174_b200 as M
+    W, H, n = 96, 64, 4001
+    s = scenes.make_room_scene(n, C, deg, seed=7 + C, width=W, height=H, f=70.0)
+    cam = scenes.view_camera(2, W, H, 70.0)
+    flat = M.pack_scene(M.Scene.from_numpy(s, dtype=torch.float32))
+    off = M.param_layout(n, C, deg)
+    K = (deg + 1) ** 2
+    v = lambda i, *shape: flat[off[i]:off[i + 1]].view(*shape)  # noqa: E731
+    scene = M.Scene(v(0, n, 3), v(1, n, 4), v(2, n, 3), v(3, n), v(5, n, 3, K), v(6, n, C), v(4, n),
+                    num_classes=C, sh_degree=deg)
+    assert scene.semantics.data_ptr() % 8 != 0  # the case under test: a 4-byte aligned semantic base
+    view = M.make_camera(cam["fx"], cam["fy"], cam["cx"], cam["cy"], W, H, cam["R_c2w"], cam["t_c2w"])
+    pix = scenes.pixel_grads(W, H, C, seed=4, scale=1.0)
+    frame = M.MultimodalFrame.empty(W, H, C, torch.float32, "cuda")
+    gflat = torch.zeros(off[-1], dtype=torch.float32, device="cuda")
+    grads = M.GradientBuffer.from_packed(gflat, n, C, deg)
+    assert grads.dsemantics.data_ptr() % 8 != 0
+    M.fwd_bwd(scene, view, M.RenderConfig(**BG), M.NormalConfig(), frame, torch_pix(pix, torch.float32),
+              grads, M.ReplayState())
+    M.rasterizer.check_device_errors()
+    fr, g_ref, _ = port.fwd_bwd(s, cam, hwc_pix(pix), BG)
+    g = grads_np(grads)
+    for k in GRAD_NAMES:
+        if g_ref[k].size:
+            e = rel_l2_err(g[k], g_ref[k])
+            print(f"deg {deg} C {C} {k}: rel L2 {e:.2e}")
+            assert e < 1e-3, k
+    same = frame.contributors.cpu().numpy() == port.render(s, cam, BG)["contributors"]
+    assert same.mean() > 0.99
+    if C:
+        sem = scenes.planar_to_hwc(frame.semantics.double().cpu().numpy())
+        assert rel_max_err(sem, fr["semantics"], np.broadcast_to(same[..., None], sem.shape)) < 1e-4
+
+
 def test_fp32_prune_mask_bit_exact(port):
     """FP32 scenes: the prune mask (trainer.cpp:135-147) and the compaction
     (:150-168) keep exactly the reference's Gaussians -- the reference's test
