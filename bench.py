@@ -655,11 +655,14 @@ def run_e2e(args, rank, world, dev, st, tc, rc, nc):
     """The headline step through the public API with HOST inputs.  Every step's
     pixel gradients (all views) are copied from pinned host memory and the
     step's result (|grad|_1 of the reduced gradient) is read back to the host.
-    The copies are software-pipelined one step ahead over two device buffer
-    sets: while step k renders from set k%2, a copy stream uploads step k+1's
-    inputs into the other set (the first step's inputs are uploaded at the
-    start of the timed region).  Each step is a CUDA graph of public-API calls
-    (ViewShardedStep is capturable); wall-clock timed, max over ranks."""
+    The copies run on a copy stream, software-pipelined over two device buffer
+    sets: while step k renders from set k%2, step k+1's inputs are uploaded
+    into the other set (K steps, K uploads, the first one inside the timed
+    region too).  Each view of a step renders as soon as its own inputs have
+    landed (per-view external events waited on inside the step's CUDA graph),
+    so the link stays busy and the renders trail it.  Each step is a CUDA
+    graph of public-API calls (ViewShardedStep is capturable); wall-clock
+    timed, max over ranks."""
     import torch
     import torch.distributed as dist
 
@@ -679,23 +682,28 @@ def run_e2e(args, rank, world, dev, st, tc, rc, nc):
     result = torch.empty(1, dtype=torch.float32, device=dev)
     res_host = torch.empty(1, dtype=torch.float32).pin_memory()
 
-    def upload(dst, stream):
-        with torch.cuda.stream(stream):
+    # ready[k][j]: view j's inputs in set k have landed.  External events: the
+    # step graphs below contain a wait node per view on them, so a view renders
+    # as soon as its own inputs are on the device -- also across the graph
+    # boundary, while the copy stream keeps the link busy with the next step.
+    ready = [[torch.cuda.Event(external=True) for _ in range(V)] for _ in range(2)]
+
+    def upload(k):
+        """Step inputs into set k on the copy stream (eager, asynchronous)."""
+        with torch.cuda.stream(copy):
             for j in step.issue_order():
                 for f, src in zip(fields, host[j]):
-                    getattr(dst[j], f).copy_(src, non_blocking=True)
+                    getattr(sets[k][j], f).copy_(src, non_blocking=True)
+                ready[k][j].record(copy)
 
-    def body(k):  # render from set k, upload the next step's inputs into set 1 - k
-        main = torch.cuda.current_stream(dev)
-        copy.wait_stream(main)
-        upload(sets[1 - k], copy)
-        step(sets[k])
+    def body(k):  # one step rendering from set k, each view after its inputs' event
+        step(sets[k], before_view=lambda j: torch.cuda.current_stream(dev).wait_event(ready[k][j]))
         torch.sum(gflat[:st["P_total"]].abs(), dim=0, keepdim=True, out=result)
-        main.wait_stream(copy)
 
-    main0 = torch.cuda.current_stream(dev)
-    upload(sets[0], main0)
+    upload(0)
+    upload(1)
     body(0)  # sizes the lanes' replays (eager)
+    body(1)
     torch.cuda.synchronize(dev)
     graphs = None
     if not args.no_graph and world == 1:
@@ -714,26 +722,33 @@ def run_e2e(args, rank, world, dev, st, tc, rc, nc):
             graphs = None
             torch.cuda.synchronize(dev)
 
-    def e2e_step(i):
-        if graphs is not None:
-            graphs[i & 1].replay()
-        else:
-            body(i & 1)
-        res_host.copy_(result)  # device -> host read of the step's result (synchronizing)
-        return float(res_host.item())
+    def run_steps(K):
+        """K steps; step i's inputs are uploaded inside the call: set 0 before
+        the first step, step i + 1's while step i renders (its set was last read
+        by step i - 1, which has completed: its result was read back)."""
+        upload(0)
+        out = 0.0
+        for i in range(K):
+            k = i & 1
+            if graphs is not None:
+                graphs[k].replay()
+            else:
+                body(k)
+            if i + 1 < K:  # queued behind step i's own uploads on the copy stream
+                upload(1 - k)
+            res_host.copy_(result)  # device -> host read of the step's result (synchronizes the step)
+            out = float(res_host.item())
+        return out
 
-    for i in range(max(1, min(args.warmup, 2))):
-        upload(sets[0], main0)
-        e2e_step(0)
+    for _ in range(max(1, min(args.warmup, 2))):
+        run_steps(2)
     vals = []
     for _ in range(max(1, args.repeats)):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
         t = time.perf_counter()
-        upload(sets[0], main0)  # the first step's inputs
-        for i in range(args.steps):
-            e2e_step(i)
+        run_steps(args.steps)
         torch.cuda.synchronize(dev)
         dt = time.perf_counter() - t
         if world > 1:
@@ -744,8 +759,9 @@ def run_e2e(args, rank, world, dev, st, tc, rc, nc):
     return {"value": statistics.median(vals), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": 4, "repeats": [round(v, 3) for v in vals],
             "note": f"public Python API (ViewShardedStep over msplat_fwd_bwd, {args.lanes} lanes); every step's "
-                    "pixel gradients (all views) copied from pinned host memory, software-pipelined one step "
-                    "ahead on a copy stream (first step's upload inside the timed region), |grad|_1 read back "
+                    "pixel gradients (all views) copied from pinned host memory inside the timed region on a copy "
+                    "stream, software-pipelined one step ahead; each view renders once its own inputs have "
+                    "landed (per-view events); |grad|_1 read back "
                     f"every step; steps as CUDA graphs ({'yes' if graphs is not None else 'no, eager'}); wall clock"}
 
 
