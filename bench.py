@@ -768,24 +768,55 @@ def run_e2e(args, rank, world, dev, st, tc, rc, nc):
 def run_e2e_fwd(args, rank, world, dev, head):
     """Forward configs end to end through the public API: every view's
     rendered modalities (colour, depth, normals, semantic logits, k map; the
-    frame's FP32 planes) are copied to pinned host memory on the view's lane
-    stream right after it is rendered, overlapping the next view's render.
-    The inputs of a render are its camera (host struct, a few hundred bytes)
-    and the resident scene, so h2d is 0 tensor bytes.  Wall-clock timed."""
+    frame's FP32 planes) are copied to pinned host memory.  The views render
+    into their own frames (ViewShardedRender(frame_per_view=True), same lanes
+    and scene as `head`), and each view's copy runs on a copy stream as soon as
+    the view is rendered, so the lanes keep rendering while the link drains the
+    finished views; a step ends when its last copy has landed.  The inputs of a
+    render are its camera (host struct, a few hundred bytes) and the resident
+    scene, so h2d is 0 tensor bytes.  Wall-clock timed."""
     import torch
     import torch.distributed as dist
+
+    from paper_2510_12174_b200.distributed import ViewShardedRender
+    e2e_head = ViewShardedRender(head.scene, head.cameras, head.rc, head.nc, lanes=head.lanes,
+                                 frame_per_view=True)
+    e2e_head.replays = head.replays  # the lanes' sized replays
     fields = ("color", "depth", "normals", "semantics", "kmap")
-    f0 = head.frames[0]
+    f0 = e2e_head.frames[0]
+    V = len(head.cameras)
     host = [[torch.empty(getattr(f0, f).shape, dtype=getattr(f0, f).dtype).pin_memory() for f in fields]
-            for _ in range(len(head.cameras))]
-    d2h = sum(t.numel() * t.element_size() for t in host[0]) * len(head.cameras)
+            for _ in range(V)]
+    d2h = sum(t.numel() * t.element_size() for t in host[0]) * V
+    copy = torch.cuda.Stream(dev)
 
-    def after(k, j, frame):
-        for f, dst in zip(fields, host[j]):
-            dst.copy_(getattr(frame, f), non_blocking=True)
+    def after(k, j, frame):  # on the lane's stream, right after view j's render
+        copy.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(copy):
+            for f, dst in zip(fields, host[j]):
+                dst.copy_(getattr(frame, f), non_blocking=True)
 
-    head(after)
+    def run_step():
+        e2e_head(after)
+        torch.cuda.current_stream(dev).wait_stream(copy)
+
+    run_step()  # eager: sizes the replays
     torch.cuda.synchronize(dev)
+    graph = None
+    if not args.no_graph and world == 1:  # eager renders read their counters back, queued behind the copies
+        try:
+            graph = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(dev)
+            cap.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.graph(graph, stream=cap):
+                run_step()
+            torch.cuda.synchronize(dev)
+            graph.replay()
+            torch.cuda.synchronize(dev)
+        except Exception as e:  # noqa: BLE001
+            print(f"# e2e graph capture failed ({e}); eager", file=sys.stderr)
+            graph = None
+            torch.cuda.synchronize(dev)
     vals = []
     for _ in range(max(1, args.repeats)):
         if world > 1:
@@ -793,19 +824,23 @@ def run_e2e_fwd(args, rank, world, dev, head):
         torch.cuda.synchronize(dev)
         t = time.perf_counter()
         for _ in range(args.steps):
-            head(after)
+            if graph is not None:
+                graph.replay()
+            else:
+                run_step()
         torch.cuda.synchronize(dev)
         dt = time.perf_counter() - t
         if world > 1:
             tt = torch.tensor([dt], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             dt = float(tt.item())
-        vals.append(world * len(head.cameras) * args.steps / dt)
+        vals.append(world * V * args.steps / dt)
     return {"value": statistics.median(vals), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(d2h),
             "repeats": [round(v, 3) for v in vals],
-            "note": "public Python API (ViewShardedRender: rasterize + estimate_normals per view, eager launches); "
-                    "every view's colour, depth, normals, semantic logits and k map copied to pinned host "
-                    "memory on its lane stream; wall clock"}
+            "note": "public Python API (ViewShardedRender(frame_per_view=True): rasterize + estimate_normals per "
+                    "view); every view's colour, depth, normals, semantic logits and k map copied to pinned host "
+                    "memory on a copy stream as soon as the view is rendered; steps as CUDA graphs "
+                    f"({'yes' if graph is not None else 'no, eager'}); wall clock"}
 
 
 def relaunch_under_torchrun(args_argv, n):

@@ -234,24 +234,29 @@ class ViewShardedRender:
     (normals.cpp:28-101) per view -- into per-lane frames.  Replicas only: the
     views are independent, so there is no collective.  lanes > 1 issues the
     views interleaved over that many context lanes on their own streams.
-    Asynchronous and CUDA-graph capturable once the replays are sized."""
+    Asynchronous and CUDA-graph capturable once the replays are sized.
+    frame_per_view=True renders every view into its own frame (frames[j])
+    instead of one frame per lane, so a view's frame can still be read out
+    while the lane renders its next view."""
 
-    def __init__(self, scene, cameras, render_cfg, normal_cfg, lanes: int = 1, dtype=None):
+    def __init__(self, scene, cameras, render_cfg, normal_cfg, lanes: int = 1, dtype=None,
+                 frame_per_view: bool = False):
         from . import rasterizer as R
         self.scene, self.cameras, self.rc, self.nc = scene, cameras, render_cfg, normal_cfg
         self.lanes = max(1, min(int(lanes), len(cameras)))
         self.blocks = lane_views(len(cameras), self.lanes)
+        self.frame_per_view = bool(frame_per_view)
         dev = scene.means.device
         W, H = cameras[0].width, cameras[0].height
         self.frames = [R.MultimodalFrame.empty(W, H, scene.num_classes, dtype or scene.dtype, dev)
-                       for _ in range(self.lanes)]
+                       for _ in range(len(cameras) if self.frame_per_view else self.lanes)]
         self.replays = [R.ReplayState(device=dev.index, lane=k) for k in range(self.lanes)]
         self.streams = [None] + [torch.cuda.Stream(dev) for _ in range(1, self.lanes)]
         self.device = dev
 
     def render_view(self, k, j, after=None):
         from . import rasterizer as R
-        f = self.frames[k]
+        f = self.frames[j if self.frame_per_view else k]
         R.rasterize(self.scene, self.cameras[j], self.rc, self.replays[k], out=f)
         R.estimate_normals(f.depth, f.transmittance, self.cameras[j], self.nc, f.normals, lane=k)
         if after is not None:

@@ -1,4 +1,4 @@
-"""Host->device copy bandwidth of the e2e step's upload pattern (per view:
+"""Host->device (and device->host) copy bandwidth of the e2e step's upload pattern (per view:
 dcolor, ddepth, dsemantics, dkmap, dnormals of a 1200x680, C=50 frame; 8
 views) from pinned memory: one copy stream vs the views spread over 2 / 4
 streams, idle GPU vs a concurrent HBM-heavy kernel.  GPU box only.
@@ -39,6 +39,21 @@ def main():
         torch.cuda.synchronize()
         return nbytes / dt / 1e9
 
+    def run_d2h(nstreams):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for j in range(V):
+            with torch.cuda.stream(streams[j % nstreams]):
+                for d, h in zip(dst[j], host[j]):
+                    h.copy_(d, non_blocking=True)
+        for s in streams[:nstreams]:
+            s.synchronize()
+        return nbytes / (time.perf_counter() - t) / 1e9
+
+    for ns in (1, 2):
+        run_d2h(ns)
+        r = sorted(run_d2h(ns) for _ in range(5))
+        print(f"device->host streams={ns}: {r[2]:.1f} GB/s (median of 5)")
     for busy in (False, True):
         for ns in (1, 2, 4):
             run(ns, busy)
