@@ -279,6 +279,41 @@ __device__ __forceinline__ bool projection_backward_one(const ProjBackwardArgs<R
 // instead of each thread striding through its own 108- / 200-byte row.
 constexpr int kK10Threads = 128;
 
+// A CTA's contiguous row range: dst[0, count) = src[0, count) (dst may be null:
+// scan only), returning whether this thread saw a non-finite value.  16-byte
+// vectors when both ends are 16-byte aligned (the packed layouts normally are),
+// scalars otherwise and for the tail.
+template <typename Real>
+__device__ __forceinline__ bool k10_move_scan(const Real* src, Real* dst, int count, bool scan) {
+    constexpr int W = 16 / int(sizeof(Real));
+    bool bad = false;
+    int done = 0;
+    if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+        const int nv = count / W;
+        const uint4* s = reinterpret_cast<const uint4*>(src);
+        uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll 4
+        for (int v = threadIdx.x; v < nv; v += kK10Threads) {
+            const uint4 x = s[v];
+            if (dst) d[v] = x;
+            if (scan) {
+                if constexpr (sizeof(Real) == 4)
+                    bad |= (x.x & 0x7f800000u) == 0x7f800000u || (x.y & 0x7f800000u) == 0x7f800000u ||
+                           (x.z & 0x7f800000u) == 0x7f800000u || (x.w & 0x7f800000u) == 0x7f800000u;
+                else
+                    bad |= (x.y & 0x7ff00000u) == 0x7ff00000u || (x.w & 0x7ff00000u) == 0x7ff00000u;
+            }
+        }
+        done = nv * W;
+    }
+    for (int e = done + int(threadIdx.x); e < count; e += kK10Threads) {
+        const Real v = src[e];
+        if (dst) dst[e] = v;
+        if (scan) bad |= !isfinite(v);
+    }
+    return bad;
+}
+
 template <typename Real>
 size_t k10_smem_bytes(int K) { return size_t(2) * kK10Threads * 3 * K * sizeof(Real); }
 
@@ -293,34 +328,27 @@ __global__ void __launch_bounds__(kK10Threads, K10_MINB) projection_backward_ker
     Real* const s_gsh = s_sh + kK10Threads * RK;
     const int64_t i0 = int64_t(blockIdx.x) * kK10Threads;
     const int nb = int(a.n - i0 < kK10Threads ? a.n - i0 : kK10Threads);
-    {
-        const Real* __restrict__ src = a.sh + size_t(i0) * RK;
-        const Real* __restrict__ gsrc = a.g_sh + size_t(i0) * RK;
-        for (int e = threadIdx.x; e < nb * RK; e += kK10Threads) {
-            s_sh[e] = src[e];
-            s_gsh[e] = gsrc[e];
-        }
-    }
+    k10_move_scan<Real>(a.sh + size_t(i0) * RK, s_sh, nb * RK, false);
+    k10_move_scan<Real>(a.g_sh + size_t(i0) * RK, s_gsh, nb * RK, false);
     __syncthreads();
     const int64_t i = i0 + threadIdx.x;
     bool ok = true;
     if (i < a.n) ok = projection_backward_one<Real>(a, i, s_sh + threadIdx.x * RK, s_gsh + threadIdx.x * RK);
     if (!ok) raise_error_ordered(a.err, kErrNonFiniteGrad, i);
     __syncthreads();
-    // write the SH gradient back; finiteness of the SH and semantic rows
-    int bad = -1;
-    {
-        Real* __restrict__ dst = a.g_sh + size_t(i0) * RK;
-        for (int e = threadIdx.x; e < nb * RK; e += kK10Threads) {
-            const Real v = s_gsh[e];
-            dst[e] = v;
-            if (!isfinite(v) && bad < 0) bad = e / RK;
-        }
+    // write the SH gradient back; finiteness of the SH and semantic rows (a
+    // block-wide vote; the rows are only identified when it fires)
+    bool any = k10_move_scan<Real>(s_gsh, a.g_sh + size_t(i0) * RK, nb * RK, true);
+    if (a.C > 0) any |= k10_move_scan<Real>(a.g_sem + size_t(i0) * a.C, nullptr, nb * a.C, true);
+    if (__syncthreads_or(any)) {
+        int bad = -1;
+        for (int e = threadIdx.x; e < nb * RK; e += kK10Threads)
+            if (!isfinite(s_gsh[e]) && bad < 0) bad = e / RK;
         const Real* __restrict__ gsem = a.g_sem + size_t(i0) * a.C;
         for (int e = threadIdx.x; e < nb * a.C; e += kK10Threads)
             if (!isfinite(gsem[e]) && bad < 0) bad = e / a.C;
+        if (bad >= 0) raise_error_ordered(a.err, kErrNonFiniteGrad, i0 + bad);
     }
-    if (bad >= 0) raise_error_ordered(a.err, kErrNonFiniteGrad, i0 + bad);
 }
 
 
