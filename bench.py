@@ -623,15 +623,17 @@ def run_train_step(args, dev, scene, flat, tc, rc, nc, cams, iters=8, warm=2):
                                  torch.randint(0, C, (H, W), generator=g, device=dev).to(torch.uint8)))
     replay = M.ReplayState()
     lambdas = (1.0, 0.1, 0.1, 0.1, 0.1, 0.1)
+    gflat = torch.empty_like(flat)  # the packed gradient buffer, written in place by the backward
+    gb = M.GradientBuffer.from_packed(gflat, scene.size(), scene.num_classes, scene.sh_degree)
 
     def one(i):
         view = cams[i % len(cams)]
         frame = M.rasterize(scene, view, rc, replay)
         M.estimate_normals(frame.depth, frame.transmittance, view, nc, frame.normals)
         _, pix = M.frame_losses(frame, gts[i % 2], view, nc, lambdas, sync=False)
-        gb = M.rasterize_backward(scene, view, frame, replay, pix)
+        M.rasterize_backward(scene, view, frame, replay, pix, out=gb)
         M.chain_activations(gb, scene)
-        M.adam_step(scene, gb, opt, tc, packed_params=flat, packed_grads=M.rasterizer.pack_grads(gb))
+        M.adam_step(scene, gb, opt, tc, packed_params=flat, packed_grads=gflat)
 
     for i in range(warm):
         one(i)

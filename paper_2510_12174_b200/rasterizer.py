@@ -618,10 +618,24 @@ def save_scene_ply(path: str, scene: Scene) -> None:
 
 
 def rasterize_backward(scene: Scene, view: CameraView, frame: MultimodalFrame, replay: ReplayState,
-                       pix: PixelGradients) -> GradientBuffer:
-    """rasterize_backward (rasterizer_backward.cpp:127-264); activated space."""
+                       pix: PixelGradients, out: GradientBuffer | None = None) -> GradientBuffer:
+    """rasterize_backward (rasterizer_backward.cpp:127-264); activated space.
+    The library zeroes the gradient arrays before accumulating, so the result
+    is a fresh buffer's; `out` (e.g. GradientBuffer.from_packed views of the
+    optimizer's packed gradient buffer) is written in place instead of a new
+    allocation."""
     ctx = _Context.get(scene.means.device.index, replay.lane)
-    grads = GradientBuffer.zeros_like_scene(scene)
+    if out is None:
+        grads = GradientBuffer(*(torch.empty_like(t) for t in (
+            scene.means, scene.quats, scene.log_scales, scene.opacity_logits, scene.sh,
+            scene.semantics, scene.k)))
+    else:
+        want = (scene.means, scene.quats, scene.log_scales, scene.opacity_logits, scene.sh, scene.semantics, scene.k)
+        have = (out.dposition, out.drotation, out.dscale, out.dopacity, out.dsh, out.dsemantics, out.dk)
+        if any(h.shape != w.shape or h.dtype != w.dtype or h.device != w.device for h, w in zip(have, want)):
+            raise ValueError("rasterize_backward: out does not match the scene")
+        grads = out
+        grads.raw_space = False
     for t in (pix.dcolor, pix.ddepth, pix.dsemantics, pix.dkmap):
         if t.dtype != scene.dtype or not t.is_contiguous():
             raise RuntimeError("rasterize_backward: pixel-gradient shape mismatch")

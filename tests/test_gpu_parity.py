@@ -758,3 +758,29 @@ def test_view_sharded_render_matches_single_renders(port, frame_per_view):
         assert rel_max_err(scenes.planar_to_hwc(got[j].cpu().numpy()), ref["color"]) < 1e-10, j
         if frame_per_view:
             assert rel_max_err(scenes.planar_to_hwc(head.frames[j].color.cpu().numpy()), ref["color"]) < 1e-10
+
+
+def test_rasterize_backward_into_packed_out(port):
+    """rasterize_backward(out=GradientBuffer.from_packed(...)) writes the same
+    gradients as a fresh buffer into the packed views (stale contents are
+    overwritten: the library zeroes before accumulating), and rejects an out
+    buffer of the wrong shape."""
+    import torch
+    import paper_2510_12174_b200 as M
+    s, cam = CASES[1]
+    scene, view, rc, replay, frame = gpu_forward(s, cam, BG, "float32")
+    pix = torch_pix(scenes.pixel_grads(cam["width"], cam["height"], s["num_classes"], seed=9, scale=1.0),
+                    torch.float32)
+    fresh = grads_np(M.rasterize_backward(scene, view, frame, replay, pix))
+    n, C, deg = scene.size(), scene.num_classes, scene.sh_degree
+    gflat = torch.full((M.param_layout(n, C, deg)[-1],), 7.0, device="cuda")  # stale
+    out = M.GradientBuffer.from_packed(gflat, n, C, deg)
+    out.raw_space = True
+    got = M.rasterize_backward(scene, view, frame, replay, pix, out=out)
+    assert got is out and not out.raw_space
+    g = grads_np(out)
+    for k in GRAD_NAMES:
+        assert np.array_equal(g[k], fresh[k]) or rel_l2_err(g[k], fresh[k]) < 1e-6, k
+    bad = M.GradientBuffer.from_packed(torch.zeros(M.param_layout(n - 1, C, deg)[-1], device="cuda"), n - 1, C, deg)
+    with pytest.raises(ValueError):
+        M.rasterize_backward(scene, view, frame, replay, pix, out=bad)
