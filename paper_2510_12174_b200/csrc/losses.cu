@@ -10,9 +10,10 @@
 //                          double accumulators (sums and masked counts);
 //   2. ssim_fwd_kernel     per valid window centre and channel: the five
 //                          windowed moments, SSIM and its three moment
-//                          adjoints (losses.cpp:120-146);
+//                          adjoints (losses.cpp:120-146); 32 x 8 tiles, the
+//                          horizontal 11-tap sums shared through shared memory;
 //   3. ssim_bwd_kernel     per pixel: the adjoint of the valid correlation
-//                          (losses.cpp:61-83, 148-156);
+//                          (losses.cpp:61-83, 148-156), tiled the same way;
 //   4. combine_kernel      one thread: the values, magnitude ratios and seed
 //                          scales of combine() (losses.cpp:285-313);
 //   5. assemble_kernel     per pixel: the seeded pixel gradients
@@ -108,88 +109,137 @@ __global__ void __launch_bounds__(kThreadsL) loss_pixel_kernel(const __grid_cons
     block_accumulate<8>(v, a.acc);
 }
 
-// Windowed moments of one valid window (separable order of losses.cpp:39-58:
-// along x first, then along y).
+// SSIM tiles: a CTA covers kSsimTX x kSsimTY outputs of one channel (blockIdx.y).
+// The 11-tap horizontal sums of the tile's rows are computed once into shared
+// memory and shared by the 11 vertical taps of each output, with every output
+// summed in the reference's order (losses.cpp:39-58: along x, i = 0..10, then
+// along y, j = 0..10) -- the same operations as one output at a time.
+constexpr int kSsimTX = 32, kSsimTY = 8, kSsimRows = kSsimTY + 10, kSsimCols = kSsimTX + 10;
+static_assert(kSsimTX * kSsimTY == kThreadsL, "one output per thread");
+
+__host__ __device__ inline int ssim_tiles_x(int w) { return (w + kSsimTX - 1) / kSsimTX; }
+__host__ __device__ inline int ssim_tiles_y(int h) { return (h + kSsimTY - 1) / kSsimTY; }
+
+// Windowed moments of the valid windows (vx, vy) in [0, W - 10) x [0, H - 10)
+// (window rows vy..vy+10, columns vx..vx+10).
 template <typename Real>
 __global__ void __launch_bounds__(kThreadsL) ssim_fwd_kernel(const __grid_constant__ LossArgs<Real> a) {
+    __shared__ Real sx[kSsimRows][kSsimCols], sy[kSsimRows][kSsimCols];
+    __shared__ Real hs[5][kSsimRows][kSsimTX];
     const int W = a.W, H = a.H, Wv = W - 10, Hv = H - 10;
     const size_t HW = size_t(W) * H, nv = size_t(Wv) * Hv;
+    const int c = blockIdx.y;
+    const int tiles_x = ssim_tiles_x(Wv);
+    const int bx = int(blockIdx.x % unsigned(tiles_x)) * kSsimTX, by = int(blockIdx.x / unsigned(tiles_x)) * kSsimTY;
+    const Real* X = a.color + c * HW;
+    const Real* Y = a.gt_rgb + c * HW;
+    for (int e = threadIdx.x; e < kSsimRows * kSsimCols; e += kThreadsL) {
+        const int r = e / kSsimCols, q = e - r * kSsimCols, gy = by + r, gx = bx + q;
+        const bool in = gy < H && gx < W;
+        sx[r][q] = in ? X[size_t(gy) * W + gx] : Real(0);
+        sy[r][q] = in ? Y[size_t(gy) * W + gx] : Real(0);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kSsimRows * kSsimTX; e += kThreadsL) {
+        const int r = e / kSsimTX, q = e - r * kSsimTX;
+        Real hx = 0, hy = 0, hx2 = 0, hy2 = 0, hxy = 0;
+        for (int i = 0; i < 11; ++i) {
+            const Real wi = Real(a.ssim_w[i]);
+            const Real x = sx[r][q + i], y = sy[r][q + i];
+            hx += wi * x;
+            hy += wi * y;
+            hx2 += wi * (x * x);
+            hy2 += wi * (y * y);
+            hxy += wi * (x * y);
+        }
+        hs[0][r][q] = hx;
+        hs[1][r][q] = hy;
+        hs[2][r][q] = hx2;
+        hs[3][r][q] = hy2;
+        hs[4][r][q] = hxy;
+    }
+    __syncthreads();
+    const int tx = threadIdx.x % kSsimTX, ty = threadIdx.x / kSsimTX;
+    const int vx = bx + tx, vy = by + ty;
     double ssum = 0;
-    for (size_t idx = size_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < 3 * nv;
-         idx += size_t(gridDim.x) * blockDim.x) {
-        const int c = int(idx / nv);
-        const size_t r = idx - size_t(c) * nv;
-        const int vy = int(r / Wv), vx = int(r - size_t(vy) * Wv);
-        const Real* X = a.color + c * HW;
-        const Real* Y = a.gt_rgb + c * HW;
+    if (vx < Wv && vy < Hv) {
         Real mx = 0, my = 0, ex2 = 0, ey2 = 0, exy = 0;
         for (int j = 0; j < 11; ++j) {
-            const size_t row = size_t(vy + j) * W + vx;
-            Real hx = 0, hy = 0, hx2 = 0, hy2 = 0, hxy = 0;
-            for (int i = 0; i < 11; ++i) {
-                const Real wi = Real(a.ssim_w[i]);
-                const Real x = X[row + i], y = Y[row + i];
-                hx += wi * x;
-                hy += wi * y;
-                hx2 += wi * (x * x);
-                hy2 += wi * (y * y);
-                hxy += wi * (x * y);
-            }
             const Real wj = Real(a.ssim_w[j]);
-            mx += wj * hx;
-            my += wj * hy;
-            ex2 += wj * hx2;
-            ey2 += wj * hy2;
-            exy += wj * hxy;
+            mx += wj * hs[0][ty + j][tx];
+            my += wj * hs[1][ty + j][tx];
+            ex2 += wj * hs[2][ty + j][tx];
+            ey2 += wj * hs[3][ty + j][tx];
+            exy += wj * hs[4][ty + j][tx];
         }
         const Real C1 = Real(0.01 * 0.01), C2 = Real(0.03 * 0.03);
-        const Real sx = ex2 - mx * mx, sy = ey2 - my * my, sxy = exy - mx * my;
+        const Real vxx = ex2 - mx * mx, vyy = ey2 - my * my, sxy = exy - mx * my;
         const Real a1 = Real(2) * mx * my + C1, a2 = Real(2) * sxy + C2;
-        const Real b1 = mx * mx + my * my + C1, b2 = sx + sy + C2;
-        const Real s = (a1 * a2) / (b1 * b2);
-        ssum += double(s);
-        if (!a.ssim_maps) continue;  // metric only
-        const Real dS = -Real(a.ssim_inv_count);
-        Real* G = a.ssim_maps + size_t(c) * nv + r;  // [3 maps][3 ch][nv]
-        G[0] = dS * (Real(2) * my * (a2 - a1) / (b1 * b2) - Real(2) * mx * s * (Real(1) / b1 - Real(1) / b2));
-        G[3 * nv] = dS * (-s / b2);
-        G[6 * nv] = dS * (Real(2) * a1 / (b1 * b2));
+        const Real b1 = mx * mx + my * my + C1, b2 = vxx + vyy + C2;
+        const Real sv = (a1 * a2) / (b1 * b2);
+        ssum = double(sv);
+        if (a.ssim_maps) {
+            const Real dS = -Real(a.ssim_inv_count);
+            Real* G = a.ssim_maps + size_t(c) * nv + size_t(vy) * Wv + vx;  // [3 maps][3 ch][nv]
+            G[0] = dS * (Real(2) * my * (a2 - a1) / (b1 * b2) - Real(2) * mx * sv * (Real(1) / b1 - Real(1) / b2));
+            G[3 * nv] = dS * (-sv / b2);
+            G[6 * nv] = dS * (Real(2) * a1 / (b1 * b2));
+        }
     }
     double v[1] = {ssum};
     block_accumulate<1>(v, a.acc + 1);
 }
 
+// The adjoint of the valid correlation per pixel (p = (px, py)): the maps G at
+// windows (px - i, py - j), i, j in 0..10 and inside the valid range, weighted
+// by w_i w_j -- zero-padded outside, which adds exact zeros.
 template <typename Real>
 __global__ void __launch_bounds__(kThreadsL) ssim_bwd_kernel(const __grid_constant__ LossArgs<Real> a) {
+    __shared__ Real sg[3][kSsimRows][kSsimCols];
+    __shared__ Real hs[3][kSsimRows][kSsimTX];
     const int W = a.W, H = a.H, Wv = W - 10, Hv = H - 10;
     const size_t HW = size_t(W) * H, nv = size_t(Wv) * Hv;
-    for (size_t idx = size_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < 3 * HW;
-         idx += size_t(gridDim.x) * blockDim.x) {
-        const int c = int(idx / HW);
-        const size_t p = idx - size_t(c) * HW;
-        const int py = int(p / W), px = int(p - size_t(py) * W);
-        const Real* G = a.ssim_maps + size_t(c) * nv;
-        Real bm = 0, b2 = 0, bxy = 0;
-        const int j0 = py - (Hv - 1) > 0 ? py - (Hv - 1) : 0, j1 = py < 10 ? py : 10;
-        const int i0 = px - (Wv - 1) > 0 ? px - (Wv - 1) : 0, i1 = px < 10 ? px : 10;
-        for (int j = j0; j <= j1; ++j) {
-            const size_t row = size_t(py - j) * Wv;
-            Real hm = 0, h2 = 0, hxy = 0;
-            for (int i = i0; i <= i1; ++i) {
-                const Real wi = Real(a.ssim_w[i]);
-                const size_t o = row + (px - i);
-                hm += wi * G[o];
-                h2 += wi * G[3 * nv + o];
-                hxy += wi * G[6 * nv + o];
-            }
-            const Real wj = Real(a.ssim_w[j]);
-            bm += wj * hm;
-            b2 += wj * h2;
-            bxy += wj * hxy;
-        }
-        const Real x = a.color[idx], y = a.gt_rgb[idx];
-        a.ssim_grad[idx] = bm + Real(2) * x * b2 + y * bxy;
+    const int c = blockIdx.y;
+    const int tiles_x = ssim_tiles_x(W);
+    const int bx = int(blockIdx.x % unsigned(tiles_x)) * kSsimTX, by = int(blockIdx.x / unsigned(tiles_x)) * kSsimTY;
+    const Real* G = a.ssim_maps + size_t(c) * nv;
+    // sg[m][r][q] = map m at window (bx - 10 + q, by - 10 + r)
+    for (int e = threadIdx.x; e < kSsimRows * kSsimCols; e += kThreadsL) {
+        const int r = e / kSsimCols, q = e - r * kSsimCols, wy = by - 10 + r, wx = bx - 10 + q;
+        const bool in = wy >= 0 && wy < Hv && wx >= 0 && wx < Wv;
+        const size_t o = in ? size_t(wy) * Wv + wx : 0;
+        sg[0][r][q] = in ? G[o] : Real(0);
+        sg[1][r][q] = in ? G[3 * nv + o] : Real(0);
+        sg[2][r][q] = in ? G[6 * nv + o] : Real(0);
     }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kSsimRows * kSsimTX; e += kThreadsL) {
+        const int r = e / kSsimTX, q = e - r * kSsimTX;
+        Real hm = 0, h2 = 0, hxy = 0;
+        for (int i = 0; i < 11; ++i) {  // window column px - i = bx + q - i -> sg column q + 10 - i
+            const Real wi = Real(a.ssim_w[i]);
+            hm += wi * sg[0][r][q + 10 - i];
+            h2 += wi * sg[1][r][q + 10 - i];
+            hxy += wi * sg[2][r][q + 10 - i];
+        }
+        hs[0][r][q] = hm;
+        hs[1][r][q] = h2;
+        hs[2][r][q] = hxy;
+    }
+    __syncthreads();
+    const int tx = threadIdx.x % kSsimTX, ty = threadIdx.x / kSsimTX;
+    const int px = bx + tx, py = by + ty;
+    if (px >= W || py >= H) return;
+    Real bm = 0, b2 = 0, bxy = 0;
+    for (int j = 0; j < 11; ++j) {  // window row py - j -> hs row ty + 10 - j
+        const Real wj = Real(a.ssim_w[j]);
+        bm += wj * hs[0][ty + 10 - j][tx];
+        b2 += wj * hs[1][ty + 10 - j][tx];
+        bxy += wj * hs[2][ty + 10 - j][tx];
+    }
+    const size_t idx = size_t(c) * HW + size_t(py) * W + px;
+    const Real x = a.color[idx], y = a.gt_rgb[idx];
+    a.ssim_grad[idx] = bm + Real(2) * x * b2 + y * bxy;
 }
 
 // combine() (losses.cpp:285-313) on the reduced sums.
@@ -339,9 +389,8 @@ void launch_frame_losses(const LossArgs<Real>& a, cudaStream_t s) {
     loss_pixel_kernel<Real><<<grid_for(HW), kThreadsL, 0, s>>>(a);
     count_launches(1);
     if (a.en[1]) {
-        const size_t nv = size_t(a.W - 10) * (a.H - 10);
-        ssim_fwd_kernel<Real><<<grid_for(3 * nv), kThreadsL, 0, s>>>(a);
-        ssim_bwd_kernel<Real><<<grid_for(3 * HW), kThreadsL, 0, s>>>(a);
+        ssim_fwd_kernel<Real><<<dim3(unsigned(ssim_tiles_x(a.W - 10) * ssim_tiles_y(a.H - 10)), 3), kThreadsL, 0, s>>>(a);
+        ssim_bwd_kernel<Real><<<dim3(unsigned(ssim_tiles_x(a.W) * ssim_tiles_y(a.H)), 3), kThreadsL, 0, s>>>(a);
         count_launches(2);
     }
     combine_kernel<Real><<<1, 1, 0, s>>>(a);
@@ -364,8 +413,7 @@ void launch_frame_metrics(const MetricArgs<Real>& a, cudaStream_t s) {
         l.color = a.color;
         l.gt_rgb = a.gt_rgb;
         l.acc = a.acc + 7;  // ssim sum lands in acc[8]
-        const size_t nv = size_t(a.W - 10) * (a.H - 10);
-        ssim_fwd_kernel<Real><<<grid_for(3 * nv), kThreadsL, 0, s>>>(l);
+        ssim_fwd_kernel<Real><<<dim3(unsigned(ssim_tiles_x(a.W - 10) * ssim_tiles_y(a.H - 10)), 3), kThreadsL, 0, s>>>(l);
         count_launches(1);
     }
 }
