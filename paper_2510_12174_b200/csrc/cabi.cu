@@ -202,7 +202,7 @@ struct msplat_context {
     // scratch owned by the context (shared by calls on its stream)
     DevBuf acc_dcolor, acc16, ddepth_total, normal_dv, kept;
     // frame losses (msplat_frame_losses)
-    DevBuf loss_acc, loss_report, ssim_maps, ssim_grad, loss_dN;
+    DevBuf loss_acc, loss_report, ssim_maps, ssim_grad, loss_dN, loss_ce;
     DevBuf metric_acc, metric_hist;
     // trainer support (msplat_init_scene, msplat_prune_compact)
     DevBuf init_pts, init_cols, init_logs, cmp_k32, cmp_idx, cmp_tiles, cmp_total;
@@ -877,6 +877,10 @@ msplat_status frame_losses_impl(msplat_context* ctx, int C, const Cam& cam, cons
         CUDA_TRY(ctx->loss_dN.ensure(3 * HW * R));
         a.dN = ctx->loss_dN.as<Real>();
     }
+    if (a.en[4] && C > 0) {
+        CUDA_TRY(ctx->loss_ce.ensure(2 * HW * R));
+        a.ce_stats = ctx->loss_ce.as<Real>();
+    }
     a.err = ctx->d_err;
     launch_frame_losses<Real>(a, ctx->stream);
     CUDA_TRY(cudaGetLastError());
@@ -921,7 +925,7 @@ void msplat_context_destroy(msplat_context* ctx) {
     CTX_DEVICE_GUARD(ctx);
     if (!ctx) return;
     cudaStreamSynchronize(ctx->stream);
-    for (DevBuf* b : {&ctx->acc_dcolor, &ctx->acc16, &ctx->loss_acc, &ctx->loss_report, &ctx->metric_acc, &ctx->metric_hist, &ctx->ssim_maps, &ctx->ssim_grad, &ctx->loss_dN, &ctx->init_pts,
+    for (DevBuf* b : {&ctx->acc_dcolor, &ctx->acc16, &ctx->loss_acc, &ctx->loss_report, &ctx->metric_acc, &ctx->metric_hist, &ctx->ssim_maps, &ctx->ssim_grad, &ctx->loss_dN, &ctx->loss_ce, &ctx->init_pts,
                        &ctx->init_cols, &ctx->init_logs, &ctx->cmp_k32, &ctx->cmp_idx, &ctx->cmp_tiles, &ctx->cmp_total,
                        &ctx->ddepth_total, &ctx->normal_dv, &ctx->kept, &ctx->det_partial, &ctx->det_keys,
                        &ctx->det_keys_alt, &ctx->det_vals, &ctx->det_vals_alt, &ctx->det_range})

@@ -184,6 +184,7 @@ struct LossArgs {
     double* report;     // [20] msplat_loss_report + 2 counts
     Real* ssim_maps;    // [3 maps][3][Hv][Wv]
     Real* ssim_grad;    // [3][H][W]
+    Real* ce_stats;     // [2][H][W] per-pixel softmax max and normaliser (loss_pixel -> assemble)
     Real *dcolor, *ddepth, *dsem, *dkmap, *dN;  // outputs (dN: seeded normal-loss gradient)
     DeviceError* err;
 };

@@ -71,11 +71,12 @@ __device__ __forceinline__ bool normal_supervised(const LossArgs<Real>& a, size_
 // Softmax cross-entropy of one pixel; writes the probability normaliser.
 template <typename Real>
 __device__ __forceinline__ Real ce_pixel(const LossArgs<Real>& a, size_t p, size_t HW, int label, Real& maxl, Real& z) {
-    maxl = a.sem[p];
-    for (int c = 1; c < a.C; ++c) maxl = a.sem[size_t(c) * HW + p] > maxl ? a.sem[size_t(c) * HW + p] : maxl;
+    const Real* __restrict__ sem = a.sem + p;
+    maxl = sem[0];
+    for (int c = 1; c < a.C; ++c) maxl = sem[size_t(c) * HW] > maxl ? sem[size_t(c) * HW] : maxl;
     z = Real(0);
-    for (int c = 0; c < a.C; ++c) z += exp(a.sem[size_t(c) * HW + p] - maxl);
-    return log(z) - (a.sem[size_t(label) * HW + p] - maxl);
+    for (int c = 0; c < a.C; ++c) z += exp(sem[size_t(c) * HW] - maxl);
+    return log(z) - (sem[size_t(label) * HW] - maxl);
 }
 
 // acc: 0 l1 sum, 1 ssim sum, 2 depth sum, 3 depth count, 4 normal dot sum,
@@ -102,6 +103,10 @@ __global__ void __launch_bounds__(kThreadsL) loss_pixel_kernel(const __grid_cons
             } else {
                 Real maxl, z;
                 v[6] += double(ce_pixel(a, p, HW, label, maxl, z));
+                if (a.ce_stats) {  // the seed assembly's softmax reuses them
+                    a.ce_stats[p] = maxl;
+                    a.ce_stats[HW + p] = z;
+                }
             }
         }
         if (a.en[5]) v[7] += double(fabs(a.kmap[p] - Real(1)));
@@ -307,10 +312,30 @@ __global__ void __launch_bounds__(kThreadsL) assemble_kernel(const __grid_consta
             const int label = a.en[4] ? int(a.labels[p]) : 0;
             if (a.en[4] && seed_seg != Real(0) && label < a.C) {
                 Real maxl, z;
-                ce_pixel(a, p, HW, label, maxl, z);
-                for (int c = 0; c < a.C; ++c) {
-                    const Real pc = exp(a.sem[size_t(c) * HW + p] - maxl) / z;
-                    a.dsem[size_t(c) * HW + p] = seed_seg * ((pc - (c == label ? Real(1) : Real(0))) * inv_hw);
+                if (a.ce_stats) {
+                    maxl = a.ce_stats[p];
+                    z = a.ce_stats[HW + p];
+                } else {
+                    ce_pixel(a, p, HW, label, maxl, z);
+                }
+                // logits in batches of 8 loads ahead of their stores (the output
+                // does not alias the frame's logits)
+                const Real* __restrict__ sem = a.sem + p;
+                Real* __restrict__ dsem = a.dsem + p;
+                int c = 0;
+                for (; c + 8 <= a.C; c += 8) {
+                    Real l[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) l[k] = sem[size_t(c + k) * HW];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const Real pc = exp(l[k] - maxl) / z;
+                        dsem[size_t(c + k) * HW] = seed_seg * ((pc - (c + k == label ? Real(1) : Real(0))) * inv_hw);
+                    }
+                }
+                for (; c < a.C; ++c) {
+                    const Real pc = exp(sem[size_t(c) * HW] - maxl) / z;
+                    dsem[size_t(c) * HW] = seed_seg * ((pc - (c == label ? Real(1) : Real(0))) * inv_hw);
                 }
             } else {
                 for (int c = 0; c < a.C; ++c) a.dsem[size_t(c) * HW + p] = Real(0);
